@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the per-mini-batch GNN training step (BASELINE.json metric: mini-batches/s
+and epoch time, GraphSAGE on a products-shaped graph; configs[1] at N=1).
+
+  python bench.py --gpus N --steps K --warmup W            (N>1: under torchrun, one rank per GPU)
+  python bench.py --impl reference ...                      (the CPU oracle, rank 0 only)
+
+One "step" = one synchronous-SGD step: every rank samples, gathers, runs forward/backward on
+its own mini-batch (global batch g = step*N + rank), all-reduces gradients (NCCL), updates.
+Prints ONE JSON line on rank 0.  Inputs are synthetic (gnn_inputs), resident in HBM before
+the timed region; X (980 MB) and the CSR are larger than L2, every step gathers new rows.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="products")
+    p.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
+    p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+METRIC = "mini-batches/s & epoch time, GraphSAGE on products-shaped graph, 1/2/4/8 B200"
+
+
+# ---------------------------------------------------------------- clocks during the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- algorithmic work per kernel class
+def agg_l1_bytes(w, sz):
+    """Layer-1 fused gather + mean aggregation, compulsory HBM bytes:
+    every unique input row once + the [X_self | mean] operand written + CSR of the block."""
+    L = w.num_layers
+    h = L - 1
+    fp = w.feat_stride
+    n_dst, n_src, E = sz["n_dst"][h], sz["n_src"][h], sz["n_edges"][h]
+    return n_src * fp * 4 + n_dst * 2 * fp * 4 + E * 4 + (n_dst + 1) * 4
+
+
+def gemm_flops(w, sz, which):
+    dims = w.dims
+    L = w.num_layers
+    f = 0
+    for li in range(L):
+        h = L - 1 - li
+        M = sz["n_dst"][h]
+        K = (2 if w.model == "sage" else 1) * dims[li]
+        N = dims[li + 1]
+        if which == "gemm_fwd":
+            f += 2 * M * K * N
+        elif which == "gemm_wgrad":
+            f += 2 * M * K * N
+        elif which == "gemm_dgrad" and li > 0:
+            f += 2 * M * K * N
+    return f
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------- oracle (cpu baseline / reference arm)
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return 1
+
+
+def time_oracle(w, graph, steps, warmup=0):
+    import oracle
+    from oracle import sampling as OS
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    params = graph["params"].astype(np.float64)
+    for s in range(warmup):
+        params = oracle.train_step(w, graph, params, 0, s, 1, perm=perm)["params"]
+    t0 = time.perf_counter()
+    for s in range(steps):
+        params = oracle.train_step(w, graph, params, 0, warmup + s, 1, perm=perm)["params"]
+    return time.perf_counter() - t0
+
+
+def oracle_graph(w, inp):
+    return dict(row_ptr=inp["row_ptr"], col=inp["col"], X=inp["X"][:, :w.feat_dim], y=inp["y"],
+                train=inp["train"], params=inp["params"])
+
+
+def run_reference(args, w, inp, rank, world):
+    if rank != 0:
+        return
+    graph = oracle_graph(w, inp)
+    secs = time_oracle(w, graph, args.steps, args.warmup)
+    v = args.steps / secs
+    cores = oracle_threads()
+    sample = f"{args.steps} consecutive mini-batches of epoch 0 (after {args.warmup} warm-up), batch {w.batch_size}"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "mini-batches/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(w, world),
+            "cpu_baseline": {"value": v, "unit": "mini-batches/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "mini-batches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "epoch_time_s": w.n_batches / v}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(w, world):
+    return {"workload": f"{w.name} (BASELINE.json configs[1])" if w.name == "products" else w.name,
+            "nodes": w.num_nodes, "nnz_target": w.nnz, "feat_dim": w.feat_dim, "classes": w.num_classes,
+            "model": "GraphSAGE-mean" if w.model == "sage" else "GCN", "sampler": w.sampler,
+            "fanouts": list(w.fanouts), "layers": w.num_layers, "hidden": w.hidden,
+            "batch_per_rank": w.batch_size, "global_batch": w.batch_size * world,
+            "parallelism": f"dp{world}", "l2": "inputs larger than L2 (feature table + CSR >> 126 MB)"}
+
+
+# ---------------------------------------------------------------- main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from gnn_inputs import WORKLOADS, build_inputs
+    w = WORKLOADS[args.config]
+    inp = build_inputs(w)
+
+    if args.impl == "reference":
+        run_reference(args, w, inp, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2403_17092_b200 import Graph, Model, comm_get_unique_id
+
+    g = Graph(inp["row_ptr"], inp["col"], inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim, device=local)
+    m = Model(g, model=w.model, sampler=w.sampler, num_layers=w.num_layers, hidden=w.hidden,
+              batch_size=w.batch_size, fanouts=w.fanouts, precision=args.precision,
+              use_graph=not args.no_graph, lr=w.lr, seed=w.sampler_seed, init_seed=w.init_seed)
+    m.set_train_nodes(inp["train"])
+    m.set_params(inp["params"])
+    if world > 1:
+        obj = [comm_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        m.comm_init(rank, world, obj[0])
+    # a real (non-legacy) stream shared by torch's events and the library's launches
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    m.set_stream(stream)
+    steps_per_epoch = (w.n_batches + world - 1) // world
+
+    def step_at(i):
+        return divmod(i, steps_per_epoch)    # (epoch, step)
+
+    def active_batches(i0, n):
+        tot = 0
+        for i in range(i0, i0 + n):
+            e, s = step_at(i)
+            tot += sum(1 for p in range(world) if s * world + p < w.n_batches)
+        return tot
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up
+    for i in range(args.warmup):
+        e, s = step_at(i)
+        m.train_minibatch(e, s, sync=False)
+    barrier()
+
+    # ---- timed region (device-resident inputs)
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.warmup, args.warmup + args.steps):
+        e, s = step_at(i)
+        m.train_minibatch(e, s, sync=False)
+    ev1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    units = active_batches(args.warmup, args.steps)
+    value = units / (ms / 1e3)
+
+    # ---- e2e: public host-pointer call, seeds H2D + loss D2H inside the timed region
+    perm0 = m.epoch_permutation(0)   # the library's own seed order (gnn_epoch_permutation)
+    seeds_pin = torch.empty(w.batch_size, dtype=torch.int32, pin_memory=True)
+    loss_pin = torch.empty(1, dtype=torch.float32, pin_memory=True)
+    base = args.warmup + args.steps
+    batches = []
+    for i in range(base, base + args.steps):
+        e, s = step_at(i % steps_per_epoch)
+        gidx = s * world + rank
+        sd = perm0[gidx * w.batch_size: (gidx + 1) * w.batch_size] if gidx < w.n_batches else perm0[:0]
+        bt = int(max(0, min(w.n_train - s * world * w.batch_size, world * w.batch_size)))
+        batches.append((np.ascontiguousarray(sd, dtype=np.int32), bt, gidx))
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h2d = 0
+    for sd, bt, gidx in batches:
+        n = sd.shape[0]
+        seeds_pin[:n].numpy()[:] = sd
+        m.train_batch_host_ptr(seeds_pin.data_ptr(), n, bt, 0, gidx, loss_pin.data_ptr())
+        h2d += 4 * n
+    e1.record(stream)
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    units_e2e = sum(1 for _ in batches) * 1   # per rank
+    if world > 1:
+        t = torch.tensor([sum(1 for sd, _, _ in batches if sd.shape[0] > 0)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        units_e2e = float(t.item())
+    else:
+        units_e2e = sum(1 for sd, _, _ in batches if sd.shape[0] > 0)
+    e2e_value = units_e2e / (ms_e2e / 1e3)
+
+    # ---- instrumented pass (per-kernel CUDA events on the library's stream, eager launches)
+    m.profile_enable(True)
+    m.profile_reset()
+    sizes = []
+    for i in range(args.warmup, args.warmup + args.steps):
+        e, s = step_at(i)
+        m.train_minibatch(e, s, sync=False)
+        sizes.append(m.last_sizes())
+    barrier()
+    prof = {k: m.profile_read(k) for k in ["sample", "relabel", "scan", "transpose", "induce", "agg_l1",
+                                           "agg", "gemm_fwd", "gemm_dgrad", "gemm_wgrad", "spmm_bwd",
+                                           "ce", "allreduce", "sgd", "other"]}
+    m.profile_enable(False)
+    tot_ms = sum(v[0] for v in prof.values())
+    hbm, bf16, bf16_sus, peak_kind = load_peaks()
+    dominant = max(prof, key=lambda k: prof[k][0])
+    # roofline of the dominant kernel class
+    if dominant.startswith("gemm"):
+        work = np.mean([gemm_flops(w, sz, dominant) for sz in sizes])
+        launches = prof[dominant][1] / args.steps
+        achieved = work / (prof[dominant][0] / args.steps * 1e-3) / 1e12
+        fp32_simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12   # FFMA/clk/SM x clock
+        roof = {"kernel": dominant, "bound": "alu", "achieved": achieved, "peak": fp32_simt_peak,
+                "unit": "TFLOP/s", "frac": achieved / fp32_simt_peak, "traffic": None,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz",
+                "launches_per_step": launches}
+    else:
+        work = np.mean([agg_l1_bytes(w, sz) for sz in sizes])
+        per_launch_ms = prof["agg_l1"][0] / max(prof["agg_l1"][1], 1)
+        achieved = work / (per_launch_ms * 1e-3) / 1e9
+        roof = {"kernel": "agg_l1", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}
+    # always also report the gather/aggregation kernel against HBM
+    per_launch_ms = prof["agg_l1"][0] / max(prof["agg_l1"][1], 1)
+    agg_bytes = float(np.mean([agg_l1_bytes(w, sz) for sz in sizes]))
+    agg = {"kernel": "agg_l1 (fused feature gather + mean aggregation, layer 1)", "bound": "hbm",
+           "bytes_per_launch": agg_bytes, "ms_per_launch": per_launch_ms,
+           "achieved": agg_bytes / (per_launch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    agg["frac"] = agg["achieved"] / hbm
+
+    # ---- cpu baseline (oracle on a bounded sample), rank 0 at N=1 only
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        graph = oracle_graph(w, inp)
+        nb = 2
+        secs = time_oracle(w, graph, nb)
+        cpu = {"value": nb / secs, "unit": "mini-batches/s", "cores": oracle_threads(), "kind": "oracle",
+               "sample": f"{nb} mini-batches (g=0,1 of epoch 0) of the same workload, full oracle step "
+                         f"(C sampling + fp64 numpy/scipy forward/backward/SGD)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "mini-batches/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == "fp32" else "bf16-gemm/f32",
+            "data": "synthetic (gnn_inputs: power-law Chung-Lu CSR, hashed features/labels)",
+            "config": config_dict(w, world),
+            "epoch_time_s": w.n_batches / value,
+            "e2e": {"value": e2e_value, "unit": "mini-batches/s", "h2d_bytes_per_step": h2d // len(batches),
+                    "d2h_bytes_per_step": 4,
+                    "api": "gnn_train_batch_host (pinned host seeds -> device, step, loss -> host; synchronous)"},
+            "gpu_launches": int(m.launches_per_step * args.steps),
+            "launches_per_step": m.launches_per_step,
+            "roofline": roof,
+            "gather_aggregate": agg,
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "kernel_share": {k: v[0] / tot_ms for k, v in prof.items()} if tot_ms else {},
+            "instrumented_ms_per_step": tot_ms / args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "mean_sizes": {k: [float(np.mean([s[k][h] for s in sizes])) for h in range(len(sizes[0][k]))]
+                           for k in ("n_dst", "n_src", "n_edges")},
+        }
+        print(json.dumps(line), flush=True)
+    m.close()
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

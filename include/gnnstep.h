@@ -1,0 +1,197 @@
+/*
+ * gnnstep.h — C ABI of the B200-native per-mini-batch GNN training step of
+ * "A Unified CPU-GPU Protocol for GNN Training" (arXiv 2403.17092).
+ *
+ * The library (paper_2403_17092_b200/libgnnstep.so) runs, per mini-batch and per
+ * trainer (one process per GPU), the step the paper's trainer processes run
+ * (§3: "sampling → data fetching → forward/backward →
+ * local gradient", then the synchronous-SGD exchange of §2.2):
+ *
+ *   neighbour / ShaDow sampling (§2.2)  → dedup + relabel
+ *   → input-feature gather (§2.2, "data fetching")
+ *   → Â·H aggregation + dense update, GCN Eq. (1) / GraphSAGE Eq. (2) (lines 131-142)
+ *   → softmax cross-entropy and the Eq. (3) mini-batch gradient (lines 161-165)
+ *   → gradient all-reduce across trainers (NCCL) → SGD update.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns gnn_status; no C++ exception crosses the ABI.  On a non-OK
+ *     return gnn_last_error() holds a thread-local message.
+ *   - Pointers named *_host are HOST memory; the library copies what it needs
+ *     (inputs) or copies into them (outputs).  The caller keeps ownership.
+ *   - Handles (gnn_graph*, gnn_model*) are created and destroyed by the caller.
+ *   - Work is enqueued on the model's CUDA stream (gnn_set_stream, default: a
+ *     stream the library owns).  Calls that return host data synchronize that
+ *     stream before returning; the others return after enqueueing.
+ *   - A call with world > 1 (after gnn_comm_init) is collective: every rank must
+ *     make the same sequence of such calls.
+ *   - Device index: the graph's device; the library makes it current on each call.
+ */
+#ifndef GNNSTEP_H
+#define GNNSTEP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GNN_ABI_VERSION 1
+
+typedef enum {
+    GNN_OK = 0,
+    GNN_ERR_RANGE = -1,   /* an id or label out of range          */
+    GNN_ERR_PARAM = -2,   /* an invalid scalar argument                  */
+    GNN_ERR_SHAPE = -3,   /* a size/shape contract violation      */
+    GNN_ERR_CONFIG = -4,  /* an unsupported model/sampler configuration */
+    GNN_ERR_STATE = -5,   /* call out of order (e.g. training before set_train_nodes)     */
+    GNN_ERR_BUFFER = -6,  /* caller buffer too small                                        */
+    GNN_ERR_OOM = -7,     /* device allocation failed                                       */
+    GNN_ERR_CUDA = -8,    /* a CUDA runtime error (message in gnn_last_error)              */
+    GNN_ERR_NCCL = -9     /* an NCCL error                                                   */
+} gnn_status;
+
+enum { GNN_SAGE_MEAN = 0, GNN_GCN = 1 };          /* Eq. (2) / Eq. (1)                  */
+enum { GNN_NEIGHBOR = 0, GNN_SHADOW = 1 };        /* §2.2 Neighbor / ShaDow K-hop       */
+enum { GNN_FP32 = 0, GNN_BF16_GEMM = 1 };         /* dense-update GEMM arithmetic        */
+
+typedef struct gnn_graph gnn_graph;
+typedef struct gnn_model gnn_model;
+
+/* Thread-local message for the last non-OK status of this thread. */
+const char* gnn_last_error(void);
+int32_t gnn_abi_version(void);
+
+/* ---------------------------------------------------------------- graph
+ * G = (V, E), N = |V|, adjacency as CSR, H^0 = features, y = labels (§2.1
+ * lines 119-124; SPEC.md Graph lines 22-28).
+ *   row_ptr_host  int64[num_nodes+1], non-decreasing, row_ptr[0] = 0.
+ *   col_idx_host  int32[row_ptr[N]]; row v lists the message sources of v (in-
+ *                 neighbours), ascending and duplicate-free; every id in [0, N).
+ *   features_host fp32[num_nodes * feat_stride], row-major; feat_stride >= feat_dim,
+ *                 a multiple of 4; columns >= feat_dim are ignored (treated as 0).
+ *   labels_host   int32[num_nodes] in [0, num_classes).
+ * Everything is copied to HBM of `device`.  Errors: RANGE for an id/label out of
+ * range, SHAPE for a malformed CSR, PARAM for bad sizes, OOM. */
+gnn_status gnn_graph_create(int64_t num_nodes, const int64_t* row_ptr_host,
+                            const int32_t* col_idx_host, int32_t feat_dim, int32_t feat_stride,
+                            const float* features_host, const int32_t* labels_host,
+                            int32_t num_classes, int32_t device, gnn_graph** out);
+gnn_status gnn_graph_destroy(gnn_graph* g);
+
+/* ---------------------------------------------------------------- model
+ * Layers l = 1..L are numbered input-first; dims = [F, hidden, ..., hidden, C].
+ * fanouts are listed input-layer-first (R1): hop h (seeds = hop 0)
+ * samples fanouts[L-1-h] neighbours per node.  NEIGHBOR needs num_fanouts ==
+ * num_layers; SHADOW samples L' = num_fanouts hops and runs num_layers layers on the
+ * induced subgraph (§2.2).  batch_size is per rank.
+ * Parameters (flat fp32, layer order): SAGE layer l is the (2*in) x out row-major
+ * matrix [W_1; W_2] (self; neighbour) of Eq. (2); GCN layer l is W^(l), in x out.
+ * Initialised Glorot-uniform from init_seed. */
+typedef struct {
+    int32_t model;          /* GNN_SAGE_MEAN | GNN_GCN                        */
+    int32_t sampler;        /* GNN_NEIGHBOR | GNN_SHADOW                      */
+    int32_t num_layers;     /* L, 1..8                                        */
+    int32_t hidden;         /* d                                              */
+    int32_t batch_size;     /* b per rank, >= 1                               */
+    int32_t num_fanouts;    /* 1..8                                           */
+    int32_t fanouts[8];     /* input-layer-first, each 1..32                  */
+    int32_t precision;      /* GNN_FP32 | GNN_BF16_GEMM                       */
+    int32_t use_graph;      /* 1: replay the step as one CUDA graph           */
+    float lr;               /* SGD learning rate                              */
+    uint64_t seed;          /* sampler seed (permutation + sampling draws)    */
+    uint64_t init_seed;     /* weight init                                    */
+} gnn_model_config;
+
+gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model** out);
+gnn_status gnn_model_destroy(gnn_model* m);
+/* stream: a cudaStream_t (as void*) on the graph's device, or NULL for the library's own. */
+gnn_status gnn_set_stream(gnn_model* m, void* stream);
+/* The train split (copied).  ids in [0, N), duplicate-free.  n may be 0. */
+gnn_status gnn_set_train_nodes(gnn_model* m, const int32_t* ids_host, int64_t n);
+int64_t gnn_param_count(const gnn_model* m);
+int64_t gnn_num_batches(const gnn_model* m);   /* ceil(n_train / batch_size) */
+gnn_status gnn_get_params(gnn_model* m, float* out_host, int64_t n);   /* n == param_count */
+gnn_status gnn_set_params(gnn_model* m, const float* in_host, int64_t n);
+
+/* ---------------------------------------------------------------- data parallel
+ * Synchronous SGD across `world` trainers (§2.2): global batch
+ * g of an epoch goes to rank g mod world at step floor(g / world); the gradient of a
+ * step is Σ over ranks of (per-sample gradient sum) / b_total, b_total = seeds in the
+ * step over all ranks (R8/R9), all-reduced with NCCL.
+ * Rank 0 calls gnn_comm_get_unique_id; the caller broadcasts the 128 bytes (e.g.
+ * torch.distributed); every rank then calls gnn_comm_init (collective). */
+gnn_status gnn_comm_get_unique_id(uint8_t out_host[128]);
+gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_t id_host[128]);
+
+/* The epoch's seed order (§2.2; SPEC.md partition_seeds lines 107-115):
+ * train ids sorted by (Philox key64(id, epoch), id) (R7); batch g is
+ * perm[g*B, min((g+1)*B, n_train)).  Computed on the device; copied into out_host
+ * (int32[n_train]); BUFFER if n < n_train. */
+gnn_status gnn_epoch_permutation(gnn_model* m, int64_t epoch, int32_t* out_host, int64_t n);
+
+/* ---------------------------------------------------------------- sampling (parity hook)
+ * Sample global batch g of `epoch` (any rank may sample any g), synchronously.
+ * sizes: hop h = 0..num_hops-1 (seeds outward): n_dst, n_src, n_edges.  For SHADOW,
+ * hop index num_hops holds the induced block (n_dst = n_src = |S|). */
+typedef struct {
+    int32_t num_hops;
+    int64_t n_dst[9], n_src[9], n_edges[9];
+} gnn_batch_sizes;
+gnn_status gnn_sample(gnn_model* m, int64_t epoch, int64_t g, gnn_batch_sizes* sizes_host);
+
+enum { GNN_SRC_IDS = 0, GNN_BLK_ROWPTR = 1, GNN_BLK_COL = 2, GNN_BLK_NBR = 3 };
+/* Copy one array of hop `hop` of the last gnn_sample into out_host (int32).
+ * Lengths: SRC_IDS n_src, BLK_ROWPTR n_dst+1, BLK_COL / BLK_NBR n_edges.
+ * BUFFER if n is smaller; n larger is fine.  For SHADOW, hop = num_hops is the induced
+ * block (BLK_NBR = global id of each source). */
+gnn_status gnn_sample_fetch(gnn_model* m, int32_t hop, int32_t what, int32_t* out_host, int64_t n);
+
+/* ---------------------------------------------------------------- training
+ * One synchronous-SGD step: this rank trains global batch g = step*world + rank of
+ * `epoch` (nothing if g >= num_batches, but it still joins the all-reduce), then the
+ * all-reduce and the SGD update.  Device-resident inputs (the epoch permutation is
+ * computed on the device when `epoch` changes).  loss_out_host: if non-NULL the call
+ * synchronizes and writes this rank's loss Σ_{i in this rank's batch} ℓ_i / b_total
+ * (the step's global loss is the sum over ranks); if NULL it returns after
+ * enqueueing. */
+gnn_status gnn_train_minibatch(gnn_model* m, int64_t epoch, int64_t step, float* loss_out_host);
+
+/* End-to-end call: the seeds of this rank's batch come from HOST memory (pinned for
+ * best speed), are copied to the device, the step runs (sampling keyed by (epoch, g)),
+ * and this rank's loss is copied back; synchronous.  b_total = seeds in the step
+ * over all ranks. */
+gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t n_seeds,
+                                int32_t b_total, int64_t epoch, int64_t g, float* loss_out_host);
+
+typedef struct { double seconds; int64_t steps; int64_t minibatches; double mean_loss; } gnn_epoch_stats;
+/* All steps of an epoch (collective when world > 1). */
+gnn_status gnn_train_epoch(gnn_model* m, int64_t epoch, gnn_epoch_stats* out_host);
+gnn_status gnn_synchronize(gnn_model* m);
+
+/* ---------------------------------------------------------------- introspection
+ * what: GNN_DBG_LOGITS (b x C of the last step, fp32), GNN_DBG_GRADS (flat, after the
+ * all-reduce, before SGD), GNN_DBG_LOSS (1 value: this rank's loss), GNN_DBG_ACT + l
+ * (layer l's output H^(l) of the last step, 0-based l, rows x out, fp32; its sign pattern
+ * is the ReLU decision the backward pass used).  BUFFER if n is too small. */
+enum { GNN_DBG_LOGITS = 0, GNN_DBG_GRADS = 1, GNN_DBG_LOSS = 2, GNN_DBG_ACT = 16 };
+gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n);
+/* Sizes of the last trained batch (synchronizes). */
+gnn_status gnn_last_sizes(gnn_model* m, gnn_batch_sizes* sizes_host);
+
+/* Per-kernel timing (CUDA events around each launch, eager mode only; for the bench's
+ * roofline).  enable=1 turns instrumentation on (and CUDA-graph replay off). */
+gnn_status gnn_profile_enable(gnn_model* m, int32_t enable);
+/* Accumulated milliseconds and launch count of kernel class `kid` (GNN_K_*). */
+enum { GNN_K_SAMPLE = 0, GNN_K_RELABEL = 1, GNN_K_AGG_L1 = 2, GNN_K_AGG = 3, GNN_K_GEMM_FWD = 4,
+       GNN_K_GEMM_DGRAD = 5, GNN_K_GEMM_WGRAD = 6, GNN_K_SPMM_BWD = 7, GNN_K_CE = 8,
+       GNN_K_SGD = 9, GNN_K_TRANSPOSE = 10, GNN_K_INDUCE = 11, GNN_K_ALLREDUCE = 12,
+       GNN_K_SCAN = 13, GNN_K_OTHER = 14, GNN_K_COUNT = 15 };
+gnn_status gnn_profile_read(gnn_model* m, int32_t kid, double* ms_out_host, int64_t* launches_out_host);
+gnn_status gnn_profile_reset(gnn_model* m);
+/* Number of kernels one step launches (for the bench's gpu_launches). */
+int64_t gnn_launches_per_step(const gnn_model* m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNNSTEP_H */

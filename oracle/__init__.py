@@ -50,7 +50,7 @@ def sample_batch(w, graph, epoch: int, g: int, perm=None):
 
 
 def train_step(w, graph, params_flat, epoch: int, step: int, world: int, perm=None, X=None,
-               lr=None):
+               lr=None, mask_override=None, keep_cache=False):
     """One synchronous-SGD step with `world` virtual ranks (O1-O9).
     Rank p trains global batch g = step*world + p (inactive if g >= n_batches).
     Returns dict(loss=global loss, rank_losses, rank_grads, grad (allreduced, flat),
@@ -64,18 +64,21 @@ def train_step(w, graph, params_flat, epoch: int, step: int, world: int, perm=No
     gs = [step * world + p for p in range(world)]
     sizes = [len(sampling.batch_seeds(perm, w.batch_size, g)) if g < nb else 0 for g in gs]
     b_total = sum(sizes)
-    rank_losses, rank_grads, logits = [], [], []
+    rank_losses, rank_grads, logits, caches = [], [], [], []
     for p, g in enumerate(gs):
         if g >= nb:
             rank_losses.append(0.0)
             rank_grads.append([np.zeros_like(W) for W in Ws])
             logits.append(None)
+            caches.append(None)
             continue
         s, seeds = sample_batch(w, graph, epoch, g, perm)
         blocks, input_ids = model.layer_blocks(s, w.sampler, w.num_layers)
         labels = graph["y"][seeds]
+        ovr = mask_override[p] if mask_override else None
         loss, grads, cache = model.minibatch_grad(Ws, w.model, blocks, input_ids, X, labels,
-                                                  len(seeds), b_total)
+                                                  len(seeds), b_total, ovr)
+        caches.append(dict(cache, Ws=Ws) if keep_cache else None)
         rank_losses.append(loss)
         rank_grads.append(grads)
         logits.append(cache["H"][-1][:len(seeds)])
@@ -83,4 +86,4 @@ def train_step(w, graph, params_flat, epoch: int, step: int, world: int, perm=No
     newW = model.sgd(Ws, G, lr)
     return dict(loss=float(sum(rank_losses)), rank_losses=rank_losses,
                 rank_grads=[model.flatten(g) for g in rank_grads], grad=model.flatten(G),
-                params=model.flatten(newW), logits=logits, b_total=b_total)
+                params=model.flatten(newW), logits=logits, b_total=b_total, caches=caches)

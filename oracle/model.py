@@ -103,7 +103,18 @@ def cross_entropy(Z, y, b_total):
 
 
 # ---------------------------------------------------------------- O7
-def backward(Ws, model, blocks, cache, dZ):
+def relu_mask(Pre, override=None):
+    """[Pre > 0] (ReLU'(0) = 0).  `override` = (rows, cols, values) replaces the decision at
+    kink-ambiguous units (|Pre| within the fp32 error of the GEMM, R27): there
+    either decision is a correct result, the caller validates which one it supplies."""
+    mask = Pre > 0.0
+    if override is not None:
+        r, c, v = override
+        mask[r, c] = v
+    return mask
+
+
+def backward(Ws, model, blocks, cache, dZ, mask_override=None):
     L = len(blocks)
     grads = [None] * L
     dPre = np.zeros_like(cache["Pre"][L - 1])
@@ -123,7 +134,8 @@ def backward(Ws, model, blocks, cache, dZ):
             dH[:blk["n_dst"]] += dSelf
         else:
             dH = Ahat.T @ dA
-        dPre = dH * (cache["Pre"][l - 1] > 0.0)   # ReLU'(0) = 0
+        ovr = mask_override.get(l - 1) if mask_override else None
+        dPre = dH * relu_mask(cache["Pre"][l - 1], ovr)
     return grads
 
 
@@ -139,13 +151,13 @@ def layer_blocks(sample, sampler, num_layers):
     return [block] * num_layers, block["src_ids"]
 
 
-def minibatch_grad(Ws, model, blocks, input_ids, X, labels, b, b_total):
+def minibatch_grad(Ws, model, blocks, input_ids, X, labels, b, b_total, mask_override=None):
     """One rank's O4-O7: returns (rank loss, list of dW, cache)."""
     X_in = np.asarray(X, dtype=np.float64)[np.asarray(input_ids, dtype=np.int64)]
     cache = forward(Ws, model, blocks, X_in)
     Z = cache["H"][-1][:b]
     loss, dZ = cross_entropy(Z, labels, b_total)
-    grads = backward(Ws, model, blocks, cache, dZ)
+    grads = backward(Ws, model, blocks, cache, dZ, mask_override)
     return loss, grads, cache
 
 

@@ -1,0 +1,8 @@
+"""B200-native (sm_100a) per-mini-batch GNN training step of arXiv 2403.17092.
+
+The product is the C-ABI library libgnnstep.so (include/gnnstep.h, sources in csrc/);
+this package is its thin Python binding.  No CPU fallback exists.
+"""
+from .gnnstep import (Graph, Model, GnnError, comm_get_unique_id, lib, KERNEL_IDS)  # noqa: F401
+
+__all__ = ["Graph", "Model", "GnnError", "comm_get_unique_id", "lib", "KERNEL_IDS"]

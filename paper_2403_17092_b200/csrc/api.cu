@@ -1,0 +1,857 @@
+// C-ABI and per-rank engine of libgnnstep.so (include/gnnstep.h).
+//
+// One step = the trainer-process work of PAPER.md §3 lines 237-242 (sampling → data
+// fetching → forward/backward → local gradient) + the synchronous-SGD exchange of §2.2
+// lines 173-175.  All buffers are sized once to worst-case bounds (DESIGN.md "Dynamic
+// shapes"); every kernel reads its extent from the device StepState, so the step body is
+// captured once as a CUDA graph and replayed per mini-batch.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <string>
+#include <vector>
+
+#include "../../include/gnnstep.h"
+#include "kernels.h"
+
+using namespace gs;
+
+namespace {
+thread_local std::string g_err;
+
+gnn_status fail(gnn_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(e_ == cudaErrorMemoryAllocation ? GNN_ERR_OOM : GNN_ERR_CUDA,           \
+                        std::string(#x) + ": " + cudaGetErrorString(e_));                       \
+    } while (0)
+#define CKN(x)                                                                                  \
+    do {                                                                                        \
+        ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess) return fail(GNN_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+#define TRY(x)                        \
+    do {                              \
+        gnn_status s_ = (x);          \
+        if (s_ != GNN_OK) return s_;  \
+    } while (0)
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+template <class T>
+gnn_status dalloc(T** p, int64_t count, std::vector<void*>& owned) {
+    *p = nullptr;
+    if (count <= 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)count);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GNN_ERR_OOM, "cudaMalloc of " + std::to_string(sizeof(T) * count) + " bytes: " +
+                                     cudaGetErrorString(e));
+    }
+    owned.push_back(*p);
+    return GNN_OK;
+}
+}  // namespace
+
+struct gnn_graph {
+    int dev = 0;
+    int64_t N = 0, nnz = 0;
+    int F = 0, stride = 0, C = 0;
+    int64_t* row_ptr = nullptr;
+    int32_t* col = nullptr;
+    float* X = nullptr;
+    int32_t* y = nullptr;
+    std::vector<void*> owned;
+};
+
+namespace {
+struct HopBufs {
+    int64_t cap_dst = 0, cap_edges = 0, cap_src = 0;
+    bool need_t = false;
+    int32_t *rowptr = nullptr, *col = nullptr, *nbr = nullptr;
+    int32_t *trowptr = nullptr, *tcursor = nullptr, *tdst = nullptr, *tdst_s = nullptr;
+};
+
+struct Layer {
+    int in = 0, out = 0, in_pad = 0, k_pad = 0, n_pad = 0, rows = 0;  // rows of W (2in or in)
+    int64_t poff = 0, pcnt = 0;
+    int blk = 0;           // block (hop or ShaDow slot) this layer aggregates over
+    int64_t m_cap = 0;     // max rows of this layer's output
+    int splits = 1;
+    float *Wp = nullptr, *A = nullptr, *H = nullptr, *dPre = nullptr, *dA = nullptr, *wpart = nullptr;
+};
+
+struct ProfPair { int kid; cudaEvent_t a, b; };
+}  // namespace
+
+struct gnn_model {
+    gnn_graph* g = nullptr;
+    gnn_model_config cfg{};
+    int L = 0, hops = 0, slot = -1;
+    bool sage = true, shadow = false;
+    std::vector<int> dims;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::vector<void*> owned;
+
+    StepState* st = nullptr;
+    int32_t *nodes = nullptr, *map = nullptr, *tcount = nullptr, *icount = nullptr;
+    uint32_t* bits = nullptr;
+    int64_t nwords = 0, nodes_cap = 0, tcap = 0;
+    ScanScratch sc{};
+    HopBufs hb[kMaxHops + 1];
+    std::vector<Layer> layers;
+    float *params = nullptr, *grads = nullptr;
+    int64_t pcount = 0;
+
+    int32_t *train = nullptr, *perm = nullptr, *train_sorted = nullptr;
+    uint64_t *keys = nullptr, *keys_alt = nullptr;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    int64_t n_train = 0, train_cap = 0, perm_epoch = -1;
+    int32_t* seeds_in = nullptr;
+
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+
+    cudaGraphExec_t gexec = nullptr;
+    int64_t launches_per_step = 0;
+
+    bool profiling = false;
+    std::vector<ProfPair> pending;
+    std::vector<cudaEvent_t> free_events;
+    double prof_ms[GNN_K_COUNT] = {};
+    int64_t prof_n[GNN_K_COUNT] = {};
+};
+
+namespace {
+// ---------------------------------------------------------------- profiling wrapper
+cudaEvent_t take_event(gnn_model* m) {
+    if (!m->free_events.empty()) {
+        cudaEvent_t e = m->free_events.back();
+        m->free_events.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+template <class Fn>
+void K(gnn_model* m, int kid, Fn&& fn) {
+    if (m->profiling) {
+        ProfPair p{kid, take_event(m), take_event(m)};
+        cudaEventRecord(p.a, m->stream);
+        fn();
+        cudaEventRecord(p.b, m->stream);
+        m->pending.push_back(p);
+    } else {
+        fn();
+    }
+}
+
+void drain_profile(gnn_model* m) {
+    for (auto& p : m->pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(p.b);
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        m->prof_ms[p.kid] += ms;
+        m->prof_n[p.kid] += 1;
+        m->free_events.push_back(p.a);
+        m->free_events.push_back(p.b);
+    }
+    m->pending.clear();
+}
+
+const int32_t* rows_ptr(gnn_model* m, int li) {   // output rows of layer li (0-based)
+    if (m->shadow && li == m->L - 1) return &m->st->batch_n;
+    return &m->st->n_dst[m->layers[li].blk];
+}
+
+// ---------------------------------------------------------------- step body
+void enqueue_sampling(gnn_model* m) {
+    gnn_graph* g = m->g;
+    cudaStream_t s = m->stream;
+    for (int h = 0; h < m->hops; ++h) {
+        const int k = m->cfg.fanouts[m->hops - 1 - h];
+        HopBufs& b = m->hb[h];
+        K(m, GNN_K_SCAN, [&] { launch_hop_rowptr(h, k, m->st, m->nodes, g->row_ptr, b.rowptr, m->sc, s); });
+        K(m, GNN_K_SAMPLE, [&] {
+            launch_sample_fill(h, k, m->st, m->nodes, g->row_ptr, g->col, b.rowptr, b.nbr, m->map, m->bits,
+                               m->cfg.seed, s);
+        });
+        K(m, GNN_K_RELABEL, [&] { launch_assign_new(h, m->st, m->bits, m->nwords, m->nodes, m->map, m->sc, s); });
+        K(m, GNN_K_RELABEL, [&] {
+            launch_relabel_edges(h, m->st, b.nbr, b.col, m->map, b.need_t ? m->tcount : nullptr, s);
+        });
+        if (b.need_t)
+            K(m, GNN_K_TRANSPOSE, [&] {
+                launch_transpose(h, m->st, b.rowptr, b.col, m->tcount, b.trowptr, b.tcursor, b.tdst, b.tdst_s,
+                                 m->sc, s);
+            });
+    }
+    if (m->shadow) {
+        HopBufs& b = m->hb[m->slot];
+        K(m, GNN_K_INDUCE, [&] {
+            launch_induce(m->hops - 1, m->slot, m->st, m->nodes, g->row_ptr, g->col, m->map, m->icount,
+                          b.rowptr, b.col, m->tcount, m->sc, s);
+        });
+        K(m, GNN_K_TRANSPOSE, [&] {
+            launch_transpose(m->slot, m->st, b.rowptr, b.col, m->tcount, b.trowptr, b.tcursor, b.tdst,
+                             b.tdst_s, m->sc, s);
+        });
+    }
+    K(m, GNN_K_OTHER, [&] { launch_reset_map(m->hops - 1, m->st, m->nodes, m->map, s); });
+}
+
+void enqueue_training(gnn_model* m) {
+    gnn_graph* g = m->g;
+    cudaStream_t s = m->stream;
+    const int L = m->L;
+    // ---- forward
+    for (int li = 0; li < L; ++li) {
+        Layer& ly = m->layers[li];
+        HopBufs& b = m->hb[ly.blk];
+        const int32_t* rows = rows_ptr(m, li);
+        const float* Hin = li == 0 ? g->X : m->layers[li - 1].H;
+        const int kid = li == 0 ? GNN_K_AGG_L1 : GNN_K_AGG;
+        if (m->sage) {
+            // layer 1 of the neighbour sampler reads X rows directly by global neighbour id
+            const bool direct = li == 0 && !m->shadow;
+            K(m, kid, [&] {
+                launch_agg_sage(rows, Hin, ly.in_pad, direct ? nullptr : (li == 0 ? m->nodes : nullptr),
+                                li == 0 ? m->nodes : nullptr, b.rowptr, direct ? b.nbr : b.col, ly.A, s);
+            });
+        } else {
+            K(m, kid, [&] {
+                launch_agg_gcn(rows, &m->st->n_dst[ly.blk], Hin, ly.in_pad, li == 0 ? m->nodes : nullptr,
+                               li == 0 ? m->nodes : nullptr, b.rowptr, b.col, b.trowptr, ly.A, s);
+            });
+        }
+        K(m, GNN_K_GEMM_FWD, [&] {
+            launch_gemm(false, false, li < L - 1, rows, 0, (int)ly.m_cap, ly.n_pad, nullptr, ly.k_pad, ly.A,
+                        ly.k_pad, ly.Wp, ly.n_pad, ly.H, ly.n_pad, 1, 0, s);
+        });
+    }
+    // ---- loss
+    Layer& last = m->layers[L - 1];
+    K(m, GNN_K_CE, [&] { launch_ce(m->st, last.H, last.n_pad, g->C, g->y, m->nodes, last.dPre, s); });
+    // ---- backward
+    for (int li = L - 1; li >= 0; --li) {
+        Layer& ly = m->layers[li];
+        const int32_t* rows = rows_ptr(m, li);
+        const int64_t stride = (int64_t)ly.k_pad * ly.n_pad;
+        K(m, GNN_K_GEMM_WGRAD, [&] {
+            launch_gemm(true, false, false, nullptr, ly.k_pad, ly.k_pad, ly.n_pad, rows, 0, ly.A, ly.k_pad,
+                        ly.dPre, ly.n_pad, ly.wpart, ly.n_pad, ly.splits, stride, s);
+            launch_wgrad_reduce(ly.wpart, ly.splits, stride, ly.rows, ly.out, ly.in, ly.in_pad, m->sage,
+                                ly.n_pad, m->grads + ly.poff, s);
+        });
+        if (li == 0) break;
+        K(m, GNN_K_GEMM_DGRAD, [&] {
+            launch_gemm(false, true, false, rows, 0, (int)ly.m_cap, ly.k_pad, nullptr, ly.n_pad, ly.dPre,
+                        ly.n_pad, ly.Wp, ly.n_pad, ly.dA, ly.k_pad, 1, 0, s);
+        });
+        Layer& prev = m->layers[li - 1];
+        HopBufs& b = m->hb[ly.blk];
+        K(m, GNN_K_SPMM_BWD, [&] {
+            launch_spmm_bwd(!m->sage, ly.blk, m->st, rows, ly.dA, ly.in_pad, b.rowptr, b.trowptr, b.tdst_s,
+                            prev.H, prev.dPre, s);
+        });
+    }
+    // ---- exchange + update
+    if (m->world > 1)
+        K(m, GNN_K_ALLREDUCE, [&] {
+            ncclAllReduce(m->grads, m->grads, (size_t)m->pcount, ncclFloat, ncclSum, m->comm, s);
+        });
+    K(m, GNN_K_SGD, [&] { launch_sgd(m->params, m->grads, m->pcount, m->cfg.lr, s); });
+    for (auto& ly : m->layers)
+        K(m, GNN_K_OTHER, [&] {
+            launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad,
+                               ly.n_pad, ly.Wp, s);
+        });
+}
+
+void enqueue_body(gnn_model* m) {
+    enqueue_sampling(m);
+    enqueue_training(m);
+}
+
+gnn_status build_graph(gnn_model* m) {
+    if (m->gexec) return GNN_OK;
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+    enqueue_body(m);
+    cudaError_t e = cudaStreamEndCapture(m->stream, &graph);
+    if (e != cudaSuccess) return fail(GNN_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    size_t n = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(graph, nodes.data(), &n));
+    int64_t kernels = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        if (t == cudaGraphNodeTypeKernel) ++kernels;
+    }
+    m->launches_per_step = kernels + 1;   // + k_begin_step (outside the graph)
+    CK(cudaGraphInstantiate(&m->gexec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    return GNN_OK;
+}
+
+gnn_status run_body(gnn_model* m) {
+    if (m->cfg.use_graph && !m->profiling) {
+        TRY(build_graph(m));
+        CK(cudaGraphLaunch(m->gexec, m->stream));
+    } else {
+        enqueue_body(m);
+        CK(cudaGetLastError());
+    }
+    return GNN_OK;
+}
+
+gnn_status ensure_perm(gnn_model* m, int64_t epoch) {
+    if (m->perm_epoch == epoch) return GNN_OK;
+    if (m->n_train > 0) {
+        launch_perm_keys(m->train_sorted, m->n_train, m->cfg.seed, epoch, m->keys, m->stream);
+        size_t bytes = m->cub_bytes;
+        CK(cub::DeviceRadixSort::SortPairs(m->cub_tmp, bytes, m->keys, m->keys_alt, m->train_sorted, m->perm,
+                                           (int)m->n_train, 0, 64, m->stream));
+    }
+    m->perm_epoch = epoch;
+    return GNN_OK;
+}
+
+int64_t num_batches(const gnn_model* m) {
+    return (m->n_train + m->cfg.batch_size - 1) / m->cfg.batch_size;
+}
+
+gnn_status set_device(int dev) {
+    CK(cudaSetDevice(dev));
+    return GNN_OK;
+}
+
+// Step for this rank: global batch g = step*world + rank.
+gnn_status begin_step_from_perm(gnn_model* m, int64_t epoch, int64_t step) {
+    TRY(ensure_perm(m, epoch));
+    const int64_t B = m->cfg.batch_size;
+    const int64_t g = step * m->world + m->rank;
+    const int64_t nb = num_batches(m);
+    const int32_t n = g < nb ? (int32_t)std::min<int64_t>(B, m->n_train - g * B) : 0;
+    const int64_t done = step * m->world * B;
+    const int32_t b_total = (int32_t)std::max<int64_t>(0, std::min<int64_t>(m->n_train - done, m->world * B));
+    launch_begin_step(m->st, n > 0 ? m->perm + g * B : m->perm, n, b_total, (uint32_t)epoch, (uint32_t)g,
+                      m->nodes, m->map, m->stream);
+    return GNN_OK;
+}
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* gnn_last_error(void) { return g_err.c_str(); }
+int32_t gnn_abi_version(void) { return GNN_ABI_VERSION; }
+
+gnn_status gnn_graph_create(int64_t num_nodes, const int64_t* row_ptr_host, const int32_t* col_idx_host,
+                            int32_t feat_dim, int32_t feat_stride, const float* features_host,
+                            const int32_t* labels_host, int32_t num_classes, int32_t device, gnn_graph** out) {
+    if (!out) return fail(GNN_ERR_PARAM, "out is NULL");
+    *out = nullptr;
+    if (num_nodes <= 0 || num_nodes >= INT32_MAX) return fail(GNN_ERR_PARAM, "num_nodes out of (0, 2^31-1)");
+    if (!row_ptr_host || !features_host || !labels_host) return fail(GNN_ERR_PARAM, "NULL input array");
+    if (feat_dim <= 0 || feat_stride < feat_dim || feat_stride % 4) return fail(GNN_ERR_PARAM, "feat_stride must be >= feat_dim and a multiple of 4");
+    if (num_classes <= 0) return fail(GNN_ERR_PARAM, "num_classes must be > 0");
+    if (row_ptr_host[0] != 0) return fail(GNN_ERR_SHAPE, "row_ptr[0] != 0");
+    for (int64_t v = 0; v < num_nodes; ++v)
+        if (row_ptr_host[v + 1] < row_ptr_host[v]) return fail(GNN_ERR_SHAPE, "row_ptr not non-decreasing at " + std::to_string(v));
+    const int64_t nnz = row_ptr_host[num_nodes];
+    if (nnz > 0 && !col_idx_host) return fail(GNN_ERR_PARAM, "col_idx is NULL");
+    for (int64_t v = 0; v < num_nodes; ++v)
+        for (int64_t p = row_ptr_host[v]; p < row_ptr_host[v + 1]; ++p) {
+            const int32_t c = col_idx_host[p];
+            if (c < 0 || c >= num_nodes) return fail(GNN_ERR_RANGE, "col_idx out of range at " + std::to_string(p));
+            if (p > row_ptr_host[v] && c <= col_idx_host[p - 1]) return fail(GNN_ERR_SHAPE, "row " + std::to_string(v) + " not ascending/duplicate-free");
+        }
+    for (int64_t v = 0; v < num_nodes; ++v)
+        if (labels_host[v] < 0 || labels_host[v] >= num_classes) return fail(GNN_ERR_RANGE, "label out of range at " + std::to_string(v));
+    TRY(set_device(device));
+    auto* g = new gnn_graph();
+    g->dev = device; g->N = num_nodes; g->nnz = nnz; g->F = feat_dim; g->stride = feat_stride; g->C = num_classes;
+    auto cleanup = [&](gnn_status s) { for (void* p : g->owned) cudaFree(p); delete g; return s; };
+    gnn_status s;
+    if ((s = dalloc(&g->row_ptr, num_nodes + 1, g->owned)) != GNN_OK) return cleanup(s);
+    if ((s = dalloc(&g->col, nnz, g->owned)) != GNN_OK) return cleanup(s);
+    if ((s = dalloc(&g->X, num_nodes * feat_stride, g->owned)) != GNN_OK) return cleanup(s);
+    if ((s = dalloc(&g->y, num_nodes, g->owned)) != GNN_OK) return cleanup(s);
+    cudaError_t e = cudaMemcpy(g->row_ptr, row_ptr_host, sizeof(int64_t) * (num_nodes + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && nnz) e = cudaMemcpy(g->col, col_idx_host, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->X, features_host, sizeof(float) * num_nodes * feat_stride, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->y, labels_host, sizeof(int32_t) * num_nodes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && feat_stride > feat_dim)   // padding columns are zero (DESIGN.md layout)
+        e = cudaMemset2D(g->X + feat_dim, sizeof(float) * feat_stride, 0, sizeof(float) * (feat_stride - feat_dim),
+                         num_nodes);
+    if (e != cudaSuccess) return cleanup(fail(GNN_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e)));
+    *out = g;
+    return GNN_OK;
+}
+
+gnn_status gnn_graph_destroy(gnn_graph* g) {
+    if (!g) return GNN_OK;
+    cudaSetDevice(g->dev);
+    for (void* p : g->owned) cudaFree(p);
+    delete g;
+    return GNN_OK;
+}
+
+gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model** out) {
+    if (!g || !cfg || !out) return fail(GNN_ERR_PARAM, "NULL argument");
+    *out = nullptr;
+    const gnn_model_config& c = *cfg;
+    if (c.model != GNN_SAGE_MEAN && c.model != GNN_GCN) return fail(GNN_ERR_CONFIG, "unknown model");
+    if (c.sampler != GNN_NEIGHBOR && c.sampler != GNN_SHADOW) return fail(GNN_ERR_CONFIG, "unknown sampler");
+    if (c.num_layers < 1 || c.num_layers > kMaxHops) return fail(GNN_ERR_CONFIG, "num_layers must be 1..8");
+    if (c.num_fanouts < 1 || c.num_fanouts > kMaxHops) return fail(GNN_ERR_CONFIG, "num_fanouts must be 1..8");
+    if (c.sampler == GNN_NEIGHBOR && c.num_fanouts != c.num_layers) return fail(GNN_ERR_CONFIG, "neighbour sampler needs num_fanouts == num_layers");
+    for (int i = 0; i < c.num_fanouts; ++i)
+        if (c.fanouts[i] < 1 || c.fanouts[i] > 32) return fail(GNN_ERR_CONFIG, "fanouts must be 1..32");
+    if (c.batch_size < 1 || c.batch_size > 1024) return fail(GNN_ERR_CONFIG, "batch_size must be 1..1024");
+    if (c.num_layers > 1 && (c.hidden < 16 || c.hidden % 16)) return fail(GNN_ERR_CONFIG, "hidden must be a positive multiple of 16");
+    if (c.precision != GNN_FP32 && c.precision != GNN_BF16_GEMM) return fail(GNN_ERR_CONFIG, "unknown precision");
+    if (!(c.lr >= 0.f)) return fail(GNN_ERR_PARAM, "lr must be >= 0");
+    TRY(set_device(g->dev));
+
+    auto* m = new gnn_model();
+    m->g = g; m->cfg = c;
+    m->L = c.num_layers; m->hops = c.num_fanouts;
+    m->sage = c.model == GNN_SAGE_MEAN; m->shadow = c.sampler == GNN_SHADOW;
+    m->slot = m->shadow ? m->hops : -1;
+    auto cleanup = [&](gnn_status s) { for (void* p : m->owned) cudaFree(p); delete m; return s; };
+    gnn_status s;
+#define AL(p, n) if ((s = dalloc(&(p), (n), m->owned)) != GNN_OK) return cleanup(s)
+
+    // ---- capacities
+    int64_t cap_dst = c.batch_size;
+    for (int h = 0; h < m->hops; ++h) {
+        HopBufs& b = m->hb[h];
+        const int k = c.fanouts[m->hops - 1 - h];
+        b.cap_dst = cap_dst;
+        b.cap_edges = cap_dst * k;
+        b.cap_src = std::min<int64_t>(g->N, cap_dst + b.cap_edges);
+        b.cap_src = std::max(b.cap_src, cap_dst);
+        b.need_t = !m->shadow && (!m->sage || h <= m->L - 2);
+        cap_dst = b.cap_src;
+    }
+    m->nodes_cap = m->hb[m->hops - 1].cap_src;
+    if (m->shadow) {
+        HopBufs& b = m->hb[m->slot];
+        b.cap_dst = b.cap_src = m->nodes_cap;
+        b.cap_edges = std::max<int64_t>(1, g->nnz);
+        b.need_t = true;
+    }
+    m->nwords = (g->N + 31) / 32;
+    m->tcap = m->nodes_cap + 1;
+    AL(m->st, 1);
+    AL(m->nodes, m->nodes_cap);
+    AL(m->map, g->N);
+    AL(m->bits, m->nwords);
+    AL(m->tcount, m->tcap);
+    AL(m->icount, m->nodes_cap);
+    AL(m->sc.partials, kScanBlocks);
+    AL(m->seeds_in, c.batch_size);
+    for (int h = 0; h <= m->hops; ++h) {
+        if (h == m->hops && !m->shadow) break;
+        HopBufs& b = m->hb[h];
+        AL(b.rowptr, b.cap_dst + 1);
+        AL(b.col, b.cap_edges);
+        if (h < m->hops) AL(b.nbr, b.cap_edges);
+        if (b.need_t) {
+            AL(b.trowptr, b.cap_src + 1);
+            AL(b.tcursor, b.cap_src + 1);
+            AL(b.tdst, b.cap_edges);
+            AL(b.tdst_s, b.cap_edges);
+        }
+    }
+    CK(cudaMemset(m->map, 0xff, sizeof(int32_t) * g->N));
+    CK(cudaMemset(m->bits, 0, sizeof(uint32_t) * m->nwords));
+    CK(cudaMemset(m->tcount, 0, sizeof(int32_t) * m->tcap));
+    CK(cudaMemset(m->st, 0, sizeof(StepState)));
+
+    // ---- layers
+    m->dims.push_back(g->F);
+    for (int l = 1; l < m->L; ++l) m->dims.push_back(c.hidden);
+    m->dims.push_back(g->C);
+    int64_t poff = 0;
+    for (int li = 0; li < m->L; ++li) {
+        Layer ly;
+        ly.in = m->dims[li];
+        ly.out = m->dims[li + 1];
+        ly.in_pad = (int)round_up(ly.in, 4);
+        ly.rows = (m->sage ? 2 : 1) * ly.in;
+        ly.k_pad = (m->sage ? 2 : 1) * ly.in_pad;
+        ly.n_pad = (int)round_up(ly.out, 16);
+        ly.poff = poff;
+        ly.pcnt = (int64_t)ly.rows * ly.out;
+        poff += ly.pcnt;
+        ly.blk = m->shadow ? m->slot : (m->hops - 1 - li);
+        ly.m_cap = m->shadow ? (li == m->L - 1 ? c.batch_size : m->nodes_cap) : m->hb[ly.blk].cap_dst;
+        ly.splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, ly.m_cap / 1024));
+        m->layers.push_back(ly);
+    }
+    m->pcount = poff;
+    for (int li = 0; li < m->L; ++li) {
+        Layer& ly = m->layers[li];
+        AL(ly.Wp, (int64_t)ly.k_pad * ly.n_pad);
+        AL(ly.A, ly.m_cap * ly.k_pad);
+        AL(ly.H, ly.m_cap * ly.n_pad);
+        AL(ly.dPre, ly.m_cap * ly.n_pad);
+        if (li > 0) AL(ly.dA, ly.m_cap * ly.k_pad);
+        AL(ly.wpart, (int64_t)ly.splits * ly.k_pad * ly.n_pad);
+    }
+    AL(m->params, m->pcount);
+    AL(m->grads, m->pcount);
+#undef AL
+    CK(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
+    m->stream = m->own_stream;
+    // ---- Glorot-uniform init (per layer block)
+    for (int li = 0; li < m->L; ++li) {
+        Layer& ly = m->layers[li];
+        const float bound = std::sqrt(6.0f / (float)(ly.in + ly.out));
+        launch_init_params(m->params + ly.poff, ly.pcnt, bound, c.init_seed, (uint32_t)li, m->stream);
+        launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad, ly.n_pad,
+                           ly.Wp, m->stream);
+    }
+    CK(cudaMemsetAsync(m->grads, 0, sizeof(float) * m->pcount, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    CK(cudaGetLastError());
+    *out = m;
+    return GNN_OK;
+}
+
+gnn_status gnn_model_destroy(gnn_model* m) {
+    if (!m) return GNN_OK;
+    cudaSetDevice(m->g->dev);
+    if (m->stream) cudaStreamSynchronize(m->stream);
+    drain_profile(m);
+    for (auto e : m->free_events) cudaEventDestroy(e);
+    if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    if (m->comm) ncclCommDestroy(m->comm);
+    for (void* p : m->owned) cudaFree(p);
+    if (m->cub_tmp) cudaFree(m->cub_tmp);
+    if (m->own_stream) cudaStreamDestroy(m->own_stream);
+    delete m;
+    return GNN_OK;
+}
+
+gnn_status gnn_set_stream(gnn_model* m, void* stream) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    TRY(set_device(m->g->dev));
+    CK(cudaStreamSynchronize(m->stream));
+    m->stream = stream ? (cudaStream_t)stream : m->own_stream;
+    return GNN_OK;
+}
+
+gnn_status gnn_set_train_nodes(gnn_model* m, const int32_t* ids_host, int64_t n) {
+    if (!m || n < 0 || (n > 0 && !ids_host)) return fail(GNN_ERR_PARAM, "bad arguments");
+    if (n >= INT32_MAX) return fail(GNN_ERR_PARAM, "too many train nodes");
+    std::vector<int32_t> ids(ids_host, ids_host + n);
+    std::sort(ids.begin(), ids.end());
+    for (int64_t i = 0; i < n; ++i) {
+        if (ids[i] < 0 || ids[i] >= m->g->N) return fail(GNN_ERR_RANGE, "train id out of range");
+        if (i && ids[i] == ids[i - 1]) return fail(GNN_ERR_PARAM, "duplicate train id");
+    }
+    TRY(set_device(m->g->dev));
+    CK(cudaStreamSynchronize(m->stream));
+    if (n > m->train_cap) {
+        for (void* p : {(void*)m->train_sorted, (void*)m->perm, (void*)m->keys, (void*)m->keys_alt, m->cub_tmp})
+            if (p) cudaFree(p);
+        CK(cudaMalloc(&m->train_sorted, sizeof(int32_t) * n));
+        CK(cudaMalloc(&m->perm, sizeof(int32_t) * n));
+        CK(cudaMalloc(&m->keys, sizeof(uint64_t) * n));
+        CK(cudaMalloc(&m->keys_alt, sizeof(uint64_t) * n));
+        m->cub_bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, m->cub_bytes, m->keys, m->keys_alt, m->train_sorted, m->perm,
+                                           (int)n, 0, 64, m->stream));
+        CK(cudaMalloc(&m->cub_tmp, m->cub_bytes));
+        m->train_cap = n;
+    }
+    if (n) CK(cudaMemcpy(m->train_sorted, ids.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    m->n_train = n;
+    m->perm_epoch = -1;
+    return GNN_OK;
+}
+
+int64_t gnn_param_count(const gnn_model* m) { return m ? m->pcount : -1; }
+int64_t gnn_num_batches(const gnn_model* m) { return m ? num_batches(m) : -1; }
+
+gnn_status gnn_get_params(gnn_model* m, float* out_host, int64_t n) {
+    if (!m || !out_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    if (n != m->pcount) return fail(GNN_ERR_SHAPE, "n != param_count");
+    TRY(set_device(m->g->dev));
+    CK(cudaMemcpyAsync(out_host, m->params, sizeof(float) * n, cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return GNN_OK;
+}
+
+gnn_status gnn_set_params(gnn_model* m, const float* in_host, int64_t n) {
+    if (!m || !in_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    if (n != m->pcount) return fail(GNN_ERR_SHAPE, "n != param_count");
+    TRY(set_device(m->g->dev));
+    CK(cudaMemcpyAsync(m->params, in_host, sizeof(float) * n, cudaMemcpyHostToDevice, m->stream));
+    for (auto& ly : m->layers)
+        launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad, ly.n_pad,
+                           ly.Wp, m->stream);
+    CK(cudaStreamSynchronize(m->stream));
+    return GNN_OK;
+}
+
+gnn_status gnn_comm_get_unique_id(uint8_t out_host[128]) {
+    if (!out_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    ncclUniqueId id;
+    CKN(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out_host, &id, 128);
+    return GNN_OK;
+}
+
+gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_t id_host[128]) {
+    if (!m || !id_host || world < 1 || rank < 0 || rank >= world) return fail(GNN_ERR_PARAM, "bad arguments");
+    TRY(set_device(m->g->dev));
+    if (m->comm) { ncclCommDestroy(m->comm); m->comm = nullptr; }
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, id_host, 128);
+        CKN(ncclCommInitRank(&m->comm, world, id, rank));
+    }
+    m->rank = rank;
+    m->world = world;
+    if (m->gexec) { cudaGraphExecDestroy(m->gexec); m->gexec = nullptr; }
+    return GNN_OK;
+}
+
+gnn_status gnn_epoch_permutation(gnn_model* m, int64_t epoch, int32_t* out_host, int64_t n) {
+    if (!m || (!out_host && m->n_train)) return fail(GNN_ERR_PARAM, "NULL argument");
+    if (n < m->n_train) return fail(GNN_ERR_BUFFER, "need n_train = " + std::to_string(m->n_train));
+    TRY(set_device(m->g->dev));
+    TRY(ensure_perm(m, epoch));
+    if (m->n_train)
+        CK(cudaMemcpyAsync(out_host, m->perm, sizeof(int32_t) * m->n_train, cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return GNN_OK;
+}
+
+gnn_status gnn_sample(gnn_model* m, int64_t epoch, int64_t g, gnn_batch_sizes* sizes_host) {
+    if (!m || !sizes_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    const int64_t nb = num_batches(m);
+    if (g < 0 || g >= nb) return fail(GNN_ERR_RANGE, "batch index out of range");
+    TRY(set_device(m->g->dev));
+    TRY(ensure_perm(m, epoch));
+    const int64_t B = m->cfg.batch_size;
+    const int32_t n = (int32_t)std::min<int64_t>(B, m->n_train - g * B);
+    launch_begin_step(m->st, m->perm + g * B, n, n, (uint32_t)epoch, (uint32_t)g, m->nodes, m->map, m->stream);
+    const bool prof = m->profiling;
+    m->profiling = false;
+    enqueue_sampling(m);
+    m->profiling = prof;
+    CK(cudaGetLastError());
+    StepState st;
+    CK(cudaMemcpyAsync(&st, m->st, sizeof(StepState), cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    sizes_host->num_hops = m->hops;
+    for (int h = 0; h <= kMaxHops; ++h) {
+        sizes_host->n_dst[h] = st.n_dst[h];
+        sizes_host->n_src[h] = st.n_src[h];
+        sizes_host->n_edges[h] = st.n_edges[h];
+    }
+    return GNN_OK;
+}
+
+gnn_status gnn_sample_fetch(gnn_model* m, int32_t hop, int32_t what, int32_t* out_host, int64_t n) {
+    if (!m || !out_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    const int maxhop = m->shadow ? m->hops : m->hops - 1;
+    if (hop < 0 || hop > maxhop) return fail(GNN_ERR_RANGE, "hop out of range");
+    TRY(set_device(m->g->dev));
+    StepState st;
+    CK(cudaMemcpyAsync(&st, m->st, sizeof(StepState), cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    const HopBufs& b = m->hb[hop];
+    int64_t len = 0;
+    const int32_t* src = nullptr;
+    switch (what) {
+        case GNN_SRC_IDS: len = st.n_src[hop]; src = m->nodes; break;
+        case GNN_BLK_ROWPTR: len = st.n_dst[hop] + 1; src = b.rowptr; break;
+        case GNN_BLK_COL: len = st.n_edges[hop]; src = b.col; break;
+        case GNN_BLK_NBR: len = st.n_edges[hop]; src = hop < m->hops ? b.nbr : b.col; break;
+        default: return fail(GNN_ERR_PARAM, "unknown array");
+    }
+    if (n < len) return fail(GNN_ERR_BUFFER, "buffer too small: need " + std::to_string(len));
+    if (len) CK(cudaMemcpy(out_host, src, sizeof(int32_t) * len, cudaMemcpyDeviceToHost));
+    if (what == GNN_BLK_NBR && hop == m->hops && len) {   // induced block: global id of each source
+        std::vector<int32_t> ids(st.n_src[hop]);
+        if (!ids.empty()) CK(cudaMemcpy(ids.data(), m->nodes, sizeof(int32_t) * ids.size(), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < len; ++i) out_host[i] = ids[out_host[i]];
+    }
+    return GNN_OK;
+}
+
+gnn_status gnn_train_minibatch(gnn_model* m, int64_t epoch, int64_t step, float* loss_out_host) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    if (step < 0 || epoch < 0) return fail(GNN_ERR_PARAM, "negative epoch/step");
+    TRY(set_device(m->g->dev));
+    TRY(begin_step_from_perm(m, epoch, step));
+    TRY(run_body(m));
+    if (loss_out_host) {
+        CK(cudaMemcpyAsync(loss_out_host, &m->st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+    }
+    return GNN_OK;
+}
+
+gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t n_seeds, int32_t b_total,
+                                int64_t epoch, int64_t g, float* loss_out_host) {
+    if (!m || (n_seeds > 0 && !seeds_host) || !loss_out_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    if (n_seeds < 0 || n_seeds > m->cfg.batch_size) return fail(GNN_ERR_SHAPE, "n_seeds must be 0..batch_size");
+    if (b_total < n_seeds) return fail(GNN_ERR_PARAM, "b_total < n_seeds");
+    TRY(set_device(m->g->dev));
+    if (n_seeds)
+        CK(cudaMemcpyAsync(m->seeds_in, seeds_host, sizeof(int32_t) * n_seeds, cudaMemcpyHostToDevice, m->stream));
+    launch_begin_step(m->st, m->seeds_in, n_seeds, b_total, (uint32_t)epoch, (uint32_t)g, m->nodes, m->map, m->stream);
+    TRY(run_body(m));
+    CK(cudaMemcpyAsync(loss_out_host, &m->st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return GNN_OK;
+}
+
+gnn_status gnn_train_epoch(gnn_model* m, int64_t epoch, gnn_epoch_stats* out_host) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    TRY(set_device(m->g->dev));
+    const int64_t nb = num_batches(m);
+    const int64_t steps = (nb + m->world - 1) / m->world;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    std::vector<float> losses(steps);
+    float* pinned = nullptr;
+    CK(cudaMallocHost(&pinned, sizeof(float) * std::max<int64_t>(steps, 1)));
+    CK(cudaEventRecord(e0, m->stream));
+    for (int64_t s = 0; s < steps; ++s) {
+        TRY(begin_step_from_perm(m, epoch, s));
+        TRY(run_body(m));
+        CK(cudaMemcpyAsync(pinned + s, &m->st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
+    }
+    CK(cudaEventRecord(e1, m->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    double tot = 0;
+    for (int64_t s = 0; s < steps; ++s) tot += pinned[s];
+    cudaFreeHost(pinned);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (out_host) {
+        out_host->seconds = ms * 1e-3;
+        out_host->steps = steps;
+        int64_t mine = 0;
+        for (int64_t s = 0; s < steps; ++s) mine += (s * m->world + m->rank) < nb;
+        out_host->minibatches = mine;
+        out_host->mean_loss = steps ? tot / (double)steps : 0.0;
+    }
+    return GNN_OK;
+}
+
+gnn_status gnn_synchronize(gnn_model* m) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    TRY(set_device(m->g->dev));
+    CK(cudaStreamSynchronize(m->stream));
+    return GNN_OK;
+}
+
+gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n) {
+    if (!m || !out_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    TRY(set_device(m->g->dev));
+    StepState st;
+    CK(cudaMemcpyAsync(&st, m->st, sizeof(StepState), cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    if (what == GNN_DBG_LOSS) {
+        if (n < 1) return fail(GNN_ERR_BUFFER, "need 1");
+        out_host[0] = st.loss;
+        return GNN_OK;
+    }
+    if (what == GNN_DBG_GRADS) {
+        if (n < m->pcount) return fail(GNN_ERR_BUFFER, "need param_count");
+        CK(cudaMemcpy(out_host, m->grads, sizeof(float) * m->pcount, cudaMemcpyDeviceToHost));
+        return GNN_OK;
+    }
+    if (what == GNN_DBG_LOGITS) {
+        const Layer& ly = m->layers[m->L - 1];
+        const int64_t need = (int64_t)st.batch_n * ly.out;
+        if (n < need) return fail(GNN_ERR_BUFFER, "need batch_n*C = " + std::to_string(need));
+        if (need)
+            CK(cudaMemcpy2D(out_host, sizeof(float) * ly.out, ly.H, sizeof(float) * ly.n_pad, sizeof(float) * ly.out,
+                            st.batch_n, cudaMemcpyDeviceToHost));
+        return GNN_OK;
+    }
+    if (what >= GNN_DBG_ACT && what < GNN_DBG_ACT + m->L) {
+        const int li = what - GNN_DBG_ACT;
+        const Layer& ly = m->layers[li];
+        const int rows = (m->shadow && li == m->L - 1) ? st.batch_n : st.n_dst[ly.blk];
+        const int64_t need = (int64_t)rows * ly.out;
+        if (n < need) return fail(GNN_ERR_BUFFER, "need rows*out = " + std::to_string(need));
+        if (need)
+            CK(cudaMemcpy2D(out_host, sizeof(float) * ly.out, ly.H, sizeof(float) * ly.n_pad, sizeof(float) * ly.out,
+                            rows, cudaMemcpyDeviceToHost));
+        return GNN_OK;
+    }
+    return fail(GNN_ERR_PARAM, "unknown debug array");
+}
+
+gnn_status gnn_last_sizes(gnn_model* m, gnn_batch_sizes* sizes_host) {
+    if (!m || !sizes_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    TRY(set_device(m->g->dev));
+    StepState st;
+    CK(cudaMemcpyAsync(&st, m->st, sizeof(StepState), cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    sizes_host->num_hops = m->hops;
+    for (int h = 0; h <= kMaxHops; ++h) {
+        sizes_host->n_dst[h] = st.n_dst[h];
+        sizes_host->n_src[h] = st.n_src[h];
+        sizes_host->n_edges[h] = st.n_edges[h];
+    }
+    return GNN_OK;
+}
+
+gnn_status gnn_profile_enable(gnn_model* m, int32_t enable) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    m->profiling = enable != 0;
+    return GNN_OK;
+}
+
+gnn_status gnn_profile_read(gnn_model* m, int32_t kid, double* ms_out_host, int64_t* launches_out_host) {
+    if (!m || kid < 0 || kid >= GNN_K_COUNT) return fail(GNN_ERR_PARAM, "bad arguments");
+    TRY(set_device(m->g->dev));
+    drain_profile(m);
+    if (ms_out_host) *ms_out_host = m->prof_ms[kid];
+    if (launches_out_host) *launches_out_host = m->prof_n[kid];
+    return GNN_OK;
+}
+
+gnn_status gnn_profile_reset(gnn_model* m) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    drain_profile(m);
+    for (int i = 0; i < GNN_K_COUNT; ++i) { m->prof_ms[i] = 0; m->prof_n[i] = 0; }
+    return GNN_OK;
+}
+
+int64_t gnn_launches_per_step(const gnn_model* m) { return m ? m->launches_per_step : -1; }
+
+}  // extern "C"

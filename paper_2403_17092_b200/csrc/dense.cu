@@ -1,0 +1,433 @@
+// Training side of the step, sm_100a: Â·H aggregation forward/backward (Eq. 1-2,
+// lines 131-142), dense update GEMMs, softmax cross-entropy + the Eq. (3) gradient (lines
+// 161-165), SGD.  All extents come from the device StepState (graph-replayable).
+#include <cub/block/block_reduce.cuh>
+
+#include "kernels.h"
+
+namespace gs {
+namespace {
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4fma(float w, float4 v, float4 a) {   // a + w*v, unfused order kept explicit
+    return make_float4(a.x + w * v.x, a.y + w * v.y, a.z + w * v.z, a.w + w * v.w);
+}
+__device__ __forceinline__ float4 f4div(float4 a, float d) {
+    return make_float4(a.x / d, a.y / d, a.z / d, a.w / d);
+}
+
+// ------------------------------------------------------------------ forward aggregation
+// Warp per destination row; lanes own 16-byte chunks of the feature row (CPL chunks each).
+// Neighbour indices are fetched 32 at a time by the warp and broadcast with shuffles; the
+// sum runs in CSR row order with plain fp32 adds, then a true division by the degree.
+template <int CPL>
+__global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ rows_ptr,
+        const float* __restrict__ H, int in_pad, const int32_t* __restrict__ gmap,
+        const int32_t* __restrict__ smap, const int32_t* __restrict__ rowptr,
+        const int32_t* __restrict__ col, float* __restrict__ A) {
+    const int n = *rows_ptr;
+    const int lane = lane_id();
+    const int nch = in_pad >> 2;
+    const int64_t lda = 2 * (int64_t)in_pad;
+    for (int i = global_warp(); i < n; i += total_warps()) {
+        const int beg = rowptr[i], end = rowptr[i + 1];
+        float4 acc[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e0 = beg; e0 < end; e0 += 32) {
+            const int m = min(32, end - e0);
+            int myidx = 0;
+            if (lane < m) { const int c = col[e0 + lane]; myidx = gmap ? gmap[c] : c; }
+            int q = 0;
+            for (; q + 2 <= m; q += 2) {
+                const int r0 = __shfl_sync(kFull, myidx, q), r1 = __shfl_sync(kFull, myidx, q + 1);
+                const float4* p0 = reinterpret_cast<const float4*>(H + (int64_t)r0 * in_pad);
+                const float4* p1 = reinterpret_cast<const float4*>(H + (int64_t)r1 * in_pad);
+                float4 v0[CPL], v1[CPL];
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    v0[c] = ch < nch ? __ldg(p0 + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    v1[c] = ch < nch ? __ldg(p1 + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) { acc[c] = f4add(acc[c], v0[c]); acc[c] = f4add(acc[c], v1[c]); }
+            }
+            if (q < m) {
+                const int r0 = __shfl_sync(kFull, myidx, q);
+                const float4* p0 = reinterpret_cast<const float4*>(H + (int64_t)r0 * in_pad);
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    if (ch < nch) acc[c] = f4add(acc[c], __ldg(p0 + ch));
+                }
+            }
+        }
+        const int deg = end - beg;
+        const int self = smap ? smap[i] : i;
+        const float4* ps = reinterpret_cast<const float4*>(H + (int64_t)self * in_pad);
+        float4* out = reinterpret_cast<float4*>(A + (int64_t)i * lda);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            if (ch < nch) {
+                out[ch] = __ldg(ps + ch);
+                out[nch + ch] = deg ? f4div(acc[c], (float)deg) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    }
+}
+
+// GCN: A[i] = Σ_e H[c_e] / sqrt(d_in(i) d_out(c_e)) + H[i] / sqrt(d_in(i) d_out(i)),
+// d_in(i) = deg(i) + 1, d_out(c) = outdeg_blk(c) + [c < n_dst]  (R12).
+template <int CPL>
+__global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ rows_ptr,
+        const int32_t* __restrict__ ndst_ptr, const float* __restrict__ H, int in_pad,
+        const int32_t* __restrict__ gmap, const int32_t* __restrict__ smap,
+        const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+        const int32_t* __restrict__ trowptr, float* __restrict__ A) {
+    const int n = *rows_ptr;
+    const int ndst = *ndst_ptr;
+    const int lane = lane_id();
+    const int nch = in_pad >> 2;
+    for (int i = global_warp(); i < n; i += total_warps()) {
+        const int beg = rowptr[i], end = rowptr[i + 1];
+        const float din = (float)(end - beg + 1);
+        float4 acc[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e0 = beg; e0 < end; e0 += 32) {
+            const int m = min(32, end - e0);
+            int myrow = 0;
+            float myw = 0.f;
+            if (lane < m) {
+                const int c = col[e0 + lane];
+                myrow = gmap ? gmap[c] : c;
+                const float dout = (float)(trowptr[c + 1] - trowptr[c] + (c < ndst ? 1 : 0));
+                myw = 1.0f / sqrtf(din * dout);
+            }
+            for (int q = 0; q < m; ++q) {
+                const int r = __shfl_sync(kFull, myrow, q);
+                const float w = __shfl_sync(kFull, myw, q);
+                const float4* p = reinterpret_cast<const float4*>(H + (int64_t)r * in_pad);
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    if (ch < nch) acc[c] = f4fma(w, __ldg(p + ch), acc[c]);
+                }
+            }
+        }
+        const float dself = (float)(trowptr[i + 1] - trowptr[i] + 1);
+        const float ws = 1.0f / sqrtf(din * dself);
+        const int self = smap ? smap[i] : i;
+        const float4* ps = reinterpret_cast<const float4*>(H + (int64_t)self * in_pad);
+        float4* out = reinterpret_cast<float4*>(A + (int64_t)i * in_pad);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            if (ch < nch) out[ch] = f4fma(ws, __ldg(ps + ch), acc[c]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ backward aggregation
+// dA rows >= dlim are not computed (ShaDow last layer: only the seeds' rows carry loss,
+// the exact receptive-field pruning of DESIGN.md R19) and contribute nothing.
+template <int CPL, bool GCN>
+__global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __restrict__ st,
+        const int32_t* __restrict__ dlim_ptr, const float* __restrict__ dA, int in_pad,
+        const int32_t* __restrict__ rowptr, const int32_t* __restrict__ trowptr,
+        const int32_t* __restrict__ tdst, const float* __restrict__ Hprev, float* __restrict__ dPre) {
+    const int nsrc = st->n_src[h];
+    const int ndst = st->n_dst[h];
+    const int dlim = *dlim_ptr;
+    const int lane = lane_id();
+    const int nch = in_pad >> 2;
+    const int64_t lda = GCN ? in_pad : 2 * (int64_t)in_pad;
+    const int moff = GCN ? 0 : nch;   // dM half of [dSelf | dM]
+    for (int u = global_warp(); u < nsrc; u += total_warps()) {
+        const int beg = trowptr[u], end = trowptr[u + 1];
+        const float dout = (float)(end - beg + (u < ndst ? 1 : 0));
+        float4 acc[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e0 = beg; e0 < end; e0 += 32) {
+            const int m = min(32, end - e0);
+            int myi = -1;
+            float myd = 1.f;
+            if (lane < m && tdst[e0 + lane] < dlim) {
+                myi = tdst[e0 + lane];
+                const float din = (float)(rowptr[myi + 1] - rowptr[myi] + (GCN ? 1 : 0));
+                myd = GCN ? 1.0f / sqrtf(din * dout) : din;
+            }
+            for (int q = 0; q < m; ++q) {
+                const int i = __shfl_sync(kFull, myi, q);
+                const float d = __shfl_sync(kFull, myd, q);
+                if (i < 0) continue;
+                const float4* p = reinterpret_cast<const float4*>(dA + (int64_t)i * lda) + moff;
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    if (ch < nch) {
+                        const float4 v = __ldg(p + ch);
+                        acc[c] = GCN ? f4fma(d, v, acc[c]) : f4add(acc[c], f4div(v, d));
+                    }
+                }
+            }
+        }
+        const float4* hp = reinterpret_cast<const float4*>(Hprev + (int64_t)u * in_pad);
+        const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
+        float4* out = reinterpret_cast<float4*>(dPre + (int64_t)u * in_pad);
+        float wself = 0.f;
+        if (GCN && u < dlim) {
+            const float din = (float)(rowptr[u + 1] - rowptr[u] + 1);
+            wself = 1.0f / sqrtf(din * dout);
+        }
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            if (ch < nch) {
+                float4 a = acc[c];
+                if (u < dlim) a = GCN ? f4fma(wself, __ldg(sp + ch), a) : f4add(a, __ldg(sp + ch));
+                const float4 hv = __ldg(hp + ch);   // ReLU'(pre) = [H > 0]  (ReLU'(0) = 0)
+                a.x = hv.x > 0.f ? a.x : 0.f; a.y = hv.y > 0.f ? a.y : 0.f;
+                a.z = hv.z > 0.f ? a.z : 0.f; a.w = hv.w > 0.f ? a.w : 0.f;
+                out[ch] = a;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ SIMT fp32 GEMM
+// 64x64 output tile, BK = 16, 256 threads x (4x4).  Exact fp32 FFMA path.
+template <bool TA, bool TB, bool RELU>
+__global__ void __launch_bounds__(256) k_gemm(const int32_t* m_ptr, int m_static, int N,
+        const int32_t* k_ptr, int k_static, const float* __restrict__ A, int lda,
+        const float* __restrict__ B, int ldb, float* __restrict__ C, int ldc, int64_t split_stride) {
+    const int M = m_ptr ? *m_ptr : m_static;
+    const int K = k_ptr ? *k_ptr : k_static;
+    const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+    if (m0 >= M && !k_ptr) return;
+    const int splits = gridDim.z;
+    const int kc = ((K + splits - 1) / splits + 15) / 16 * 16;
+    const int kb = blockIdx.z * kc;
+    const int ke = min(K, kb + kc);
+    C += blockIdx.z * split_stride;
+    __shared__ float As[16][64 + 4];
+    __shared__ float Bs[16][64 + 4];
+    const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+    float acc[4][4] = {};
+    for (int k0 = kb; k0 < ke; k0 += 16) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int idx = t + 256 * r;
+            int mm, kk;
+            if (TA) { kk = idx >> 6; mm = idx & 63; } else { mm = idx >> 4; kk = idx & 15; }
+            const int gm = m0 + mm, gk = k0 + kk;
+            float v = 0.f;
+            if (gm < M && gk < ke) v = TA ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk];
+            As[kk][mm] = v;
+            int nn;
+            if (TB) { nn = idx >> 4; kk = idx & 15; } else { kk = idx >> 6; nn = idx & 63; }
+            const int gn = n0 + nn, gk2 = k0 + kk;
+            float w = 0.f;
+            if (gn < N && gk2 < ke) w = TB ? B[(int64_t)gn * ldb + gk2] : B[(int64_t)gk2 * ldb + gn];
+            Bs[kk][nn] = w;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { a[i] = As[kk][ty * 4 + i]; b[i] = Bs[kk][tx * 4 + i]; }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gm = m0 + ty * 4 + i;
+        if (gm >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gn = n0 + tx * 4 + j;
+            if (gn < N) C[(int64_t)gm * ldc + gn] = RELU ? fmaxf(acc[i][j], 0.f) : acc[i][j];
+        }
+    }
+}
+
+__global__ void k_wgrad_reduce(const float* __restrict__ part, int splits, int64_t split_stride,
+                               int rows, int out, int in, int in_pad, bool sage, int n_pad,
+                               float* __restrict__ grads) {
+    const int64_t total = (int64_t)rows * out;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
+         f += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(f / out), c = (int)(f % out);
+        const int rp = sage ? (r / in) * in_pad + (r % in) : r;
+        float s = 0.f;
+        for (int z = 0; z < splits; ++z) s += part[z * split_stride + (int64_t)rp * n_pad + c];
+        grads[f] = s;
+    }
+}
+
+__global__ void k_pack_weight(const float* __restrict__ W, int rows, int out, int in, int in_pad,
+                              bool sage, int k_pad, int n_pad, float* __restrict__ Wp) {
+    const int64_t total = (int64_t)k_pad * n_pad;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
+         f += (int64_t)gridDim.x * blockDim.x) {
+        const int rp = (int)(f / n_pad), c = (int)(f % n_pad);
+        int r = -1;
+        if (sage) { const int half = rp / in_pad, j = rp % in_pad; if (j < in && half < 2) r = half * in + j; }
+        else if (rp < in) r = rp;
+        Wp[f] = (r >= 0 && c < out) ? W[(int64_t)r * out + c] : 0.f;
+    }
+}
+
+// ------------------------------------------------------------------ softmax cross-entropy
+// One block; warp w takes rows w, w+32, ...  ℓ_i = max + log Σ exp(z - max) - z_y.
+// Loss = Σ ℓ_i / b_total summed in a fixed order (deterministic).
+__global__ void __launch_bounds__(1024) k_ce(StepState* st, const float* __restrict__ Z, int ldz, int C,
+                                             const int32_t* __restrict__ labels,
+                                             const int32_t* __restrict__ nodes, float* __restrict__ dZ) {
+    __shared__ float wsum[32];
+    const int b = st->batch_n;
+    const float inv_bt = 1.0f / (float)max(st->b_total, 1);
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    float mine = 0.f;
+    for (int r = w; r < b; r += 32) {
+        const float* z = Z + (int64_t)r * ldz;
+        float m = -INFINITY;
+        for (int c = lane; c < C; c += 32) m = fmaxf(m, z[c]);
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+        float s = 0.f;
+        for (int c = lane; c < C; c += 32) s += expf(z[c] - m);
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+        const int y = labels[nodes[r]];
+        const float lse = m + logf(s);
+        float* dz = dZ + (int64_t)r * ldz;
+        for (int c = lane; c < ldz; c += 32) {
+            float v = 0.f;
+            if (c < C) v = (expf(z[c] - m) / s - (c == y ? 1.f : 0.f)) * inv_bt;
+            dz[c] = v;
+        }
+        mine += lse - z[y];
+    }
+    if (lane == 0) wsum[w] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float tot = 0.f;
+        for (int i = 0; i < 32; ++i) tot += wsum[i];
+        st->loss = tot * inv_bt;
+    }
+}
+
+__global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = p[i] - lr * g[i];
+}
+
+__global__ void k_init(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = method_draw(seed, 4u, layer, (uint32_t)(i >> 32), 0u, 0u, (uint32_t)i);
+        const float u = (float)(r >> 8) * (1.0f / 16777216.0f);
+        p[i] = (2.f * u - 1.f) * bound;
+    }
+}
+
+int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
+}  // namespace
+
+#define GS_CPL_DISPATCH(cpl, KERNEL, ...)                                           \
+    switch (cpl) {                                                                  \
+        case 1: KERNEL<1><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
+        case 2: KERNEL<2><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
+        case 3: KERNEL<3><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
+        case 4: KERNEL<4><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
+        case 5: KERNEL<5><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
+        case 6: KERNEL<6><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
+        case 7: KERNEL<7><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
+        default: KERNEL<8><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;           \
+    }
+
+void launch_agg_sage(const int32_t* rows_ptr, const float* H, int in_pad, const int32_t* gmap,
+                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, float* A,
+                     cudaStream_t s) {
+    GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A);
+}
+
+void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const float* H, int in_pad,
+                    const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
+                    const int32_t* col, const int32_t* trowptr, float* A, cudaStream_t s) {
+    GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_gcn, rows_ptr, ndst_ptr, H, in_pad, gmap, smap, blk_rowptr,
+                    col, trowptr, A);
+}
+
+template <bool GCN>
+static void spmm_bwd(int h, const StepState* st, const int32_t* dlim, const float* dA, int in_pad,
+                     const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
+                     const float* H_prev, float* dPre_prev, cudaStream_t s) {
+    switch (cpl_of(in_pad)) {
+        case 1: k_spmm_bwd<1, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+        case 2: k_spmm_bwd<2, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+        case 3: k_spmm_bwd<3, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+        default: k_spmm_bwd<4, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+    }
+}
+
+void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, const float* dA,
+                     int in_pad, const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
+                     const float* H_prev, float* dPre_prev, cudaStream_t s) {
+    if (gcn) spmm_bwd<true>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
+    else spmm_bwd<false>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
+}
+
+void launch_gemm(bool transA, bool transB, bool relu, const int32_t* m_ptr, int m_static, int m_cap,
+                 int n, const int32_t* k_ptr, int k_static, const float* A, int lda, const float* B,
+                 int ldb, float* C, int ldc, int splits, int64_t split_stride, cudaStream_t s) {
+    dim3 grid((n + 63) / 64, (m_cap + 63) / 64, splits);
+#define GS_GEMM(TA, TB, R) k_gemm<TA, TB, R><<<grid, 256, 0, s>>>(m_ptr, m_static, n, k_ptr, k_static, A, lda, B, ldb, C, ldc, split_stride)
+    if (!transA && !transB) { if (relu) GS_GEMM(false, false, true); else GS_GEMM(false, false, false); }
+    else if (!transA && transB) GS_GEMM(false, true, false);
+    else if (transA && !transB) GS_GEMM(true, false, false);
+    else GS_GEMM(true, true, false);
+#undef GS_GEMM
+}
+
+void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, int rows, int out, int in,
+                         int in_pad, bool sage, int n_pad, float* grads, cudaStream_t s) {
+    const int64_t total = (int64_t)rows * out;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+    k_wgrad_reduce<<<blocks, 256, 0, s>>>(part, splits, split_stride, rows, out, in, in_pad, sage, n_pad, grads);
+}
+
+void launch_pack_weight(const float* W, int rows, int out, int in, int in_pad, bool sage, int k_pad,
+                        int n_pad, float* Wp, cudaStream_t s) {
+    const int64_t total = (int64_t)k_pad * n_pad;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+    k_pack_weight<<<blocks, 256, 0, s>>>(W, rows, out, in, in_pad, sage, k_pad, n_pad, Wp);
+}
+
+void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,
+               float* dZ, cudaStream_t s) {
+    k_ce<<<1, 1024, 0, s>>>(st, Z, ldz, C, labels, nodes, dZ);
+}
+
+void launch_sgd(float* params, const float* grads, int64_t n, float lr, cudaStream_t s) {
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+    k_sgd<<<blocks, 256, 0, s>>>(params, grads, n, lr);
+}
+
+void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer, cudaStream_t s) {
+    const int blocks = (int)std::min<int64_t>((cnt + 255) / 256, 148 * 4);
+    k_init<<<blocks, 256, 0, s>>>(p, cnt, bound, seed, layer);
+}
+
+}  // namespace gs

@@ -1,0 +1,86 @@
+// Host-side launchers of the sm_100a kernels (internal to libgnnstep.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+
+namespace gs {
+
+// ------------------------------------------------------------------ sampling side (sample.cu)
+struct ScanScratch { int32_t* partials; };   // kScanBlocks ints
+constexpr int kScanBlocks = 296;             // 2 x 148 SMs
+constexpr int kWarpGrid = 148 * 16;          // blocks of 256 threads for warp-per-item kernels
+
+// Epoch permutation keys (Philox tag 1): keys[i] = (w0<<32)|w1 of (train[i], 0, epoch).
+void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t epoch,
+                      uint64_t* keys, cudaStream_t s);
+// Start of a step: state fields, seeds -> nodes[0:n), map[seed] = i.
+void launch_begin_step(StepState* st, const int32_t* seed_src, int32_t n, int32_t b_total,
+                       uint32_t epoch, uint32_t g, int32_t* nodes, int32_t* map, cudaStream_t s);
+// Hop h: counts min(deg, k) -> blk_rowptr (exclusive scan), n_edges[h].
+void launch_hop_rowptr(int h, int k, StepState* st, const int32_t* nodes, const int64_t* row_ptr,
+                       int32_t* blk_rowptr, ScanScratch sc, cudaStream_t s);
+// Hop h: Floyd k-of-d per dst node (warp per node), blk_nbr, bitmap of unseen nbrs.
+void launch_sample_fill(int h, int k, const StepState* st, const int32_t* nodes,
+                        const int64_t* row_ptr, const int32_t* col, const int32_t* blk_rowptr,
+                        int32_t* blk_nbr, const int32_t* map, uint32_t* bits, uint64_t seed,
+                        cudaStream_t s);
+// Hop h: new nodes in ascending global id (bitmap rank), nodes[n_dst + r], map, n_src.
+void launch_assign_new(int h, StepState* st, uint32_t* bits, int64_t nwords, int32_t* nodes,
+                       int32_t* map, ScanScratch sc, cudaStream_t s);
+// Hop h: blk_col[e] = map[blk_nbr[e]]; optional transposed counts.
+void launch_relabel_edges(int h, const StepState* st, const int32_t* blk_nbr, int32_t* blk_col,
+                          const int32_t* map, int32_t* tcount, cudaStream_t s);
+// Transposed block CSR (rows = local src ids), deterministic (ascending dst index).
+void launch_transpose(int h, StepState* st, const int32_t* blk_rowptr, const int32_t* blk_col,
+                      int32_t* tcount, int32_t* trowptr, int32_t* tcursor, int32_t* tdst,
+                      int32_t* tdst_sorted, ScanScratch sc, cudaStream_t s);
+// ShaDow: induced block over S = nodes[0:n_src[hs]] -> state slot `slot`.
+void launch_induce(int hs, int slot, StepState* st, const int32_t* nodes, const int64_t* row_ptr,
+                   const int32_t* col, const int32_t* map, int32_t* icount, int32_t* ind_rowptr,
+                   int32_t* ind_col, int32_t* tcount, ScanScratch sc, cudaStream_t s);
+// map[nodes[i]] = -1 for i < n_src[h].
+void launch_reset_map(int h, const StepState* st, const int32_t* nodes, int32_t* map, cudaStream_t s);
+
+// ------------------------------------------------------------------ training side (dense.cu)
+// Layouts: activations are row-major fp32 with row stride =
+// padded width (in_pad = roundup(in, 4); GEMM N padded to 16).  GEMM operand A_l has
+// K_pad = 2*in_pad (SAGE: [H_self | mean]) or in_pad (GCN: Â H) columns.
+
+// SAGE-mean aggregation into A = [H_self | mean] for rows i < *rows_ptr.  Neighbour row of
+// source c is gmap ? gmap[c] : c, self row smap ? smap[i] : i (layer 1 reads X by global id:
+// the fused feature gather).
+void launch_agg_sage(const int32_t* rows_ptr, const float* H, int in_pad, const int32_t* gmap,
+                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, float* A,
+                     cudaStream_t s);
+// GCN aggregation A = Â H (self loop included) for rows i < *rows_ptr of a block with
+// *ndst_ptr destinations; d_out from the transposed row pointer.  col must be local ids.
+void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const float* H, int in_pad,
+                    const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
+                    const int32_t* col, const int32_t* trowptr, float* A, cudaStream_t s);
+// C[M x N] = op(A)[M x K] op(B)[K x N] (+ReLU), fp32.  M = *m_ptr if non-null (dynamic rows),
+// K = *k_ptr if non-null (dynamic reduction, split over gridDim.z into C + z*split_stride).
+void launch_gemm(bool transA, bool transB, bool relu, const int32_t* m_ptr, int m_static,
+                 int m_cap, int n, const int32_t* k_ptr, int k_static, const float* A, int lda,
+                 const float* B, int ldb, float* C, int ldc, int splits, int64_t split_stride,
+                 cudaStream_t s);
+// grads[off + r*out + c] = Σ_z part[z][rpad(r)*n_pad + c]   (fixed z order; unpads rows/cols)
+void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, int rows, int out,
+                         int in, int in_pad, bool sage, int n_pad, float* grads, cudaStream_t s);
+// Wp[K_pad x N_pad] from flat W (rows x out), zero padding.
+void launch_pack_weight(const float* W, int rows, int out, int in, int in_pad, bool sage,
+                        int k_pad, int n_pad, float* Wp, cudaStream_t s);
+// Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total.
+void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels,
+               const int32_t* nodes, float* dZ, cudaStream_t s);
+// Backward aggregation over the transposed block (atomic-free, fixed order), u < n_src[h]:
+//   SAGE: dPre_prev[u] = ([u<dlim] dA[u,:in_pad] + Σ_{e in T(u), dst<dlim} dA[dst, in_pad:]/deg(dst)) * [H_prev[u]>0]
+//   GCN:  dPre_prev[u] = (Â^T dA)[u] * [H_prev[u] > 0]   (dA rows < dlim)
+void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, const float* dA,
+                     int in_pad, const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
+                     const float* H_prev, float* dPre_prev, cudaStream_t s);
+void launch_sgd(float* params, const float* grads, int64_t n, float lr, cudaStream_t s);
+void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer,
+                        cudaStream_t s);
+
+}  // namespace gs

@@ -1,0 +1,93 @@
+"""Helpers for the -m gpu parity tests: build the CUDA path and the oracle on the same
+seeded inputs (gnn_inputs), compare element by element."""
+import numpy as np
+
+from gnn_inputs import WORKLOADS, build_inputs
+
+TOL_FP32 = 1e-4     # BASELINE.json north_star: fp32 loss/logits/grads within 1e-4 relative
+TOL_BF16 = 2e-2     # bf16-GEMM variant
+
+
+def rel(a, b):
+    """DESIGN.md R24: per-tensor ||gpu - oracle||_2 / ||oracle||_2."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+_cache = {}
+
+
+def inputs_for(name):
+    if name not in _cache:
+        w = WORKLOADS[name]
+        inp = build_inputs(w)
+        graph = dict(row_ptr=inp["row_ptr"], col=inp["col"], X=inp["X"][:, :w.feat_dim],
+                     y=inp["y"], train=inp["train"])
+        _cache.clear()
+        _cache[name] = (w, inp, graph)
+    return _cache[name]
+
+
+def make_gpu(w, inp, use_graph=True, precision="fp32", batch_size=None, params=None):
+    from paper_2403_17092_b200 import Graph, Model
+    g = Graph(inp["row_ptr"], inp["col"], inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim)
+    m = Model(g, model=w.model, sampler=w.sampler, num_layers=w.num_layers, hidden=w.hidden,
+              batch_size=batch_size or w.batch_size, fanouts=w.fanouts, precision=precision,
+              use_graph=use_graph, lr=w.lr, seed=w.sampler_seed, init_seed=w.init_seed)
+    m.set_train_nodes(inp["train"])
+    m.set_params(inp["params"] if params is None else params)
+    return g, m
+
+
+def assert_blocks_equal(gpu_hops, ora_hops):
+    assert len(gpu_hops) == len(ora_hops)
+    for h, (a, b) in enumerate(zip(gpu_hops, ora_hops)):
+        for k in ("n_dst", "n_src", "n_edges"):
+            assert a[k] == b[k], (h, k, a[k], b[k])
+        for k in ("src_ids", "blk_rowptr", "blk_col", "blk_nbr"):
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), (h, k)
+
+
+def kink_override(m, cache, w, rows_limit=None):
+    """Reading R27: the ReLU mask is a floating-point decision.  Where the GPU's decision
+    (sign of its H^(l)) differs from the oracle's, the unit must be kink-ambiguous:
+    |Pre| <= 1e-5 * (|A| |W|)_uj, i.e. inside the fp32 rounding error of the GEMM; there
+    both decisions are correct results.  Returns the validated GPU decisions as an oracle
+    mask override, and how many units differed."""
+    ovr, n = {}, 0
+    for li in range(w.num_layers - 1):
+        Pre = cache["Pre"][li]
+        rows, out = Pre.shape
+        H = m.activation(li, rows, out)
+        gpu_pos = H > 0
+        r, c = np.nonzero(gpu_pos != (Pre > 0))
+        if r.size:
+            S = (np.abs(cache["A"][li][r]) @ np.abs(cache["Ws"][li]))[np.arange(r.size), c]
+            assert np.all(np.abs(Pre[r, c]) <= 1e-5 * S), \
+                ("ReLU decision differs at a unit that is not kink-ambiguous", li, np.abs(Pre[r, c]).max())
+            ovr[li] = (r, c, gpu_pos[r, c])
+            n += r.size
+    return ovr, n
+
+
+def check_train_step(m, w, graph, params, epoch, step, perm, loss, tol=TOL_FP32):
+    """Compare one GPU step (already run) with the oracle step from `params` (the oracle's
+    own trajectory).  Returns the oracle result (its params continue the trajectory)."""
+    import oracle
+    from oracle import sampling as OS
+    out = oracle.train_step(w, graph, params, epoch, step, 1, perm=perm, keep_cache=True)
+    b = len(OS.batch_seeds(perm, w.batch_size, step))
+    err = dict(loss=abs(loss - out["loss"]) / abs(out["loss"]),
+               logits=rel(m.logits(b, w.num_classes), out["logits"][0]))
+    ovr, nflip = kink_override(m, out["caches"][0], w)
+    gref = out["grad"]
+    if nflip:
+        gref = oracle.train_step(w, graph, params, epoch, step, 1, perm=perm, mask_override=[ovr])["grad"]
+    err["grad"] = rel(m.grads(), gref)
+    for k, v in err.items():
+        assert v <= tol, (step, k, v, nflip)
+    out["errors"], out["kink_flips"] = err, nflip
+    out["caches"] = None
+    return out

@@ -1,0 +1,58 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU, and exports every symbol
+include/gnnstep.h declares (no compute calls here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gnnstep.h")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(gnn_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ["gnn_graph_create", "gnn_model_create", "gnn_sample", "gnn_train_minibatch",
+              "gnn_train_epoch", "gnn_get_params", "gnn_set_params", "gnn_comm_init",
+              "gnn_train_batch_host"]:
+        assert s in syms
+
+
+def test_library_loads_and_exports_every_symbol():
+    from paper_2403_17092_b200 import lib
+    L = lib()
+    for s in declared_symbols():
+        assert hasattr(L, s), s
+    assert L.gnn_abi_version() == 1
+    path = L._name
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    for s in declared_symbols():
+        assert re.search(rf"\bT {s}\b", out), s
+
+
+def test_library_is_sm100a():
+    from paper_2403_17092_b200 import lib
+    path = lib()._name
+    out = subprocess.run(["cuobjdump", "--list-elf", path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_oracle_not_linked_into_product():
+    """The product library and binding never reference the oracle."""
+    from paper_2403_17092_b200 import lib
+    path = lib()._name
+    out = subprocess.run(["nm", "-D", path], capture_output=True, text=True).stdout
+    assert "oracle_" not in out
+    pkg = os.path.join(ROOT, "paper_2403_17092_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f

@@ -1,0 +1,54 @@
+"""Full-size parity (BASELINE.json configs[1..3]) in the launch configuration bench.py times
+(CUDA graph replay, batch 1024): sampling bit-exact on sampled batches (first, second,
+middle, ragged last), training steps within 1e-4 of the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import sampling as OS
+from tests.gpu_common import (TOL_FP32, assert_blocks_equal, check_train_step, inputs_for, make_gpu,
+                              rel)
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+CASES = {
+    "products": dict(batches=(0, 1, 96, 192), steps=3),
+    "reddit": dict(batches=(0, 1, 75, 149), steps=2),
+    "products_shadow": dict(batches=(0, 192), steps=1),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fullsize_sampling_bitexact(name):
+    w, inp, graph = inputs_for(name)
+    g, m = make_gpu(w, inp)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    for b in CASES[name]["batches"]:
+        want, _ = oracle.sample_batch(w, graph, 0, b, perm)
+        got = m.sample(0, b)
+        if w.sampler == "shadow":
+            assert_blocks_equal(got[0], want[0])
+            assert_blocks_equal([got[1]], [want[1]])
+        else:
+            assert_blocks_equal(got, want)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fullsize_training_parity(name):
+    w, inp, graph = inputs_for(name)
+    g, m = make_gpu(w, inp)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    params = inp["params"].astype(np.float64)
+    for step in range(CASES[name]["steps"]):
+        loss = m.train_minibatch(0, step)
+        out = check_train_step(m, w, graph, params, 0, step, perm, loss)
+        print(name, step, out["errors"], "kink flips", out["kink_flips"])
+        params = out["params"]
+        assert rel(m.get_params(), params) <= TOL_FP32
+    # ragged last batch through the end-to-end host call, from the initial params
+    last = w.n_batches - 1
+    seeds = OS.batch_seeds(perm, w.batch_size, last)
+    m.set_params(inp["params"])
+    loss = m.train_batch_host(seeds, len(seeds), 0, last)
+    out = check_train_step(m, w, graph, inp["params"], 0, last, perm, loss)
+    print(name, "ragged", out["errors"], "kink flips", out["kink_flips"])
