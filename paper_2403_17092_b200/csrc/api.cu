@@ -88,7 +88,10 @@ struct Layer {
     int blk = 0;           // block (hop or ShaDow slot) this layer aggregates over
     int64_t m_cap = 0;     // max rows of this layer's output
     int splits = 1;
-    float *Wp = nullptr, *A = nullptr, *H = nullptr, *dPre = nullptr, *dA = nullptr, *wpart = nullptr;
+    int64_t rows_alloc = 0;  // operand-plane rows (m_cap rounded to the 128-row GEMM tile)
+    Split A{}, dPre{}, Wkn{}, Wnk{};   // bf16 split planes (GEMM operands)
+    float *H = nullptr, *dA = nullptr, *wpart = nullptr;
+    TcGemmMaps map_fwd{}, map_dgrad{}, map_wgrad{};
 };
 
 struct ProfPair { int kid; cudaEvent_t a, b; };
@@ -124,6 +127,7 @@ struct gnn_model {
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
 
+    bool bf16x3 = true;            // fp32 parity mode: 3-term bf16 split GEMMs
     cudaGraphExec_t gexec = nullptr;
     int64_t launches_per_step = 0;
 
@@ -234,13 +238,14 @@ void enqueue_training(gnn_model* m) {
             });
         } else {
             K(m, kid, [&] {
-                launch_agg_gcn(rows, &m->st->n_dst[ly.blk], Hin, ly.in_pad, li == 0 ? m->nodes : nullptr,
+                launch_agg_gcn(rows, &m->st->n_dst[ly.blk], Hin, ly.in_pad, ly.k_pad, li == 0 ? m->nodes : nullptr,
                                li == 0 ? m->nodes : nullptr, b.rowptr, b.col, b.trowptr, ly.A, s);
             });
         }
+        // Pre = A W (+ReLU) -> H (fp32)
         K(m, GNN_K_GEMM_FWD, [&] {
-            launch_gemm(false, false, li < L - 1, rows, 0, (int)ly.m_cap, ly.n_pad, nullptr, ly.k_pad, ly.A,
-                        ly.k_pad, ly.Wp, ly.n_pad, ly.H, ly.n_pad, 1, 0, s);
+            launch_gemm_tc(0, m->bf16x3, ly.map_fwd, rows, 0, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, ly.n_pad,
+                           ly.n_pad, li < L - 1, 1, 0, s);
         });
     }
     // ---- loss
@@ -251,16 +256,18 @@ void enqueue_training(gnn_model* m) {
         Layer& ly = m->layers[li];
         const int32_t* rows = rows_ptr(m, li);
         const int64_t stride = (int64_t)ly.k_pad * ly.n_pad;
+        // dW = A^T dPre (deterministic split over rows) -> grads
         K(m, GNN_K_GEMM_WGRAD, [&] {
-            launch_gemm(true, false, false, nullptr, ly.k_pad, ly.k_pad, ly.n_pad, rows, 0, ly.A, ly.k_pad,
-                        ly.dPre, ly.n_pad, ly.wpart, ly.n_pad, ly.splits, stride, s);
+            launch_gemm_tc(1, m->bf16x3, ly.map_wgrad, rows, ly.k_pad, ly.k_pad, ly.n_pad, 0, ly.wpart, ly.n_pad,
+                           ly.n_pad, false, ly.splits, stride, s);
             launch_wgrad_reduce(ly.wpart, ly.splits, stride, ly.rows, ly.out, ly.in, ly.in_pad, m->sage,
                                 ly.n_pad, m->grads + ly.poff, s);
         });
         if (li == 0) break;
+        // dA = dPre W^T (fp32)
         K(m, GNN_K_GEMM_DGRAD, [&] {
-            launch_gemm(false, true, false, rows, 0, (int)ly.m_cap, ly.k_pad, nullptr, ly.n_pad, ly.dPre,
-                        ly.n_pad, ly.Wp, ly.n_pad, ly.dA, ly.k_pad, 1, 0, s);
+            launch_gemm_tc(0, m->bf16x3, ly.map_dgrad, rows, 0, (int)ly.m_cap, ly.k_pad, ly.n_pad, ly.dA, ly.k_pad,
+                           ly.k_pad, false, 1, 0, s);
         });
         Layer& prev = m->layers[li - 1];
         HopBufs& b = m->hb[ly.blk];
@@ -278,7 +285,7 @@ void enqueue_training(gnn_model* m) {
     for (auto& ly : m->layers)
         K(m, GNN_K_OTHER, [&] {
             launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad,
-                               ly.n_pad, ly.Wp, s);
+                               ly.n_pad, ly.Wkn, ly.Wnk, s);
         });
 }
 
@@ -436,6 +443,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     m->L = c.num_layers; m->hops = c.num_fanouts;
     m->sage = c.model == GNN_SAGE_MEAN; m->shadow = c.sampler == GNN_SHADOW;
     m->slot = m->shadow ? m->hops : -1;
+    m->bf16x3 = c.precision == GNN_FP32;
     auto cleanup = [&](gnn_status s) { for (void* p : m->owned) cudaFree(p); delete m; return s; };
     gnn_status s;
 #define AL(p, n) if ((s = dalloc(&(p), (n), m->owned)) != GNN_OK) return cleanup(s)
@@ -498,7 +506,8 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         ly.out = m->dims[li + 1];
         ly.in_pad = (int)round_up(ly.in, 4);
         ly.rows = (m->sage ? 2 : 1) * ly.in;
-        ly.k_pad = (m->sage ? 2 : 1) * ly.in_pad;
+        // GEMM reduction width; a multiple of 8 so bf16 rows are 16-byte strided (TMA)
+        ly.k_pad = m->sage ? 2 * ly.in_pad : (int)round_up(ly.in_pad, 8);
         ly.n_pad = (int)round_up(ly.out, 16);
         ly.poff = poff;
         ly.pcnt = (int64_t)ly.rows * ly.out;
@@ -511,12 +520,38 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     m->pcount = poff;
     for (int li = 0; li < m->L; ++li) {
         Layer& ly = m->layers[li];
-        AL(ly.Wp, (int64_t)ly.k_pad * ly.n_pad);
-        AL(ly.A, ly.m_cap * ly.k_pad);
+        ly.rows_alloc = round_up(ly.m_cap, 128);
+        const bool x3 = m->bf16x3;
+        auto split = [&](Split& sp, int64_t count) -> gnn_status {
+            gnn_status r = dalloc(&sp.hi, count, m->owned);
+            if (r == GNN_OK && x3) r = dalloc(&sp.lo, count, m->owned);
+            if (r == GNN_OK) { cudaMemset(sp.hi, 0, 2 * count); if (sp.lo) cudaMemset(sp.lo, 0, 2 * count); }
+            return r;
+        };
+        if ((s = split(ly.A, ly.rows_alloc * ly.k_pad)) != GNN_OK) return cleanup(s);
+        if ((s = split(ly.dPre, ly.rows_alloc * ly.n_pad)) != GNN_OK) return cleanup(s);
+        if ((s = split(ly.Wkn, (int64_t)ly.k_pad * ly.n_pad)) != GNN_OK) return cleanup(s);
+        if ((s = split(ly.Wnk, (int64_t)ly.k_pad * ly.n_pad)) != GNN_OK) return cleanup(s);
         AL(ly.H, ly.m_cap * ly.n_pad);
-        AL(ly.dPre, ly.m_cap * ly.n_pad);
         if (li > 0) AL(ly.dA, ly.m_cap * ly.k_pad);
         AL(ly.wpart, (int64_t)ly.splits * ly.k_pad * ly.n_pad);
+        // TMA descriptors (128B swizzle) of this layer's three GEMMs
+        auto lo_or_hi = [](const Split& sp) { return sp.lo ? (const void*)sp.lo : (const void*)sp.hi; };
+        bool ok = true;
+        const int bn_f = tc_tile_n(ly.n_pad), bn_d = tc_tile_n(ly.k_pad);
+        ok &= make_tmap_bf16(&ly.map_fwd.a_hi, ly.A.hi, ly.rows_alloc, ly.k_pad, 128);
+        ok &= make_tmap_bf16(&ly.map_fwd.a_lo, lo_or_hi(ly.A), ly.rows_alloc, ly.k_pad, 128);
+        ok &= make_tmap_bf16(&ly.map_fwd.b_hi, ly.Wnk.hi, ly.n_pad, ly.k_pad, bn_f);
+        ok &= make_tmap_bf16(&ly.map_fwd.b_lo, lo_or_hi(ly.Wnk), ly.n_pad, ly.k_pad, bn_f);
+        ok &= make_tmap_bf16(&ly.map_dgrad.a_hi, ly.dPre.hi, ly.rows_alloc, ly.n_pad, 128);
+        ok &= make_tmap_bf16(&ly.map_dgrad.a_lo, lo_or_hi(ly.dPre), ly.rows_alloc, ly.n_pad, 128);
+        ok &= make_tmap_bf16(&ly.map_dgrad.b_hi, ly.Wkn.hi, ly.k_pad, ly.n_pad, bn_d);
+        ok &= make_tmap_bf16(&ly.map_dgrad.b_lo, lo_or_hi(ly.Wkn), ly.k_pad, ly.n_pad, bn_d);
+        ok &= make_tmap_bf16(&ly.map_wgrad.a_hi, ly.A.hi, ly.rows_alloc, ly.k_pad, 64);
+        ok &= make_tmap_bf16(&ly.map_wgrad.a_lo, lo_or_hi(ly.A), ly.rows_alloc, ly.k_pad, 64);
+        ok &= make_tmap_bf16(&ly.map_wgrad.b_hi, ly.dPre.hi, ly.rows_alloc, ly.n_pad, 64);
+        ok &= make_tmap_bf16(&ly.map_wgrad.b_lo, lo_or_hi(ly.dPre), ly.rows_alloc, ly.n_pad, 64);
+        if (!ok) return cleanup(fail(GNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(li)));
     }
     AL(m->params, m->pcount);
     AL(m->grads, m->pcount);
@@ -529,7 +564,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         const float bound = std::sqrt(6.0f / (float)(ly.in + ly.out));
         launch_init_params(m->params + ly.poff, ly.pcnt, bound, c.init_seed, (uint32_t)li, m->stream);
         launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad, ly.n_pad,
-                           ly.Wp, m->stream);
+                           ly.Wkn, ly.Wnk, m->stream);
     }
     CK(cudaMemsetAsync(m->grads, 0, sizeof(float) * m->pcount, m->stream));
     CK(cudaStreamSynchronize(m->stream));
@@ -610,7 +645,7 @@ gnn_status gnn_set_params(gnn_model* m, const float* in_host, int64_t n) {
     CK(cudaMemcpyAsync(m->params, in_host, sizeof(float) * n, cudaMemcpyHostToDevice, m->stream));
     for (auto& ly : m->layers)
         launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad, ly.n_pad,
-                           ly.Wp, m->stream);
+                           ly.Wkn, ly.Wnk, m->stream);
     CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }

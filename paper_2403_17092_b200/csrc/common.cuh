@@ -18,7 +18,9 @@ struct StepState {
     uint32_t epoch;
     uint32_t g;           // global batch index (sampling key, R3)
     float loss;           // this rank's Σ ℓ_i / b_total
-    int32_t pad[3];
+    uint32_t ce_done;     // CE blocks finished (reset by the last one)
+    int32_t pad[2];
+    float row_loss[1024]; // ℓ_i of the batch rows (batch_size <= 1024)
 };
 
 // Philox4x32-10 (R3): the method's counter-based draws.

@@ -1,6 +1,7 @@
 // Training side of the step, sm_100a: Â·H aggregation forward/backward (Eq. 1-2,
-// lines 131-142), dense update GEMMs, softmax cross-entropy + the Eq. (3) gradient (lines
-// 161-165), SGD.  All extents come from the device StepState (graph-replayable).
+// lines 131-142), softmax cross-entropy + the Eq. (3) gradient (lines 161-165), weight
+// packing for the tensor-core GEMMs (gemm_tc.cu), SGD.  All extents come from the device
+// StepState (graph-replayable).  GEMM operands are written as bf16 split planes.
 #include <cub/block/block_reduce.cuh>
 
 #include "kernels.h"
@@ -12,12 +13,35 @@ constexpr unsigned kFull = 0xffffffffu;
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
     return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
-__device__ __forceinline__ float4 f4fma(float w, float4 v, float4 a) {   // a + w*v, unfused order kept explicit
+__device__ __forceinline__ float4 f4fma(float w, float4 v, float4 a) {   // a + w*v
     return make_float4(a.x + w * v.x, a.y + w * v.y, a.z + w * v.z, a.w + w * v.w);
 }
 __device__ __forceinline__ float4 f4div(float4 a, float d) {
     return make_float4(a.x / d, a.y / d, a.z / d, a.w / d);
 }
+__device__ __forceinline__ uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
+    return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+}
+// x = hi + lo + O(2^-16 |x|):  hi = bf16_rn(x), lo = bf16_rn(x - hi)
+__device__ __forceinline__ void store_split4(const Split& o, int64_t idx, float4 v) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(v.x), h1 = __float2bfloat16_rn(v.y);
+    const __nv_bfloat16 h2 = __float2bfloat16_rn(v.z), h3 = __float2bfloat16_rn(v.w);
+    *reinterpret_cast<uint2*>(o.hi + idx) = make_uint2(pack2(h0, h1), pack2(h2, h3));
+    if (o.lo) {
+        const __nv_bfloat16 l0 = __float2bfloat16_rn(v.x - __bfloat162float(h0));
+        const __nv_bfloat16 l1 = __float2bfloat16_rn(v.y - __bfloat162float(h1));
+        const __nv_bfloat16 l2 = __float2bfloat16_rn(v.z - __bfloat162float(h2));
+        const __nv_bfloat16 l3 = __float2bfloat16_rn(v.w - __bfloat162float(h3));
+        *reinterpret_cast<uint2*>(o.lo + idx) = make_uint2(pack2(l0, l1), pack2(l2, l3));
+    }
+}
+__device__ __forceinline__ void store_split1(const Split& o, int64_t idx, float v) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    o.hi[idx] = h;
+    if (o.lo) o.lo[idx] = __float2bfloat16_rn(v - __bfloat162float(h));
+}
+__device__ __forceinline__ int round64(int n) { return (n + 63) & ~63; }
+constexpr float4 kZero4 = {0.f, 0.f, 0.f, 0.f};
 
 // ------------------------------------------------------------------ forward aggregation
 // Warp per destination row; lanes own 16-byte chunks of the feature row (CPL chunks each).
@@ -27,16 +51,21 @@ template <int CPL>
 __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ rows_ptr,
         const float* __restrict__ H, int in_pad, const int32_t* __restrict__ gmap,
         const int32_t* __restrict__ smap, const int32_t* __restrict__ rowptr,
-        const int32_t* __restrict__ col, float* __restrict__ A) {
+        const int32_t* __restrict__ col, Split A) {
     const int n = *rows_ptr;
+    const int nr = round64(n);
     const int lane = lane_id();
     const int nch = in_pad >> 2;
     const int64_t lda = 2 * (int64_t)in_pad;
-    for (int i = global_warp(); i < n; i += total_warps()) {
+    for (int i = global_warp(); i < nr; i += total_warps()) {
+        if (i >= n) {                                   // zero tail rows of the operand planes
+            for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, i * lda + 4 * ch, kZero4);
+            continue;
+        }
         const int beg = rowptr[i], end = rowptr[i + 1];
         float4 acc[CPL];
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
         for (int e0 = beg; e0 < end; e0 += 32) {
             const int m = min(32, end - e0);
             int myidx = 0;
@@ -50,8 +79,8 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
-                    v0[c] = ch < nch ? __ldg(p0 + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    v1[c] = ch < nch ? __ldg(p1 + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    v0[c] = ch < nch ? __ldg(p0 + ch) : kZero4;
+                    v1[c] = ch < nch ? __ldg(p1 + ch) : kZero4;
                 }
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) { acc[c] = f4add(acc[c], v0[c]); acc[c] = f4add(acc[c], v1[c]); }
@@ -69,13 +98,12 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
         const int deg = end - beg;
         const int self = smap ? smap[i] : i;
         const float4* ps = reinterpret_cast<const float4*>(H + (int64_t)self * in_pad);
-        float4* out = reinterpret_cast<float4*>(A + (int64_t)i * lda);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
             if (ch < nch) {
-                out[ch] = __ldg(ps + ch);
-                out[nch + ch] = deg ? f4div(acc[c], (float)deg) : make_float4(0.f, 0.f, 0.f, 0.f);
+                store_split4(A, i * lda + 4 * ch, __ldg(ps + ch));
+                store_split4(A, i * lda + 4 * (nch + ch), deg ? f4div(acc[c], (float)deg) : kZero4);
             }
         }
     }
@@ -85,20 +113,25 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
 // d_in(i) = deg(i) + 1, d_out(c) = outdeg_blk(c) + [c < n_dst]  (R12).
 template <int CPL>
 __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ rows_ptr,
-        const int32_t* __restrict__ ndst_ptr, const float* __restrict__ H, int in_pad,
+        const int32_t* __restrict__ ndst_ptr, const float* __restrict__ H, int in_pad, int lda,
         const int32_t* __restrict__ gmap, const int32_t* __restrict__ smap,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-        const int32_t* __restrict__ trowptr, float* __restrict__ A) {
+        const int32_t* __restrict__ trowptr, Split A) {
     const int n = *rows_ptr;
+    const int nr = round64(n);
     const int ndst = *ndst_ptr;
     const int lane = lane_id();
     const int nch = in_pad >> 2;
-    for (int i = global_warp(); i < n; i += total_warps()) {
+    for (int i = global_warp(); i < nr; i += total_warps()) {
+        if (i >= n) {
+            for (int ch = lane; ch < (lda >> 2); ch += 32) store_split4(A, (int64_t)i * lda + 4 * ch, kZero4);
+            continue;
+        }
         const int beg = rowptr[i], end = rowptr[i + 1];
         const float din = (float)(end - beg + 1);
         float4 acc[CPL];
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
         for (int e0 = beg; e0 < end; e0 += 32) {
             const int m = min(32, end - e0);
             int myrow = 0;
@@ -124,11 +157,10 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
         const float ws = 1.0f / sqrtf(din * dself);
         const int self = smap ? smap[i] : i;
         const float4* ps = reinterpret_cast<const float4*>(H + (int64_t)self * in_pad);
-        float4* out = reinterpret_cast<float4*>(A + (int64_t)i * in_pad);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
-            if (ch < nch) out[ch] = f4fma(ws, __ldg(ps + ch), acc[c]);
+            if (ch < nch) store_split4(A, (int64_t)i * lda + 4 * ch, f4fma(ws, __ldg(ps + ch), acc[c]));
         }
     }
 }
@@ -140,20 +172,25 @@ template <int CPL, bool GCN>
 __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __restrict__ st,
         const int32_t* __restrict__ dlim_ptr, const float* __restrict__ dA, int in_pad,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ trowptr,
-        const int32_t* __restrict__ tdst, const float* __restrict__ Hprev, float* __restrict__ dPre) {
+        const int32_t* __restrict__ tdst, const float* __restrict__ Hprev, Split dPre) {
     const int nsrc = st->n_src[h];
+    const int nr = round64(nsrc);
     const int ndst = st->n_dst[h];
     const int dlim = *dlim_ptr;
     const int lane = lane_id();
     const int nch = in_pad >> 2;
     const int64_t lda = GCN ? in_pad : 2 * (int64_t)in_pad;
     const int moff = GCN ? 0 : nch;   // dM half of [dSelf | dM]
-    for (int u = global_warp(); u < nsrc; u += total_warps()) {
+    for (int u = global_warp(); u < nr; u += total_warps()) {
+        if (u >= nsrc) {
+            for (int ch = lane; ch < nch; ch += 32) store_split4(dPre, (int64_t)u * in_pad + 4 * ch, kZero4);
+            continue;
+        }
         const int beg = trowptr[u], end = trowptr[u + 1];
         const float dout = (float)(end - beg + (u < ndst ? 1 : 0));
         float4 acc[CPL];
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
         for (int e0 = beg; e0 < end; e0 += 32) {
             const int m = min(32, end - e0);
             int myi = -1;
@@ -180,7 +217,6 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
         }
         const float4* hp = reinterpret_cast<const float4*>(Hprev + (int64_t)u * in_pad);
         const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
-        float4* out = reinterpret_cast<float4*>(dPre + (int64_t)u * in_pad);
         float wself = 0.f;
         if (GCN && u < dlim) {
             const float din = (float)(rowptr[u + 1] - rowptr[u] + 1);
@@ -195,73 +231,13 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
                 const float4 hv = __ldg(hp + ch);   // ReLU'(pre) = [H > 0]  (ReLU'(0) = 0)
                 a.x = hv.x > 0.f ? a.x : 0.f; a.y = hv.y > 0.f ? a.y : 0.f;
                 a.z = hv.z > 0.f ? a.z : 0.f; a.w = hv.w > 0.f ? a.w : 0.f;
-                out[ch] = a;
+                store_split4(dPre, (int64_t)u * in_pad + 4 * ch, a);
             }
         }
     }
 }
 
-// ------------------------------------------------------------------ SIMT fp32 GEMM
-// 64x64 output tile, BK = 16, 256 threads x (4x4).  Exact fp32 FFMA path.
-template <bool TA, bool TB, bool RELU>
-__global__ void __launch_bounds__(256) k_gemm(const int32_t* m_ptr, int m_static, int N,
-        const int32_t* k_ptr, int k_static, const float* __restrict__ A, int lda,
-        const float* __restrict__ B, int ldb, float* __restrict__ C, int ldc, int64_t split_stride) {
-    const int M = m_ptr ? *m_ptr : m_static;
-    const int K = k_ptr ? *k_ptr : k_static;
-    const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-    if (m0 >= M && !k_ptr) return;
-    const int splits = gridDim.z;
-    const int kc = ((K + splits - 1) / splits + 15) / 16 * 16;
-    const int kb = blockIdx.z * kc;
-    const int ke = min(K, kb + kc);
-    C += blockIdx.z * split_stride;
-    __shared__ float As[16][64 + 4];
-    __shared__ float Bs[16][64 + 4];
-    const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-    float acc[4][4] = {};
-    for (int k0 = kb; k0 < ke; k0 += 16) {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int idx = t + 256 * r;
-            int mm, kk;
-            if (TA) { kk = idx >> 6; mm = idx & 63; } else { mm = idx >> 4; kk = idx & 15; }
-            const int gm = m0 + mm, gk = k0 + kk;
-            float v = 0.f;
-            if (gm < M && gk < ke) v = TA ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk];
-            As[kk][mm] = v;
-            int nn;
-            if (TB) { nn = idx >> 4; kk = idx & 15; } else { kk = idx >> 6; nn = idx & 63; }
-            const int gn = n0 + nn, gk2 = k0 + kk;
-            float w = 0.f;
-            if (gn < N && gk2 < ke) w = TB ? B[(int64_t)gn * ldb + gk2] : B[(int64_t)gk2 * ldb + gn];
-            Bs[kk][nn] = w;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-            float a[4], b[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { a[i] = As[kk][ty * 4 + i]; b[i] = Bs[kk][tx * 4 + i]; }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int gm = m0 + ty * 4 + i;
-        if (gm >= M) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gn = n0 + tx * 4 + j;
-            if (gn < N) C[(int64_t)gm * ldc + gn] = RELU ? fmaxf(acc[i][j], 0.f) : acc[i][j];
-        }
-    }
-}
-
+// ------------------------------------------------------------------ weights, reduce, SGD
 __global__ void k_wgrad_reduce(const float* __restrict__ part, int splits, int64_t split_stride,
                                int rows, int out, int in, int in_pad, bool sage, int n_pad,
                                float* __restrict__ grads) {
@@ -276,8 +252,8 @@ __global__ void k_wgrad_reduce(const float* __restrict__ part, int splits, int64
     }
 }
 
-__global__ void k_pack_weight(const float* __restrict__ W, int rows, int out, int in, int in_pad,
-                              bool sage, int k_pad, int n_pad, float* __restrict__ Wp) {
+__global__ void k_pack_weight(const float* __restrict__ W, int rows, int out, int in, int in_pad, bool sage,
+                              int k_pad, int n_pad, Split Wkn, Split Wnk) {
     const int64_t total = (int64_t)k_pad * n_pad;
     for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
          f += (int64_t)gridDim.x * blockDim.x) {
@@ -285,22 +261,30 @@ __global__ void k_pack_weight(const float* __restrict__ W, int rows, int out, in
         int r = -1;
         if (sage) { const int half = rp / in_pad, j = rp % in_pad; if (j < in && half < 2) r = half * in + j; }
         else if (rp < in) r = rp;
-        Wp[f] = (r >= 0 && c < out) ? W[(int64_t)r * out + c] : 0.f;
+        const float v = (r >= 0 && c < out) ? W[(int64_t)r * out + c] : 0.f;
+        store_split1(Wkn, f, v);
+        store_split1(Wnk, (int64_t)c * k_pad + rp, v);
     }
 }
 
 // ------------------------------------------------------------------ softmax cross-entropy
-// One block; warp w takes rows w, w+32, ...  ℓ_i = max + log Σ exp(z - max) - z_y.
-// Loss = Σ ℓ_i / b_total summed in a fixed order (deterministic).
-__global__ void __launch_bounds__(1024) k_ce(StepState* st, const float* __restrict__ Z, int ldz, int C,
-                                             const int32_t* __restrict__ labels,
-                                             const int32_t* __restrict__ nodes, float* __restrict__ dZ) {
-    __shared__ float wsum[32];
+// Warp per row.  ℓ_i = max + log Σ exp(z - max) - z_y;  dZ = (softmax - onehot) / b_total.
+// The last block to finish sums the row losses in row order (deterministic).
+__global__ void __launch_bounds__(256) k_ce(StepState* st, const float* __restrict__ Z, int ldz, int C,
+                                            const int32_t* __restrict__ labels, const int32_t* __restrict__ nodes,
+                                            Split dZ, float* __restrict__ row_loss, uint32_t* __restrict__ done) {
+    using BR = cub::BlockReduce<float, 256>;
+    __shared__ typename BR::TempStorage tmp;
+    __shared__ bool last;
     const int b = st->batch_n;
+    const int br = round64(b);
     const float inv_bt = 1.0f / (float)max(st->b_total, 1);
-    const int lane = lane_id(), w = threadIdx.x >> 5;
-    float mine = 0.f;
-    for (int r = w; r < b; r += 32) {
+    const int lane = lane_id();
+    for (int r = global_warp(); r < br; r += total_warps()) {
+        if (r >= b) {
+            for (int c = lane; c < ldz; c += 32) store_split1(dZ, (int64_t)r * ldz + c, 0.f);
+            continue;
+        }
         const float* z = Z + (int64_t)r * ldz;
         float m = -INFINITY;
         for (int c = lane; c < C; c += 32) m = fmaxf(m, z[c]);
@@ -309,21 +293,25 @@ __global__ void __launch_bounds__(1024) k_ce(StepState* st, const float* __restr
         for (int c = lane; c < C; c += 32) s += expf(z[c] - m);
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
         const int y = labels[nodes[r]];
-        const float lse = m + logf(s);
-        float* dz = dZ + (int64_t)r * ldz;
         for (int c = lane; c < ldz; c += 32) {
             float v = 0.f;
             if (c < C) v = (expf(z[c] - m) / s - (c == y ? 1.f : 0.f)) * inv_bt;
-            dz[c] = v;
+            store_split1(dZ, (int64_t)r * ldz + c, v);
         }
-        mine += lse - z[y];
+        if (lane == 0) row_loss[r] = (m + logf(s)) - z[y];
     }
-    if (lane == 0) wsum[w] = mine;
+    __threadfence();
     __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    float part = 0.f;
+    for (int r = threadIdx.x; r < b; r += 256) part += row_loss[r];
+    const float tot = BR(tmp).Sum(part);
     if (threadIdx.x == 0) {
-        float tot = 0.f;
-        for (int i = 0; i < 32; ++i) tot += wsum[i];
         st->loss = tot * inv_bt;
+        *done = 0u;
     }
 }
 
@@ -358,22 +346,22 @@ int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
     }
 
 void launch_agg_sage(const int32_t* rows_ptr, const float* H, int in_pad, const int32_t* gmap,
-                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, float* A,
+                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A,
                      cudaStream_t s) {
     GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A);
 }
 
-void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const float* H, int in_pad,
+void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const float* H, int in_pad, int lda,
                     const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
-                    const int32_t* col, const int32_t* trowptr, float* A, cudaStream_t s) {
-    GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_gcn, rows_ptr, ndst_ptr, H, in_pad, gmap, smap, blk_rowptr,
+                    const int32_t* col, const int32_t* trowptr, Split A, cudaStream_t s) {
+    GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_gcn, rows_ptr, ndst_ptr, H, in_pad, lda, gmap, smap, blk_rowptr,
                     col, trowptr, A);
 }
 
 template <bool GCN>
 static void spmm_bwd(int h, const StepState* st, const int32_t* dlim, const float* dA, int in_pad,
                      const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
-                     const float* H_prev, float* dPre_prev, cudaStream_t s) {
+                     const float* H_prev, Split dPre_prev, cudaStream_t s) {
     switch (cpl_of(in_pad)) {
         case 1: k_spmm_bwd<1, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
         case 2: k_spmm_bwd<2, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
@@ -384,21 +372,9 @@ static void spmm_bwd(int h, const StepState* st, const int32_t* dlim, const floa
 
 void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, const float* dA,
                      int in_pad, const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
-                     const float* H_prev, float* dPre_prev, cudaStream_t s) {
+                     const float* H_prev, Split dPre_prev, cudaStream_t s) {
     if (gcn) spmm_bwd<true>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
     else spmm_bwd<false>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
-}
-
-void launch_gemm(bool transA, bool transB, bool relu, const int32_t* m_ptr, int m_static, int m_cap,
-                 int n, const int32_t* k_ptr, int k_static, const float* A, int lda, const float* B,
-                 int ldb, float* C, int ldc, int splits, int64_t split_stride, cudaStream_t s) {
-    dim3 grid((n + 63) / 64, (m_cap + 63) / 64, splits);
-#define GS_GEMM(TA, TB, R) k_gemm<TA, TB, R><<<grid, 256, 0, s>>>(m_ptr, m_static, n, k_ptr, k_static, A, lda, B, ldb, C, ldc, split_stride)
-    if (!transA && !transB) { if (relu) GS_GEMM(false, false, true); else GS_GEMM(false, false, false); }
-    else if (!transA && transB) GS_GEMM(false, true, false);
-    else if (transA && !transB) GS_GEMM(true, false, false);
-    else GS_GEMM(true, true, false);
-#undef GS_GEMM
 }
 
 void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, int rows, int out, int in,
@@ -409,15 +385,15 @@ void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, in
 }
 
 void launch_pack_weight(const float* W, int rows, int out, int in, int in_pad, bool sage, int k_pad,
-                        int n_pad, float* Wp, cudaStream_t s) {
+                        int n_pad, Split Wkn, Split Wnk, cudaStream_t s) {
     const int64_t total = (int64_t)k_pad * n_pad;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-    k_pack_weight<<<blocks, 256, 0, s>>>(W, rows, out, in, in_pad, sage, k_pad, n_pad, Wp);
+    k_pack_weight<<<blocks, 256, 0, s>>>(W, rows, out, in, in_pad, sage, k_pad, n_pad, Wkn, Wnk);
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,
-               float* dZ, cudaStream_t s) {
-    k_ce<<<1, 1024, 0, s>>>(st, Z, ldz, C, labels, nodes, dZ);
+               Split dZ, cudaStream_t s) {
+    k_ce<<<128, 256, 0, s>>>(st, Z, ldz, C, labels, nodes, dZ, st->row_loss, &st->ce_done);
 }
 
 void launch_sgd(float* params, const float* grads, int64_t n, float lr, cudaStream_t s) {

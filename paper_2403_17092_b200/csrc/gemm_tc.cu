@@ -1,0 +1,369 @@
+// Dense update GEMMs of the step on the 5th-generation tensor cores (sm_100a):
+// TMA (cp.async.bulk.tensor, 128B swizzle) -> shared memory -> tcgen05.mma (kind::f16, bf16
+// operands, fp32 accumulator in TMEM) -> tcgen05.ld -> fp32 epilogue (+ReLU).
+//
+// fp32 parity (north_star: 1e-4) uses a 3-term bf16 split: x = x_hi + x_lo with
+// x_hi = bf16(x), x_lo = bf16(x - x_hi); D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in
+// fp32 (relative error ~ 2^-16 per product).  The bf16 variant
+// (GNN_BF16_GEMM) issues the A_hi B_hi term only.
+//
+// Three uses:
+//   fwd   Pre = A W         A: [M x K] K-major,   B = W^T [N x K] K-major      (+ReLU)
+//   dgrad dA  = dPre W^T    A: [M x N] K-major,   B = W   [K x N] K-major
+//   wgrad dW  = A^T dPre    A^T: MN-major,        B = dPre MN-major, split over M (deterministic)
+// Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer, warps 2..5 =
+// epilogue (one TMEM lane quarter each).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+
+namespace gs {
+namespace {
+
+constexpr int kBM = 128;     // UMMA M (cta_group::1)
+constexpr int kBK = 64;      // bf16 elements per 128-byte swizzle row
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start>>4 [0,14),
+// LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48), layout SWIZZLE_128B (2) [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// Instruction descriptor, kind::f16: D f32, A/B bf16, majors, N>>3, M>>4.
+template <int BN, bool A_MN, bool B_MN>
+__host__ __device__ constexpr uint32_t idesc() {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
+           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+}
+
+template <int BN>
+struct TileCfg {
+    static constexpr int kAStage = kBM * kBK * 2;                 // 16 KB per plane
+    static constexpr int kBStage = ((BN + 63) / 64) * 64 * kBK * 2;  // rounded to whole 64-wide boxes (MN-major)
+    static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    // bytes one stage's TMA boxes deliver (OOB parts are zero-filled but still counted)
+    static constexpr int kBBytesK = BN * kBK * 2;                     // K-major: box {64, BN}
+    static constexpr int kBBytesMN = ((BN + 63) / 64) * 64 * kBK * 2; // MN-major: boxes {64, 64}
+};
+
+struct GemmArgs {
+    const int32_t* m_ptr;   // fwd/dgrad: rows of C (dynamic); wgrad: reduction length (dynamic)
+    int m_static;
+    int k_blocks;           // fwd/dgrad: reduction in 64-blocks (static)
+    int n_store;            // columns of C to store
+    float* C;
+    int ldc;
+    int relu;
+    int64_t split_stride;   // wgrad: C + blockIdx.z * split_stride
+};
+
+// MODE 0 = fwd/dgrad (A, B K-major; tile (m = blockIdx.x, n = blockIdx.y)),
+// MODE 1 = wgrad (A, B MN-major; tile (m' = blockIdx.x over K_pad, n = blockIdx.y), split z).
+template <int BN, int STAGES, int TERMS, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
+          const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo, GemmArgs args) {
+    using Cfg = TileCfg<BN>;
+    constexpr bool MN = MODE == 1;
+    constexpr int kAPlanes = TERMS == 3 ? 2 : 1;
+    constexpr int kStageBytes = kAPlanes * (Cfg::kAStage + Cfg::kBStage);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_full;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile_m = blockIdx.x * kBM;
+    const int tile_n = blockIdx.y * BN;
+
+    // ---- work extent
+    int kb_begin = 0, kb_end = args.k_blocks;
+    int m_rows = args.m_static;
+    if (MODE == 0) {
+        m_rows = args.m_ptr ? *args.m_ptr : args.m_static;
+        if (tile_m >= m_rows) return;
+    } else {
+        const int M = *args.m_ptr;                          // reduction length (rows of A and dPre)
+        const int nkb = (M + kBK - 1) / kBK;
+        const int per = (nkb + gridDim.z - 1) / gridDim.z;
+        kb_begin = min(nkb, (int)blockIdx.z * per);
+        kb_end = min(nkb, kb_begin + per);
+    }
+    const int nkb = kb_end - kb_begin;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+        mbar_init(&tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(Cfg::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == 0) {
+        // ================= TMA producer
+        if (lane == 0) {
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % STAGES;
+                if (i >= STAGES) mbar_wait(&empty_bar[s], ((i / STAGES) - 1) & 1);
+                uint8_t* st = smem + s * kStageBytes;
+                uint8_t* a_hi = st;
+                uint8_t* b_hi = st + Cfg::kAStage;
+                uint8_t* a_lo = st + Cfg::kAStage + Cfg::kBStage;
+                uint8_t* b_lo = a_lo + Cfg::kAStage;
+                mbar_expect_tx(&full_bar[s], kAPlanes * (Cfg::kAStage + (MN ? Cfg::kBBytesMN : Cfg::kBBytesK)));
+                const int k0 = (kb_begin + i) * kBK;
+                if (MODE == 0) {
+                    // K-major: box {64 (k), rows}
+                    tma_load_2d(a_hi, &mA_hi, &full_bar[s], k0, tile_m);
+                    tma_load_2d(b_hi, &mB_hi, &full_bar[s], k0, tile_n);
+                    if (TERMS == 3) {
+                        tma_load_2d(a_lo, &mA_lo, &full_bar[s], k0, tile_m);
+                        tma_load_2d(b_lo, &mB_lo, &full_bar[s], k0, tile_n);
+                    }
+                } else {
+                    // MN-major: boxes {64 (mn), 64 (k rows)}, 64-wide MN blocks 8 KB apart
+#pragma unroll
+                    for (int j = 0; j < kBM / 64; ++j) {
+                        tma_load_2d(a_hi + j * 8192, &mA_hi, &full_bar[s], tile_m + 64 * j, k0);
+                        if (TERMS == 3) tma_load_2d(a_lo + j * 8192, &mA_lo, &full_bar[s], tile_m + 64 * j, k0);
+                    }
+#pragma unroll
+                    for (int j = 0; j < (BN + 63) / 64; ++j) {
+                        tma_load_2d(b_hi + j * 8192, &mB_hi, &full_bar[s], tile_n + 64 * j, k0);
+                        if (TERMS == 3) tma_load_2d(b_lo + j * 8192, &mB_lo, &full_bar[s], tile_n + 64 * j, k0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer (one thread)
+        if (lane == 0) {
+            constexpr uint32_t id = idesc<BN, MN, MN>();
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&full_bar[s], (i / STAGES) & 1);
+                tc_fence_after();
+                uint8_t* st = smem + s * kStageBytes;
+                const uint32_t a_hi = smem_u32(st), b_hi = smem_u32(st + Cfg::kAStage);
+                const uint32_t a_lo = smem_u32(st + Cfg::kAStage + Cfg::kBStage);
+                const uint32_t b_lo = a_lo + Cfg::kAStage;
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                    // K-major: +32 B per 16-element k step inside the 128 B swizzle row;
+                    // MN-major: +16 rows x 128 B per k step.
+                    const uint32_t off = MN ? kk * 2048 : kk * 32;
+                    const uint32_t lbo = MN ? 8192 : 16, sbo = 1024;
+                    const uint64_t dah = sdesc(a_hi + off, lbo, sbo), dbh = sdesc(b_hi + off, lbo, sbo);
+                    const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
+                    tc_mma(tmem, dah, dbh, id, acc0);
+                    if (TERMS == 3) {
+                        const uint64_t dal = sdesc(a_lo + off, lbo, sbo), dbl = sdesc(b_lo + off, lbo, sbo);
+                        tc_mma(tmem, dah, dbl, id, 1u);
+                        tc_mma(tmem, dal, dbh, id, 1u);
+                    }
+                }
+                tc_commit(&empty_bar[s]);
+            }
+            tc_commit(&tmem_full);
+        }
+    } else {
+        // ================= epilogue: TMEM -> registers -> fp32 global (+ReLU)
+        const int q = warp & 3;                       // TMEM lane quarter this warp may access
+        const int row = tile_m + q * 32 + lane;
+        float* Cbase = args.C + (MODE == 1 ? (int64_t)blockIdx.z * args.split_stride : 0);
+        const bool row_ok = MODE == 1 ? row < args.m_static : row < m_rows;
+        if (nkb > 0) {
+            mbar_wait(&tmem_full, 0);
+            tc_fence_after();
+        }
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t v[16];
+            if (nkb > 0) {
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0u;
+            }
+            if (row_ok) {
+                float* crow = Cbase + (int64_t)row * args.ldc + tile_n + c0;
+                const int lim = args.n_store - tile_n - c0;
+                if (lim >= 16 && (args.ldc % 4) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4) {
+                        float4 f;
+                        f.x = __uint_as_float(v[j]); f.y = __uint_as_float(v[j + 1]);
+                        f.z = __uint_as_float(v[j + 2]); f.w = __uint_as_float(v[j + 3]);
+                        if (args.relu) { f.x = fmaxf(f.x, 0.f); f.y = fmaxf(f.y, 0.f); f.z = fmaxf(f.z, 0.f); f.w = fmaxf(f.w, 0.f); }
+                        *reinterpret_cast<float4*>(crow + j) = f;
+                    }
+                } else {
+                    for (int j = 0; j < 16 && j < lim; ++j) {
+                        float f = __uint_as_float(v[j]);
+                        crow[j] = args.relu ? fmaxf(f, 0.f) : f;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
+    }
+}
+
+// ------------------------------------------------------------------ host: tensor maps
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+// 2-D bf16 row-major [rows x cols] (cols contiguous), box {64, box_rows}, 128B swizzle, OOB -> 0.
+bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+    EncodeFn fn = encode_fn();
+    if (!fn || !base) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1u, 1u};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
+template <int BN, int STAGES, int TERMS, int MODE>
+cudaError_t launch_tc(dim3 grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
+    using Cfg = TileCfg<BN>;
+    constexpr int kAPlanes = TERMS == 3 ? 2 : 1;
+    constexpr int smem = STAGES * kAPlanes * (Cfg::kAStage + Cfg::kBStage) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, TERMS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    k_gemm_tc<BN, STAGES, TERMS, MODE><<<grid, kThreads, smem, s>>>(mp.a_hi, mp.a_lo, mp.b_hi, mp.b_lo, a);
+    return cudaGetLastError();
+}
+
+template <int TERMS, int MODE>
+cudaError_t dispatch_bn(int bn, dim3 grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
+    switch (bn) {
+        case 16: return launch_tc<16, 4, TERMS, MODE>(grid, mp, a, s);
+        case 32: return launch_tc<32, 4, TERMS, MODE>(grid, mp, a, s);
+        case 48: return launch_tc<48, 4, TERMS, MODE>(grid, mp, a, s);
+        case 64: return launch_tc<64, 4, TERMS, MODE>(grid, mp, a, s);
+        case 96: return launch_tc<96, 3, TERMS, MODE>(grid, mp, a, s);
+        case 128: return launch_tc<128, 3, TERMS, MODE>(grid, mp, a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+}  // namespace
+
+int tc_tile_n(int n_pad) {
+    if (n_pad <= 128) return n_pad;   // n_pad is a multiple of 16
+    return 128;
+}
+
+cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_static,
+                           int m_cap, int n_pad, int k_pad, float* C, int ldc, int n_store, bool relu, int splits,
+                           int64_t split_stride, cudaStream_t s) {
+    const int bn = tc_tile_n(n_pad);
+    GemmArgs a{};
+    a.m_ptr = m_ptr;
+    a.m_static = m_static;
+    a.k_blocks = (k_pad + kBK - 1) / kBK;
+    a.n_store = n_store;
+    a.C = C;
+    a.ldc = ldc;
+    a.relu = relu ? 1 : 0;
+    a.split_stride = split_stride;
+    if (mode == 0) {
+        dim3 grid((m_cap + kBM - 1) / kBM, (n_pad + bn - 1) / bn, 1);
+        return bf16x3 ? dispatch_bn<3, 0>(bn, grid, maps, a, s) : dispatch_bn<1, 0>(bn, grid, maps, a, s);
+    }
+    // wgrad: C rows = m_static (K_pad of the layer), reduction length *m_ptr
+    dim3 grid((m_static + kBM - 1) / kBM, (n_pad + bn - 1) / bn, splits);
+    return bf16x3 ? dispatch_bn<3, 1>(bn, grid, maps, a, s) : dispatch_bn<1, 1>(bn, grid, maps, a, s);
+}
+
+}  // namespace gs

@@ -1,7 +1,10 @@
 // Host-side launchers of the sm_100a kernels (internal to libgnnstep.so).
 #pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
 #include "common.cuh"
 
 namespace gs {
@@ -43,44 +46,59 @@ void launch_induce(int hs, int slot, StepState* st, const int32_t* nodes, const 
 void launch_reset_map(int h, const StepState* st, const int32_t* nodes, int32_t* map, cudaStream_t s);
 
 // ------------------------------------------------------------------ training side (dense.cu)
-// Layouts: activations are row-major fp32 with row stride =
-// padded width (in_pad = roundup(in, 4); GEMM N padded to 16).  GEMM operand A_l has
-// K_pad = 2*in_pad (SAGE: [H_self | mean]) or in_pad (GCN: Â H) columns.
+// Layouts: fp32 activations are row-major with row stride = padded
+// width (in_pad = roundup(in, 4); GEMM N padded to 16).  GEMM operands are bf16 split planes
+// (hi = bf16(x), lo = bf16(x - hi); lo == nullptr in the bf16-GEMM variant), row-major, and
+// rows [M, roundup(M, 64)) of every operand plane are written as zeros (the wgrad reduction
+// runs over whole 64-row blocks).  A_l has K_pad = 2*in_pad (SAGE: [H_self | mean]) or in_pad
+// (GCN: Â H) columns.
+struct Split { __nv_bfloat16* hi; __nv_bfloat16* lo; };
 
 // SAGE-mean aggregation into A = [H_self | mean] for rows i < *rows_ptr.  Neighbour row of
 // source c is gmap ? gmap[c] : c, self row smap ? smap[i] : i (layer 1 reads X by global id:
 // the fused feature gather).
 void launch_agg_sage(const int32_t* rows_ptr, const float* H, int in_pad, const int32_t* gmap,
-                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, float* A,
+                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A,
                      cudaStream_t s);
 // GCN aggregation A = Â H (self loop included) for rows i < *rows_ptr of a block with
 // *ndst_ptr destinations; d_out from the transposed row pointer.  col must be local ids.
-void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const float* H, int in_pad,
+void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const float* H, int in_pad, int lda,
                     const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
-                    const int32_t* col, const int32_t* trowptr, float* A, cudaStream_t s);
-// C[M x N] = op(A)[M x K] op(B)[K x N] (+ReLU), fp32.  M = *m_ptr if non-null (dynamic rows),
-// K = *k_ptr if non-null (dynamic reduction, split over gridDim.z into C + z*split_stride).
-void launch_gemm(bool transA, bool transB, bool relu, const int32_t* m_ptr, int m_static,
-                 int m_cap, int n, const int32_t* k_ptr, int k_static, const float* A, int lda,
-                 const float* B, int ldb, float* C, int ldc, int splits, int64_t split_stride,
-                 cudaStream_t s);
-// grads[off + r*out + c] = Σ_z part[z][rpad(r)*n_pad + c]   (fixed z order; unpads rows/cols)
+                    const int32_t* col, const int32_t* trowptr, Split A, cudaStream_t s);
+// grads[r*out + c] = Σ_z part[z][rpad(r)*n_pad + c]   (fixed z order; unpads rows/cols)
 void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, int rows, int out,
                          int in, int in_pad, bool sage, int n_pad, float* grads, cudaStream_t s);
-// Wp[K_pad x N_pad] from flat W (rows x out), zero padding.
+// W [K_pad x N_pad] and W^T [N_pad x K_pad] split planes from flat fp32 W (rows x out).
 void launch_pack_weight(const float* W, int rows, int out, int in, int in_pad, bool sage,
-                        int k_pad, int n_pad, float* Wp, cudaStream_t s);
-// Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total.
+                        int k_pad, int n_pad, Split Wkn, Split Wnk, cudaStream_t s);
+// Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total
+// written as split planes [rows x ldz] (+ zero tail rows).
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels,
-               const int32_t* nodes, float* dZ, cudaStream_t s);
+               const int32_t* nodes, Split dZ, cudaStream_t s);
 // Backward aggregation over the transposed block (atomic-free, fixed order), u < n_src[h]:
 //   SAGE: dPre_prev[u] = ([u<dlim] dA[u,:in_pad] + Σ_{e in T(u), dst<dlim} dA[dst, in_pad:]/deg(dst)) * [H_prev[u]>0]
 //   GCN:  dPre_prev[u] = (Â^T dA)[u] * [H_prev[u] > 0]   (dA rows < dlim)
+// dPre_prev is written as split planes [n_src x in_pad] (+ zero tail rows).
 void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, const float* dA,
                      int in_pad, const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
-                     const float* H_prev, float* dPre_prev, cudaStream_t s);
+                     const float* H_prev, Split dPre_prev, cudaStream_t s);
 void launch_sgd(float* params, const float* grads, int64_t n, float lr, cudaStream_t s);
 void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer,
                         cudaStream_t s);
+
+// ------------------------------------------------------------------ tensor-core GEMM (gemm_tc.cu)
+struct TcGemmMaps { CUtensorMap a_hi, a_lo, b_hi, b_lo; };
+// 2-D bf16 row-major [rows x cols], box {64 cols, box_rows}, 128B swizzle, OOB reads -> 0.
+bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
+// N tile the GEMM uses for an output width n_pad (TMA box rows of a K-major B operand).
+int tc_tile_n(int n_pad);
+// mode 0 (fwd / dgrad): C[M x n_store] = A[M x k_pad] B^T (B given as [n_pad x k_pad]), M = *m_ptr
+//   (rows >= M not stored), optional ReLU.  A, B K-major; maps: A box rows 128, B box rows tc_tile_n.
+// mode 1 (wgrad): C_z[m_static x n_pad] = Σ_{m in split z} A[m, :]^T B[m, :], reduction length
+//   *m_ptr split into `splits` ranges of 64-row blocks; A, B MN-major, maps with box rows 64.
+// bf16x3: 3-term split product (fp32 parity); else 1 term (bf16 GEMM variant).
+cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_static,
+                           int m_cap, int n_pad, int k_pad, float* C, int ldc, int n_store, bool relu, int splits,
+                           int64_t split_stride, cudaStream_t s);
 
 }  // namespace gs
