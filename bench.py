@@ -95,32 +95,53 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- algorithmic work per kernel class
-def agg_l1_bytes(w, sz):
-    """Layer-1 fused gather + mean aggregation, compulsory HBM bytes:
-    every unique input row once + the [X_self | mean] operand written + CSR of the block."""
-    L = w.num_layers
-    h = L - 1
-    fp = w.feat_stride
-    n_dst, n_src, E = sz["n_dst"][h], sz["n_src"][h], sz["n_edges"][h]
-    return n_src * fp * 4 + n_dst * 2 * fp * 4 + E * 4 + (n_dst + 1) * 4
+def layer_dims(w):
+    """Per layer (input-first): in, out, in_pad, k_pad, n_pad (the library's padded layout)."""
+    out = []
+    for li in range(w.num_layers):
+        fi, fo = w.dims[li], w.dims[li + 1]
+        in_pad = (fi + 3) // 4 * 4
+        k_pad = 2 * in_pad if w.model == "sage" else (in_pad + 7) // 8 * 8
+        out.append((fi, fo, in_pad, k_pad, (fo + 15) // 16 * 16))
+    return out
 
 
-def gemm_flops(w, sz, which):
-    dims = w.dims
+def kernel_work(w, sz, kind, terms=3, splits=None):
+    """Algorithmic (compulsory) HBM bytes and FLOPs of one step's launches of a kernel class
+    (DESIGN.md "Roofline").  sz: per-hop sizes of the batch."""
     L = w.num_layers
-    f = 0
-    for li in range(L):
-        h = L - 1 - li
-        M = sz["n_dst"][h]
-        K = (2 if w.model == "sage" else 1) * dims[li]
-        N = dims[li + 1]
-        if which == "gemm_fwd":
-            f += 2 * M * K * N
-        elif which == "gemm_wgrad":
-            f += 2 * M * K * N
-        elif which == "gemm_dgrad" and li > 0:
-            f += 2 * M * K * N
-    return f
+    byt, flo = 0.0, 0.0
+    for li, (fi, fo, in_pad, k_pad, n_pad) in enumerate(layer_dims(w)):
+        h = L - 1 - li if w.sampler == "neighbor" else L  # ShaDow: the induced block slot
+        M, S, E = sz["n_dst"][h], sz["n_src"][h], sz["n_edges"][h]
+        if kind == "agg_l1" and li == 0 or kind == "agg" and li > 0:
+            byt += S * in_pad * 4 + M * k_pad * 4 + E * 4 + (M + 1) * 4
+        elif kind == "gemm_fwd":
+            byt += M * k_pad * 4 + k_pad * n_pad * 4 + M * n_pad * 4
+            flo += 2.0 * M * k_pad * n_pad * terms
+        elif kind == "gemm_dgrad" and li > 0:
+            byt += M * n_pad * 4 + k_pad * n_pad * 4 + M * k_pad * 4
+            flo += 2.0 * M * n_pad * k_pad * terms
+        elif kind == "gemm_wgrad":
+            sp = splits[li] if splits else 1
+            byt += M * k_pad * 4 + M * n_pad * 4 + 2 * sp * k_pad * n_pad * 4 + (2 if w.model == "sage" else 1) * fi * fo * 4
+            flo += 2.0 * M * k_pad * n_pad * terms
+        elif kind == "spmm_bwd" and li > 0:
+            byt += 2 * M * in_pad * 4 + 2 * S * in_pad * 4 + E * 4 + (S + 1) * 4 + (M + 1) * 4
+    return byt, flo
+
+
+def caps_of(w):
+    """Row capacity per layer (the library's worst-case bounds, used for its split-K count)."""
+    caps, cap = [], w.batch_size
+    hop_caps = []
+    for h in range(len(w.fanouts)):
+        k = w.fanouts[len(w.fanouts) - 1 - h]
+        hop_caps.append(cap)
+        cap = min(w.num_nodes, cap + cap * k)
+    if w.sampler == "neighbor":
+        return [hop_caps[w.num_layers - 1 - li] for li in range(w.num_layers)]
+    return [cap] * (w.num_layers - 1) + [w.batch_size]
 
 
 def load_peaks():
@@ -317,30 +338,41 @@ def main():
     m.profile_enable(False)
     tot_ms = sum(v[0] for v in prof.values())
     hbm, bf16, bf16_sus, peak_kind = load_peaks()
-    dominant = max(prof, key=lambda k: prof[k][0])
-    # roofline of the dominant kernel class
-    if dominant.startswith("gemm"):
-        work = np.mean([gemm_flops(w, sz, dominant) for sz in sizes])
-        launches = prof[dominant][1] / args.steps
-        achieved = work / (prof[dominant][0] / args.steps * 1e-3) / 1e12
-        fp32_simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12   # FFMA/clk/SM x clock
-        roof = {"kernel": dominant, "bound": "alu", "achieved": achieved, "peak": fp32_simt_peak,
-                "unit": "TFLOP/s", "frac": achieved / fp32_simt_peak, "traffic": None,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz",
-                "launches_per_step": launches}
-    else:
-        work = np.mean([agg_l1_bytes(w, sz) for sz in sizes])
-        per_launch_ms = prof["agg_l1"][0] / max(prof["agg_l1"][1], 1)
-        achieved = work / (per_launch_ms * 1e-3) / 1e9
-        roof = {"kernel": "agg_l1", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}
-    # always also report the gather/aggregation kernel against HBM
-    per_launch_ms = prof["agg_l1"][0] / max(prof["agg_l1"][1], 1)
-    agg_bytes = float(np.mean([agg_l1_bytes(w, sz) for sz in sizes]))
-    agg = {"kernel": "agg_l1 (fused feature gather + mean aggregation, layer 1)", "bound": "hbm",
-           "bytes_per_launch": agg_bytes, "ms_per_launch": per_launch_ms,
-           "achieved": agg_bytes / (per_launch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
-    agg["frac"] = agg["achieved"] / hbm
+    terms = 3 if args.precision == "fp32" else 1
+    def _splits(li, cap):
+        fi, fo, in_pad, k_pad, n_pad = layer_dims(w)[li]
+        bn = n_pad if n_pad <= 128 else 128
+        tiles = ((k_pad + 127) // 128) * ((n_pad + bn - 1) // bn)
+        return max(1, min(148 // tiles, cap // 128))
+    splits = [_splits(li, c) for li, c in enumerate(caps_of(w))]
+    traffic = {}
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(w.name, {})
+    rooflines = {}
+    for kind in ("agg_l1", "agg", "gemm_fwd", "gemm_wgrad", "gemm_dgrad", "spmm_bwd"):
+        t_ms, nl = prof[kind]
+        if nl == 0 or t_ms <= 0:
+            continue
+        wk = [kernel_work(w, sz, kind, terms, splits) for sz in sizes]
+        byt = float(np.mean([x[0] for x in wk])) / (nl / args.steps)     # per launch
+        flo = float(np.mean([x[1] for x in wk])) / (nl / args.steps)
+        dur = t_ms / nl * 1e-3                                           # s per launch
+        t_hbm, t_tc = byt / (hbm * 1e9), flo / (bf16 * 1e12)
+        if flo > 0 and t_tc > t_hbm:
+            r = {"bound": "tensor", "achieved": flo / dur / 1e12, "peak": bf16, "unit": "TFLOP/s"}
+        else:
+            r = {"bound": "hbm", "achieved": byt / dur / 1e9, "peak": hbm, "unit": "GB/s"}
+        r["frac"] = r["achieved"] / r["peak"]
+        tr = traffic.get(kind)
+        r["traffic"] = tr
+        r.update({"kernel": kind, "bytes_per_launch": byt, "flops_per_launch": flo,
+                  "ms_per_launch": dur * 1e3, "launches_per_step": nl / args.steps,
+                  "peak_source": f"{peak_kind} MEASURED_PEAKS.json " + ("bf16_tflops" if r["bound"] == "tensor" else "hbm_gbs")})
+        rooflines[kind] = r
+    dominant = max(rooflines, key=lambda k: prof[k][0])
+    roof = dict(rooflines[dominant])
+    agg = rooflines.get("agg_l1")
 
     # ---- cpu baseline (oracle on a bounded sample), rank 0 at N=1 only
     cpu = None
@@ -368,6 +400,7 @@ def main():
             "launches_per_step": m.launches_per_step,
             "roofline": roof,
             "gather_aggregate": agg,
+            "rooflines": rooflines,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
             "kernel_share": {k: v[0] / tot_ms for k, v in prof.items()} if tot_ms else {},
             "instrumented_ms_per_step": tot_ms / args.steps,

@@ -129,6 +129,8 @@ struct gnn_model {
 
     bool bf16x3 = true;            // fp32 parity mode: 3-term bf16 split GEMMs
     cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t prof_gexec = nullptr;   // instrumented copy (event-record nodes)
+    std::vector<ProfPair> prof_pairs;
     int64_t launches_per_step = 0;
 
     bool profiling = false;
@@ -155,9 +157,13 @@ template <class Fn>
 void K(gnn_model* m, int kid, Fn&& fn) {
     if (m->profiling) {
         ProfPair p{kid, take_event(m), take_event(m)};
-        cudaEventRecord(p.a, m->stream);
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(m->stream, &cs);
+        // inside a capture, only an "external" record node really records at replay time
+        const unsigned fl = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+        cudaEventRecordWithFlags(p.a, m->stream, fl);
         fn();
-        cudaEventRecord(p.b, m->stream);
+        cudaEventRecordWithFlags(p.b, m->stream, fl);
         m->pending.push_back(p);
     } else {
         fn();
@@ -177,6 +183,17 @@ void drain_profile(gnn_model* m) {
     m->pending.clear();
 }
 
+PackAll pack_desc(gnn_model* m) {
+    PackAll p{};
+    p.n = m->L;
+    p.sage = m->sage;
+    for (int li = 0; li < m->L; ++li) {
+        const Layer& ly = m->layers[li];
+        p.l[li] = PackLayer{m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, ly.k_pad, ly.n_pad, ly.Wkn, ly.Wnk};
+    }
+    return p;
+}
+
 const int32_t* rows_ptr(gnn_model* m, int li) {   // output rows of layer li (0-based)
     if (m->shadow && li == m->L - 1) return &m->st->batch_n;
     return &m->st->n_dst[m->layers[li].blk];
@@ -189,7 +206,7 @@ void enqueue_sampling(gnn_model* m) {
     for (int h = 0; h < m->hops; ++h) {
         const int k = m->cfg.fanouts[m->hops - 1 - h];
         HopBufs& b = m->hb[h];
-        K(m, GNN_K_SCAN, [&] { launch_hop_rowptr(h, k, m->st, m->nodes, g->row_ptr, b.rowptr, m->sc, s); });
+        K(m, GNN_K_SCAN, [&] { launch_hop_rowptr(h, k, m->st, m->nodes, g->row_ptr, b.rowptr, b.cap_dst, m->sc, s); });
         K(m, GNN_K_SAMPLE, [&] {
             launch_sample_fill(h, k, m->st, m->nodes, g->row_ptr, g->col, b.rowptr, b.nbr, m->map, m->bits,
                                m->cfg.seed, s);
@@ -201,18 +218,18 @@ void enqueue_sampling(gnn_model* m) {
         if (b.need_t)
             K(m, GNN_K_TRANSPOSE, [&] {
                 launch_transpose(h, m->st, b.rowptr, b.col, m->tcount, b.trowptr, b.tcursor, b.tdst, b.tdst_s,
-                                 m->sc, s);
+                                 b.cap_src, m->sc, s);
             });
     }
     if (m->shadow) {
         HopBufs& b = m->hb[m->slot];
         K(m, GNN_K_INDUCE, [&] {
             launch_induce(m->hops - 1, m->slot, m->st, m->nodes, g->row_ptr, g->col, m->map, m->icount,
-                          b.rowptr, b.col, m->tcount, m->sc, s);
+                          b.rowptr, b.col, m->tcount, b.cap_src, m->sc, s);
         });
         K(m, GNN_K_TRANSPOSE, [&] {
             launch_transpose(m->slot, m->st, b.rowptr, b.col, m->tcount, b.trowptr, b.tcursor, b.tdst,
-                             b.tdst_s, m->sc, s);
+                             b.tdst_s, b.cap_src, m->sc, s);
         });
     }
     K(m, GNN_K_OTHER, [&] { launch_reset_map(m->hops - 1, m->st, m->nodes, m->map, s); });
@@ -282,11 +299,7 @@ void enqueue_training(gnn_model* m) {
             ncclAllReduce(m->grads, m->grads, (size_t)m->pcount, ncclFloat, ncclSum, m->comm, s);
         });
     K(m, GNN_K_SGD, [&] { launch_sgd(m->params, m->grads, m->pcount, m->cfg.lr, s); });
-    for (auto& ly : m->layers)
-        K(m, GNN_K_OTHER, [&] {
-            launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad,
-                               ly.n_pad, ly.Wkn, ly.Wnk, s);
-        });
+    K(m, GNN_K_OTHER, [&] { launch_pack_all(pack_desc(m), s); });
 }
 
 void enqueue_body(gnn_model* m) {
@@ -294,11 +307,19 @@ void enqueue_body(gnn_model* m) {
     enqueue_training(m);
 }
 
-gnn_status build_graph(gnn_model* m) {
-    if (m->gexec) return GNN_OK;
+// Capture the step body once.  With profiling on, the capture also records an event pair
+// around every kernel class launch (event-record nodes), read back after each replay.
+gnn_status build_graph(gnn_model* m, bool prof) {
+    cudaGraphExec_t* target = prof ? &m->prof_gexec : &m->gexec;
+    if (*target) return GNN_OK;
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+    const size_t before = m->pending.size();
     enqueue_body(m);
+    if (prof) {
+        m->prof_pairs.assign(m->pending.begin() + before, m->pending.end());
+        m->pending.resize(before);
+    }
     cudaError_t e = cudaStreamEndCapture(m->stream, &graph);
     if (e != cudaSuccess) return fail(GNN_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     size_t n = 0;
@@ -311,16 +332,27 @@ gnn_status build_graph(gnn_model* m) {
         cudaGraphNodeGetType(nd, &t);
         if (t == cudaGraphNodeTypeKernel) ++kernels;
     }
-    m->launches_per_step = kernels + 1;   // + k_begin_step (outside the graph)
-    CK(cudaGraphInstantiate(&m->gexec, graph, 0));
+    if (!prof) m->launches_per_step = kernels + 1;   // + k_begin_step (outside the graph)
+    CK(cudaGraphInstantiate(target, graph, 0));
     CK(cudaGraphDestroy(graph));
     return GNN_OK;
 }
 
 gnn_status run_body(gnn_model* m) {
     if (m->cfg.use_graph && !m->profiling) {
-        TRY(build_graph(m));
+        TRY(build_graph(m, false));
         CK(cudaGraphLaunch(m->gexec, m->stream));
+    } else if (m->cfg.use_graph) {
+        // instrumented replay: the same graph body with event-record nodes; read them back now
+        TRY(build_graph(m, true));
+        CK(cudaGraphLaunch(m->prof_gexec, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        for (auto& p : m->prof_pairs) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p.a, p.b));
+            m->prof_ms[p.kid] += ms;
+            m->prof_n[p.kid] += 1;
+        }
     } else {
         enqueue_body(m);
         CK(cudaGetLastError());
@@ -475,7 +507,14 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     AL(m->bits, m->nwords);
     AL(m->tcount, m->tcap);
     AL(m->icount, m->nodes_cap);
-    AL(m->sc.partials, kScanBlocks);
+    {   // single-pass scan state, sized for the largest scan (bitmap words or node lists)
+        const int64_t items = std::max<int64_t>(m->nwords, m->nodes_cap + 1);
+        m->sc.max_tiles = (int)((items + 2047) / 2048);
+        AL(m->sc.ctrl, 2);
+        AL(m->sc.status, m->sc.max_tiles);
+        CK(cudaMemset(m->sc.ctrl, 0, 2 * sizeof(uint32_t)));
+        CK(cudaMemset(m->sc.status, 0, sizeof(unsigned long long) * m->sc.max_tiles));
+    }
     AL(m->seeds_in, c.batch_size);
     for (int h = 0; h <= m->hops; ++h) {
         if (h == m->hops && !m->shadow) break;
@@ -514,7 +553,11 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         poff += ly.pcnt;
         ly.blk = m->shadow ? m->slot : (m->hops - 1 - li);
         ly.m_cap = m->shadow ? (li == m->L - 1 ? c.batch_size : m->nodes_cap) : m->hb[ly.blk].cap_dst;
-        ly.splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, ly.m_cap / 1024));
+        {   // wgrad split over the reduction so that tiles x splits fills the 148 SMs once
+            const int bn = tc_tile_n(ly.n_pad);
+            const int64_t tiles = ((ly.k_pad + 127) / 128) * ((ly.n_pad + bn - 1) / bn);
+            ly.splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / tiles, ly.m_cap / 128));
+        }
         m->layers.push_back(ly);
     }
     m->pcount = poff;
@@ -563,9 +606,8 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         Layer& ly = m->layers[li];
         const float bound = std::sqrt(6.0f / (float)(ly.in + ly.out));
         launch_init_params(m->params + ly.poff, ly.pcnt, bound, c.init_seed, (uint32_t)li, m->stream);
-        launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad, ly.n_pad,
-                           ly.Wkn, ly.Wnk, m->stream);
     }
+    launch_pack_all(pack_desc(m), m->stream);
     CK(cudaMemsetAsync(m->grads, 0, sizeof(float) * m->pcount, m->stream));
     CK(cudaStreamSynchronize(m->stream));
     CK(cudaGetLastError());
@@ -580,6 +622,8 @@ gnn_status gnn_model_destroy(gnn_model* m) {
     drain_profile(m);
     for (auto e : m->free_events) cudaEventDestroy(e);
     if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    if (m->prof_gexec) cudaGraphExecDestroy(m->prof_gexec);
+    for (auto& p : m->prof_pairs) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     if (m->comm) ncclCommDestroy(m->comm);
     for (void* p : m->owned) cudaFree(p);
     if (m->cub_tmp) cudaFree(m->cub_tmp);
@@ -643,9 +687,7 @@ gnn_status gnn_set_params(gnn_model* m, const float* in_host, int64_t n) {
     if (n != m->pcount) return fail(GNN_ERR_SHAPE, "n != param_count");
     TRY(set_device(m->g->dev));
     CK(cudaMemcpyAsync(m->params, in_host, sizeof(float) * n, cudaMemcpyHostToDevice, m->stream));
-    for (auto& ly : m->layers)
-        launch_pack_weight(m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, m->sage, ly.k_pad, ly.n_pad,
-                           ly.Wkn, ly.Wnk, m->stream);
+    launch_pack_all(pack_desc(m), m->stream);
     CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }
@@ -671,6 +713,7 @@ gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_
     m->rank = rank;
     m->world = world;
     if (m->gexec) { cudaGraphExecDestroy(m->gexec); m->gexec = nullptr; }
+    if (m->prof_gexec) { cudaGraphExecDestroy(m->prof_gexec); m->prof_gexec = nullptr; }
     return GNN_OK;
 }
 

@@ -252,18 +252,28 @@ __global__ void k_wgrad_reduce(const float* __restrict__ part, int splits, int64
     }
 }
 
-__global__ void k_pack_weight(const float* __restrict__ W, int rows, int out, int in, int in_pad, bool sage,
-                              int k_pad, int n_pad, Split Wkn, Split Wnk) {
-    const int64_t total = (int64_t)k_pad * n_pad;
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
-         f += (int64_t)gridDim.x * blockDim.x) {
-        const int rp = (int)(f / n_pad), c = (int)(f % n_pad);
-        int r = -1;
-        if (sage) { const int half = rp / in_pad, j = rp % in_pad; if (j < in && half < 2) r = half * in + j; }
-        else if (rp < in) r = rp;
-        const float v = (r >= 0 && c < out) ? W[(int64_t)r * out + c] : 0.f;
-        store_split1(Wkn, f, v);
-        store_split1(Wnk, (int64_t)c * k_pad + rp, v);
+__device__ __forceinline__ float packed_value(const PackLayer& L, bool sage, int rp, int c) {
+    int r = -1;
+    if (sage) { const int half = rp / L.in_pad, j = rp % L.in_pad; if (j < L.in && half < 2) r = half * L.in + j; }
+    else if (rp < L.in) r = rp;
+    return (r >= 0 && c < L.out) ? L.W[(int64_t)r * L.out + c] : 0.f;
+}
+
+// All layers in one launch; both layouts written in their own (coalesced) order.
+__global__ void k_pack_all(PackAll P) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int l = 0; l < P.n; ++l) {
+        const PackLayer& L = P.l[l];
+        const int64_t total = (int64_t)L.k_pad * L.n_pad;
+        for (int64_t f = tid; f < total; f += nth) {
+            const int rp = (int)(f / L.n_pad), c = (int)(f % L.n_pad);
+            store_split1(L.Wkn, f, packed_value(L, P.sage, rp, c));
+        }
+        for (int64_t f = tid; f < total; f += nth) {
+            const int c = (int)(f / L.k_pad), rp = (int)(f % L.k_pad);
+            store_split1(L.Wnk, f, packed_value(L, P.sage, rp, c));
+        }
     }
 }
 
@@ -384,11 +394,8 @@ void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, in
     k_wgrad_reduce<<<blocks, 256, 0, s>>>(part, splits, split_stride, rows, out, in, in_pad, sage, n_pad, grads);
 }
 
-void launch_pack_weight(const float* W, int rows, int out, int in, int in_pad, bool sage, int k_pad,
-                        int n_pad, Split Wkn, Split Wnk, cudaStream_t s) {
-    const int64_t total = (int64_t)k_pad * n_pad;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-    k_pack_weight<<<blocks, 256, 0, s>>>(W, rows, out, in, in_pad, sage, k_pad, n_pad, Wkn, Wnk);
+void launch_pack_all(const PackAll& p, cudaStream_t s) {
+    k_pack_all<<<148 * 2, 256, 0, s>>>(p);
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,

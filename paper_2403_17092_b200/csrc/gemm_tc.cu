@@ -11,8 +11,10 @@
 //   fwd   Pre = A W         A: [M x K] K-major,   B = W^T [N x K] K-major      (+ReLU)
 //   dgrad dA  = dPre W^T    A: [M x N] K-major,   B = W   [K x N] K-major
 //   wgrad dW  = A^T dPre    A^T: MN-major,        B = dPre MN-major, split over M (deterministic)
-// Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer, warps 2..5 =
-// epilogue (one TMEM lane quarter each).
+//
+// Persistent: one CTA per SM walks a static tile list (tile count read on the device).  Warp 0
+// = TMA producer, warp 1 = TMEM allocator + MMA issuer, warps 2..5 = epilogue (one TMEM lane
+// quarter each).  Two TMEM accumulators: the epilogue of tile j overlaps the MMAs of tile j+1.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -34,6 +36,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
@@ -89,9 +94,10 @@ __host__ __device__ constexpr uint32_t idesc() {
 
 template <int BN>
 struct TileCfg {
-    static constexpr int kAStage = kBM * kBK * 2;                 // 16 KB per plane
-    static constexpr int kBStage = ((BN + 63) / 64) * 64 * kBK * 2;  // rounded to whole 64-wide boxes (MN-major)
-    static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    static constexpr int kAStage = kBM * kBK * 2;                    // 16 KB per plane
+    static constexpr int kBStage = ((BN + 63) / 64) * 64 * kBK * 2;  // whole 64-wide boxes (MN-major)
+    static constexpr int kAccCols = BN <= 32 ? 32 : BN <= 64 ? 64 : 128;      // one accumulator
+    static constexpr int kTmemCols = 2 * kAccCols;                            // double buffered
     // bytes one stage's TMA boxes deliver (OOB parts are zero-filled but still counted)
     static constexpr int kBBytesK = BN * kBK * 2;                     // K-major: box {64, BN}
     static constexpr int kBBytesMN = ((BN + 63) / 64) * 64 * kBK * 2; // MN-major: boxes {64, 64}
@@ -99,17 +105,45 @@ struct TileCfg {
 
 struct GemmArgs {
     const int32_t* m_ptr;   // fwd/dgrad: rows of C (dynamic); wgrad: reduction length (dynamic)
-    int m_static;
+    int m_static;           // wgrad: rows of C
+    int m_tiles_cap;        // fwd/dgrad: tile rows of the worst case
+    int n_tiles;
+    int splits;             // wgrad
     int k_blocks;           // fwd/dgrad: reduction in 64-blocks (static)
     int n_store;            // columns of C to store
     float* C;
     int ldc;
     int relu;
-    int64_t split_stride;   // wgrad: C + blockIdx.z * split_stride
+    int64_t split_stride;   // wgrad: C + z * split_stride
 };
 
-// MODE 0 = fwd/dgrad (A, B K-major; tile (m = blockIdx.x, n = blockIdx.y)),
-// MODE 1 = wgrad (A, B MN-major; tile (m' = blockIdx.x over K_pad, n = blockIdx.y), split z).
+struct TileInfo { int tm, tn, z, kb0, nkb; };
+
+template <int MODE>
+__device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t, int M) {
+    TileInfo ti;
+    if (MODE == 0) {
+        ti.tm = t / a.n_tiles;
+        ti.tn = t % a.n_tiles;
+        ti.z = 0;
+        ti.kb0 = 0;
+        ti.nkb = a.k_blocks;
+    } else {
+        const int mt = (a.m_static + kBM - 1) / kBM;
+        const int per_z = mt * a.n_tiles;
+        ti.z = t / per_z;
+        const int r = t % per_z;
+        ti.tm = r / a.n_tiles;
+        ti.tn = r % a.n_tiles;
+        const int nkb_all = (M + kBK - 1) / kBK;
+        const int per = (nkb_all + a.splits - 1) / a.splits;
+        ti.kb0 = min(nkb_all, ti.z * per);
+        ti.nkb = min(nkb_all, ti.kb0 + per) - ti.kb0;
+    }
+    return ti;
+}
+
+// MODE 0 = fwd/dgrad (A, B K-major), MODE 1 = wgrad (A, B MN-major, split z).
 template <int BN, int STAGES, int TERMS, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
@@ -120,31 +154,18 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     constexpr int kStageBytes = kAPlanes * (Cfg::kAStage + Cfg::kBStage);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tmem_full;
+    __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile_m = blockIdx.x * kBM;
-    const int tile_n = blockIdx.y * BN;
-
-    // ---- work extent
-    int kb_begin = 0, kb_end = args.k_blocks;
-    int m_rows = args.m_static;
-    if (MODE == 0) {
-        m_rows = args.m_ptr ? *args.m_ptr : args.m_static;
-        if (tile_m >= m_rows) return;
-    } else {
-        const int M = *args.m_ptr;                          // reduction length (rows of A and dPre)
-        const int nkb = (M + kBK - 1) / kBK;
-        const int per = (nkb + gridDim.z - 1) / gridDim.z;
-        kb_begin = min(nkb, (int)blockIdx.z * per);
-        kb_end = min(nkb, kb_begin + per);
-    }
-    const int nkb = kb_end - kb_begin;
+    const int M = *args.m_ptr;
+    const int ntiles = MODE == 0 ? ((M + kBM - 1) / kBM) * args.n_tiles
+                                 : ((args.m_static + kBM - 1) / kBM) * args.n_tiles * args.splits;
+    if ((int)blockIdx.x >= ntiles) return;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-        mbar_init(&tmem_full, 1);
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -161,35 +182,38 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     if (warp == 0) {
         // ================= TMA producer
         if (lane == 0) {
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                if (i >= STAGES) mbar_wait(&empty_bar[s], ((i / STAGES) - 1) & 1);
-                uint8_t* st = smem + s * kStageBytes;
-                uint8_t* a_hi = st;
-                uint8_t* b_hi = st + Cfg::kAStage;
-                uint8_t* a_lo = st + Cfg::kAStage + Cfg::kBStage;
-                uint8_t* b_lo = a_lo + Cfg::kAStage;
-                mbar_expect_tx(&full_bar[s], kAPlanes * (Cfg::kAStage + (MN ? Cfg::kBBytesMN : Cfg::kBBytesK)));
-                const int k0 = (kb_begin + i) * kBK;
-                if (MODE == 0) {
-                    // K-major: box {64 (k), rows}
-                    tma_load_2d(a_hi, &mA_hi, &full_bar[s], k0, tile_m);
-                    tma_load_2d(b_hi, &mB_hi, &full_bar[s], k0, tile_n);
-                    if (TERMS == 3) {
-                        tma_load_2d(a_lo, &mA_lo, &full_bar[s], k0, tile_m);
-                        tma_load_2d(b_lo, &mB_lo, &full_bar[s], k0, tile_n);
-                    }
-                } else {
-                    // MN-major: boxes {64 (mn), 64 (k rows)}, 64-wide MN blocks 8 KB apart
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const TileInfo ti = tile_info<MODE>(args, t, M);
+                const int tile_m = ti.tm * kBM, tile_n = ti.tn * BN;
+                for (int kb = 0; kb < ti.nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
+                    uint8_t* st = smem + s * kStageBytes;
+                    uint8_t* a_hi = st;
+                    uint8_t* b_hi = st + Cfg::kAStage;
+                    uint8_t* a_lo = st + Cfg::kAStage + Cfg::kBStage;
+                    uint8_t* b_lo = a_lo + Cfg::kAStage;
+                    mbar_expect_tx(&full_bar[s], kAPlanes * (Cfg::kAStage + (MN ? Cfg::kBBytesMN : Cfg::kBBytesK)));
+                    const int k0 = (ti.kb0 + kb) * kBK;
+                    if (MODE == 0) {
+                        tma_load_2d(a_hi, &mA_hi, &full_bar[s], k0, tile_m);
+                        tma_load_2d(b_hi, &mB_hi, &full_bar[s], k0, tile_n);
+                        if (TERMS == 3) {
+                            tma_load_2d(a_lo, &mA_lo, &full_bar[s], k0, tile_m);
+                            tma_load_2d(b_lo, &mB_lo, &full_bar[s], k0, tile_n);
+                        }
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < kBM / 64; ++j) {
-                        tma_load_2d(a_hi + j * 8192, &mA_hi, &full_bar[s], tile_m + 64 * j, k0);
-                        if (TERMS == 3) tma_load_2d(a_lo + j * 8192, &mA_lo, &full_bar[s], tile_m + 64 * j, k0);
-                    }
+                        for (int j = 0; j < kBM / 64; ++j) {
+                            tma_load_2d(a_hi + j * 8192, &mA_hi, &full_bar[s], tile_m + 64 * j, k0);
+                            if (TERMS == 3) tma_load_2d(a_lo + j * 8192, &mA_lo, &full_bar[s], tile_m + 64 * j, k0);
+                        }
 #pragma unroll
-                    for (int j = 0; j < (BN + 63) / 64; ++j) {
-                        tma_load_2d(b_hi + j * 8192, &mB_hi, &full_bar[s], tile_n + 64 * j, k0);
-                        if (TERMS == 3) tma_load_2d(b_lo + j * 8192, &mB_lo, &full_bar[s], tile_n + 64 * j, k0);
+                        for (int j = 0; j < (BN + 63) / 64; ++j) {
+                            tma_load_2d(b_hi + j * 8192, &mB_hi, &full_bar[s], tile_n + 64 * j, k0);
+                            if (TERMS == 3) tma_load_2d(b_lo + j * 8192, &mB_lo, &full_bar[s], tile_n + 64 * j, k0);
+                        }
                     }
                 }
             }
@@ -198,76 +222,101 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         // ================= MMA issuer (one thread)
         if (lane == 0) {
             constexpr uint32_t id = idesc<BN, MN, MN>();
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                mbar_wait(&full_bar[s], (i / STAGES) & 1);
-                tc_fence_after();
-                uint8_t* st = smem + s * kStageBytes;
-                const uint32_t a_hi = smem_u32(st), b_hi = smem_u32(st + Cfg::kAStage);
-                const uint32_t a_lo = smem_u32(st + Cfg::kAStage + Cfg::kBStage);
-                const uint32_t b_lo = a_lo + Cfg::kAStage;
+            int it = 0, j = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const TileInfo ti = tile_info<MODE>(args, t, M);
+                if (ti.nkb == 0) continue;
+                const int acc = j & 1;
+                if (j >= 2) { mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1); tc_fence_after(); }
+                const uint32_t d = tmem + (uint32_t)(acc * Cfg::kAccCols);
+                for (int kb = 0; kb < ti.nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full_bar[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    uint8_t* st = smem + s * kStageBytes;
+                    const uint32_t a_hi = smem_u32(st), b_hi = smem_u32(st + Cfg::kAStage);
+                    const uint32_t a_lo = smem_u32(st + Cfg::kAStage + Cfg::kBStage);
+                    const uint32_t b_lo = a_lo + Cfg::kAStage;
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk) {
-                    // K-major: +32 B per 16-element k step inside the 128 B swizzle row;
-                    // MN-major: +16 rows x 128 B per k step.
-                    const uint32_t off = MN ? kk * 2048 : kk * 32;
-                    const uint32_t lbo = MN ? 8192 : 16, sbo = 1024;
-                    const uint64_t dah = sdesc(a_hi + off, lbo, sbo), dbh = sdesc(b_hi + off, lbo, sbo);
-                    const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
-                    tc_mma(tmem, dah, dbh, id, acc0);
-                    if (TERMS == 3) {
-                        const uint64_t dal = sdesc(a_lo + off, lbo, sbo), dbl = sdesc(b_lo + off, lbo, sbo);
-                        tc_mma(tmem, dah, dbl, id, 1u);
-                        tc_mma(tmem, dal, dbh, id, 1u);
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        // K-major: +32 B per 16-element k step inside the 128 B swizzle row;
+                        // MN-major: +16 rows x 128 B per k step.
+                        const uint32_t off = MN ? kk * 2048 : kk * 32;
+                        const uint32_t lbo = MN ? 8192 : 16, sbo = 1024;
+                        const uint64_t dah = sdesc(a_hi + off, lbo, sbo), dbh = sdesc(b_hi + off, lbo, sbo);
+                        tc_mma(d, dah, dbh, id, (kb > 0 || kk > 0) ? 1u : 0u);
+                        if (TERMS == 3) {
+                            const uint64_t dal = sdesc(a_lo + off, lbo, sbo), dbl = sdesc(b_lo + off, lbo, sbo);
+                            tc_mma(d, dah, dbl, id, 1u);
+                            tc_mma(d, dal, dbh, id, 1u);
+                        }
                     }
+                    tc_commit(&empty_bar[s]);
                 }
-                tc_commit(&empty_bar[s]);
+                tc_commit(&tfull[acc]);
+                ++j;
             }
-            tc_commit(&tmem_full);
         }
     } else {
         // ================= epilogue: TMEM -> registers -> fp32 global (+ReLU)
         const int q = warp & 3;                       // TMEM lane quarter this warp may access
-        const int row = tile_m + q * 32 + lane;
-        float* Cbase = args.C + (MODE == 1 ? (int64_t)blockIdx.z * args.split_stride : 0);
-        const bool row_ok = MODE == 1 ? row < args.m_static : row < m_rows;
-        if (nkb > 0) {
-            mbar_wait(&tmem_full, 0);
-            tc_fence_after();
-        }
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t v[16];
-            if (nkb > 0) {
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = 0u;
+        int j = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const TileInfo ti = tile_info<MODE>(args, t, M);
+            const int row = ti.tm * kBM + q * 32 + lane;
+            const int tile_n = ti.tn * BN;
+            float* Cbase = args.C + (MODE == 1 ? (int64_t)ti.z * args.split_stride : 0);
+            const bool row_ok = MODE == 1 ? row < args.m_static : row < M;
+            const bool has = ti.nkb > 0;
+            const int acc = j & 1;
+            if (has) {
+                mbar_wait(&tfull[acc], (j >> 1) & 1);
+                tc_fence_after();
             }
-            if (row_ok) {
-                float* crow = Cbase + (int64_t)row * args.ldc + tile_n + c0;
-                const int lim = args.n_store - tile_n - c0;
-                if (lim >= 16 && (args.ldc % 4) == 0) {
-#pragma unroll
-                    for (int j = 0; j < 16; j += 4) {
-                        float4 f;
-                        f.x = __uint_as_float(v[j]); f.y = __uint_as_float(v[j + 1]);
-                        f.z = __uint_as_float(v[j + 2]); f.w = __uint_as_float(v[j + 3]);
-                        if (args.relu) { f.x = fmaxf(f.x, 0.f); f.y = fmaxf(f.y, 0.f); f.z = fmaxf(f.z, 0.f); f.w = fmaxf(f.w, 0.f); }
-                        *reinterpret_cast<float4*>(crow + j) = f;
-                    }
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t v[16];
+                if (has) {
+                    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::kAccCols + c0);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                          "=r"(v[15])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 } else {
-                    for (int j = 0; j < 16 && j < lim; ++j) {
-                        float f = __uint_as_float(v[j]);
-                        crow[j] = args.relu ? fmaxf(f, 0.f) : f;
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) v[x] = 0u;
+                }
+                if (row_ok) {
+                    float* crow = Cbase + (int64_t)row * args.ldc + tile_n + c0;
+                    const int lim = args.n_store - tile_n - c0;
+                    if (lim >= 16) {
+#pragma unroll
+                        for (int x = 0; x < 16; x += 4) {
+                            float4 f;
+                            f.x = __uint_as_float(v[x]); f.y = __uint_as_float(v[x + 1]);
+                            f.z = __uint_as_float(v[x + 2]); f.w = __uint_as_float(v[x + 3]);
+                            if (args.relu) { f.x = fmaxf(f.x, 0.f); f.y = fmaxf(f.y, 0.f); f.z = fmaxf(f.z, 0.f); f.w = fmaxf(f.w, 0.f); }
+                            *reinterpret_cast<float4*>(crow + x) = f;
+                        }
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < 16; ++x) {
+                            if (x < lim) {
+                                const float f = __uint_as_float(v[x]);
+                                crow[x] = args.relu ? fmaxf(f, 0.f) : f;
+                            }
+                        }
                     }
                 }
+            }
+            if (has) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                ++j;
             }
         }
     }
@@ -311,8 +360,10 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t co
 }
 
 namespace {
+constexpr int kSMs = 148;
+
 template <int BN, int STAGES, int TERMS, int MODE>
-cudaError_t launch_tc(dim3 grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
+cudaError_t launch_tc(int grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
     using Cfg = TileCfg<BN>;
     constexpr int kAPlanes = TERMS == 3 ? 2 : 1;
     constexpr int smem = STAGES * kAPlanes * (Cfg::kAStage + Cfg::kBStage) + 1024;
@@ -326,7 +377,7 @@ cudaError_t launch_tc(dim3 grid, const TcGemmMaps& mp, const GemmArgs& a, cudaSt
 }
 
 template <int TERMS, int MODE>
-cudaError_t dispatch_bn(int bn, dim3 grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
+cudaError_t dispatch_bn(int bn, int grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
     switch (bn) {
         case 16: return launch_tc<16, 4, TERMS, MODE>(grid, mp, a, s);
         case 32: return launch_tc<32, 4, TERMS, MODE>(grid, mp, a, s);
@@ -351,18 +402,20 @@ cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const 
     GemmArgs a{};
     a.m_ptr = m_ptr;
     a.m_static = m_static;
+    a.m_tiles_cap = (m_cap + kBM - 1) / kBM;
+    a.n_tiles = (n_pad + bn - 1) / bn;
+    a.splits = splits;
     a.k_blocks = (k_pad + kBK - 1) / kBK;
     a.n_store = n_store;
     a.C = C;
     a.ldc = ldc;
     a.relu = relu ? 1 : 0;
     a.split_stride = split_stride;
-    if (mode == 0) {
-        dim3 grid((m_cap + kBM - 1) / kBM, (n_pad + bn - 1) / bn, 1);
-        return bf16x3 ? dispatch_bn<3, 0>(bn, grid, maps, a, s) : dispatch_bn<1, 0>(bn, grid, maps, a, s);
-    }
-    // wgrad: C rows = m_static (K_pad of the layer), reduction length *m_ptr
-    dim3 grid((m_static + kBM - 1) / kBM, (n_pad + bn - 1) / bn, splits);
+    int tiles_cap;
+    if (mode == 0) tiles_cap = a.m_tiles_cap * a.n_tiles;
+    else tiles_cap = ((m_static + kBM - 1) / kBM) * a.n_tiles * splits;
+    const int grid = std::max(1, std::min(kSMs, tiles_cap));
+    if (mode == 0) return bf16x3 ? dispatch_bn<3, 0>(bn, grid, maps, a, s) : dispatch_bn<1, 0>(bn, grid, maps, a, s);
     return bf16x3 ? dispatch_bn<3, 1>(bn, grid, maps, a, s) : dispatch_bn<1, 1>(bn, grid, maps, a, s);
 }
 

@@ -10,8 +10,9 @@
 namespace gs {
 
 // ------------------------------------------------------------------ sampling side (sample.cu)
-struct ScanScratch { int32_t* partials; };   // kScanBlocks ints
-constexpr int kScanBlocks = 296;             // 2 x 148 SMs
+// Single-pass scan state: ctrl[0] = tile ticket, ctrl[1] = blocks done; status[t] = look-back
+// word of tile t (flag << 32 | value).  All zero between scans.
+struct ScanScratch { uint32_t* ctrl; unsigned long long* status; int max_tiles; };
 constexpr int kWarpGrid = 148 * 16;          // blocks of 256 threads for warp-per-item kernels
 
 // Epoch permutation keys (Philox tag 1): keys[i] = (w0<<32)|w1 of (train[i], 0, epoch).
@@ -22,7 +23,7 @@ void launch_begin_step(StepState* st, const int32_t* seed_src, int32_t n, int32_
                        uint32_t epoch, uint32_t g, int32_t* nodes, int32_t* map, cudaStream_t s);
 // Hop h: counts min(deg, k) -> blk_rowptr (exclusive scan), n_edges[h].
 void launch_hop_rowptr(int h, int k, StepState* st, const int32_t* nodes, const int64_t* row_ptr,
-                       int32_t* blk_rowptr, ScanScratch sc, cudaStream_t s);
+                       int32_t* blk_rowptr, int64_t max_dst, ScanScratch sc, cudaStream_t s);
 // Hop h: Floyd k-of-d per dst node (warp per node), blk_nbr, bitmap of unseen nbrs.
 void launch_sample_fill(int h, int k, const StepState* st, const int32_t* nodes,
                         const int64_t* row_ptr, const int32_t* col, const int32_t* blk_rowptr,
@@ -37,11 +38,11 @@ void launch_relabel_edges(int h, const StepState* st, const int32_t* blk_nbr, in
 // Transposed block CSR (rows = local src ids), deterministic (ascending dst index).
 void launch_transpose(int h, StepState* st, const int32_t* blk_rowptr, const int32_t* blk_col,
                       int32_t* tcount, int32_t* trowptr, int32_t* tcursor, int32_t* tdst,
-                      int32_t* tdst_sorted, ScanScratch sc, cudaStream_t s);
+                      int32_t* tdst_sorted, int64_t max_src, ScanScratch sc, cudaStream_t s);
 // ShaDow: induced block over S = nodes[0:n_src[hs]] -> state slot `slot`.
 void launch_induce(int hs, int slot, StepState* st, const int32_t* nodes, const int64_t* row_ptr,
                    const int32_t* col, const int32_t* map, int32_t* icount, int32_t* ind_rowptr,
-                   int32_t* ind_col, int32_t* tcount, ScanScratch sc, cudaStream_t s);
+                   int32_t* ind_col, int32_t* tcount, int64_t max_src, ScanScratch sc, cudaStream_t s);
 // map[nodes[i]] = -1 for i < n_src[h].
 void launch_reset_map(int h, const StepState* st, const int32_t* nodes, int32_t* map, cudaStream_t s);
 
@@ -68,9 +69,11 @@ void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const floa
 // grads[r*out + c] = Σ_z part[z][rpad(r)*n_pad + c]   (fixed z order; unpads rows/cols)
 void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, int rows, int out,
                          int in, int in_pad, bool sage, int n_pad, float* grads, cudaStream_t s);
-// W [K_pad x N_pad] and W^T [N_pad x K_pad] split planes from flat fp32 W (rows x out).
-void launch_pack_weight(const float* W, int rows, int out, int in, int in_pad, bool sage,
-                        int k_pad, int n_pad, Split Wkn, Split Wnk, cudaStream_t s);
+// W [K_pad x N_pad] and W^T [N_pad x K_pad] split planes from flat fp32 W (rows x out), all
+// layers in one launch.
+struct PackLayer { const float* W; int rows, out, in, in_pad, k_pad, n_pad; Split Wkn, Wnk; };
+struct PackAll { PackLayer l[kMaxHops]; int n; bool sage; };
+void launch_pack_all(const PackAll& p, cudaStream_t s);
 // Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total
 // written as split planes [rows x ldz] (+ zero tail rows).
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels,

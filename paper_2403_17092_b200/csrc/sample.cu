@@ -12,59 +12,119 @@ namespace gs {
 
 namespace {
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kScanThreads = 512;
+constexpr int kScanThreads = 256;
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
 // ------------------------------------------------------------------ device-wide exclusive scan
-// Two kernels.  Block b owns a contiguous chunk of [0, n); pass 1 sums it, pass 2 scans the
-// block sums, then its chunk tile by tile.  n is read on the device.  Deterministic.
-template <class F>
-__global__ void __launch_bounds__(kScanThreads) k_scan_partials(F f, int32_t* partials) {
-    using BR = cub::BlockReduce<int, kScanThreads>;
-    __shared__ typename BR::TempStorage tmp;
-    const int n = f.size();
-    const int chunk = ceil_div(ceil_div(n, gridDim.x), kScanThreads) * kScanThreads;
-    const int beg = blockIdx.x * chunk;
-    const int end = min(n, beg + chunk);
-    int s = 0;
-    for (int i = beg + threadIdx.x; i < end; i += kScanThreads) s += f(i);
-    s = BR(tmp).Sum(s);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+// Single pass, decoupled look-back.  Tiles of kScanTile items are claimed in order through a
+// ticket counter; a tile publishes its aggregate (flag 1), looks back over its predecessors'
+// published values, then publishes its inclusive prefix (flag 2).  n is read on the device,
+// the grid is sized for the worst case and surplus blocks exit; the last block to finish
+// resets the ticket/status words for the next scan.  Deterministic (integer sums).
+constexpr int kScanIPT = 8;
+constexpr int kScanTile = kScanThreads * kScanIPT;
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
 template <class F, class W>
-__global__ void __launch_bounds__(kScanThreads) k_scan_final(F f, W w, const int32_t* partials) {
-    using BR = cub::BlockReduce<int, kScanThreads>;
+__global__ void __launch_bounds__(kScanThreads) k_scan_lookback(F f, W w, ScanScratch sc) {
     using BS = cub::BlockScan<int, kScanThreads>;
-    __shared__ union { typename BR::TempStorage r; typename BS::TempStorage s; } tmp;
-    __shared__ int s_off;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ int s_vals[kScanTile + kScanTile / 32];
+    __shared__ int s_tile, s_excl;
     const int n = f.size();
-    int o = 0;
-    for (int j = threadIdx.x; j < (int)blockIdx.x; j += kScanThreads) o += partials[j];
-    o = BR(tmp.r).Sum(o);
-    if (threadIdx.x == 0) s_off = o;
+    const int ntiles = (n + kScanTile - 1) / kScanTile;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(&sc.ctrl[0], 1u);
     __syncthreads();
-    int carry = s_off;
-    const int chunk = ceil_div(ceil_div(n, gridDim.x), kScanThreads) * kScanThreads;
-    const int beg = blockIdx.x * chunk;
-    const int end = min(n, beg + chunk);
-    for (int base = beg; base < end; base += kScanThreads) {
-        const int i = base + threadIdx.x;
-        const int v = i < end ? f(i) : 0;
-        int excl, tile;
-        BS(tmp.s).ExclusiveSum(v, excl, tile);
-        if (i < end) w(i, carry + excl, v);
-        carry += tile;
+    const int tile = s_tile;
+    if (tile < ntiles) {
+        const int base = tile * kScanTile;
+        // striped (coalesced) evaluation into shared memory, blocked read-back
+#pragma unroll
+        for (int i = 0; i < kScanIPT; ++i) {
+            const int li = i * kScanThreads + threadIdx.x;
+            const int gi = base + li;
+            s_vals[li + li / 32] = gi < n ? f(gi) : 0;
+        }
         __syncthreads();
+        int v[kScanIPT], tsum = 0;
+#pragma unroll
+        for (int j = 0; j < kScanIPT; ++j) {
+            const int li = threadIdx.x * kScanIPT + j;
+            v[j] = s_vals[li + li / 32];
+            tsum += v[j];
+        }
+        int texcl, agg;
+        BS(tmp).ExclusiveSum(tsum, texcl, agg);
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            int excl = 0;
+            if (tile == 0) {
+                if (lane == 0) {
+                    __threadfence();
+                    atomicExch(&sc.status[0], (2ull << 32) | (unsigned)agg);
+                }
+            } else {
+                if (lane == 0) {
+                    __threadfence();
+                    atomicExch(&sc.status[tile], (1ull << 32) | (unsigned)agg);
+                }
+                int j = tile - 1;
+                while (true) {
+                    const int idx = j - lane;
+                    unsigned long long st = idx >= 0 ? ld_volatile_u64(&sc.status[idx]) : (2ull << 32);
+                    while (__any_sync(0xffffffffu, (st >> 32) == 0)) {
+                        if ((st >> 32) == 0) st = ld_volatile_u64(&sc.status[idx]);
+                    }
+                    const unsigned pmask = __ballot_sync(0xffffffffu, (st >> 32) == 2);
+                    const int last = pmask ? __ffs(pmask) - 1 : 31;
+                    int val = lane <= last ? (int)(unsigned)(st & 0xffffffffu) : 0;
+                    for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                    excl += val;
+                    if (pmask) break;
+                    j -= 32;
+                }
+                if (lane == 0) {
+                    __threadfence();
+                    atomicExch(&sc.status[tile], (2ull << 32) | (unsigned)(excl + agg));
+                }
+            }
+            if (lane == 0) s_excl = excl;
+        }
+        __syncthreads();
+        int run = s_excl + texcl;
+#pragma unroll
+        for (int j = 0; j < kScanIPT; ++j) {
+            const int gi = base + threadIdx.x * kScanIPT + j;
+            if (gi < n) w(gi, run, v[j]);
+            run += v[j];
+        }
+        if (tile == ntiles - 1 && threadIdx.x == kScanThreads - 1) w.finish(run);
+    } else if (ntiles == 0 && tile == 0 && threadIdx.x == 0) {
+        w.finish(0);
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) w.finish(s_off + partials[blockIdx.x]);
+    // the last block out resets the scan state (all look-backs are complete by then)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(&sc.ctrl[1], 1u);
+        s_tile = done == gridDim.x - 1 ? 1 : 0;
+    }
+    __syncthreads();
+    if (s_tile) {
+        for (int t = threadIdx.x; t < ntiles; t += kScanThreads) sc.status[t] = 0ull;
+        if (threadIdx.x == 0) { sc.ctrl[0] = 0u; sc.ctrl[1] = 0u; }
+    }
 }
 
 template <class F, class W>
-void device_scan(F f, W w, ScanScratch sc, cudaStream_t s) {
-    k_scan_partials<F><<<kScanBlocks, kScanThreads, 0, s>>>(f, sc.partials);
-    k_scan_final<F, W><<<kScanBlocks, kScanThreads, 0, s>>>(f, w, sc.partials);
+void device_scan(F f, W w, int64_t max_items, ScanScratch sc, cudaStream_t s) {
+    int grid = (int)std::min<int64_t>((max_items + kScanTile - 1) / kScanTile, sc.max_tiles);
+    if (grid < 1) grid = 1;
+    k_scan_lookback<F, W><<<grid, kScanThreads, 0, s>>>(f, w, sc);
 }
 
 // ------------------------------------------------------------------ functors
@@ -327,8 +387,8 @@ void launch_begin_step(StepState* st, const int32_t* seed_src, int32_t n, int32_
 }
 
 void launch_hop_rowptr(int h, int k, StepState* st, const int32_t* nodes, const int64_t* row_ptr,
-                       int32_t* blk_rowptr, ScanScratch sc, cudaStream_t s) {
-    device_scan(RowCountF{st, h, k, nodes, row_ptr}, RowPtrW{st, h, blk_rowptr}, sc, s);
+                       int32_t* blk_rowptr, int64_t max_dst, ScanScratch sc, cudaStream_t s) {
+    device_scan(RowCountF{st, h, k, nodes, row_ptr}, RowPtrW{st, h, blk_rowptr}, max_dst, sc, s);
 }
 
 void launch_sample_fill(int h, int k, const StepState* st, const int32_t* nodes, const int64_t* row_ptr,
@@ -340,7 +400,7 @@ void launch_sample_fill(int h, int k, const StepState* st, const int32_t* nodes,
 
 void launch_assign_new(int h, StepState* st, uint32_t* bits, int64_t nwords, int32_t* nodes,
                        int32_t* map, ScanScratch sc, cudaStream_t s) {
-    device_scan(PopF{bits, (int)nwords}, AssignW{st, h, bits, nodes, map}, sc, s);
+    device_scan(PopF{bits, (int)nwords}, AssignW{st, h, bits, nodes, map}, nwords, sc, s);
 }
 
 void launch_relabel_edges(int h, const StepState* st, const int32_t* blk_nbr, int32_t* blk_col,
@@ -350,17 +410,17 @@ void launch_relabel_edges(int h, const StepState* st, const int32_t* blk_nbr, in
 
 void launch_transpose(int h, StepState* st, const int32_t* blk_rowptr, const int32_t* blk_col,
                       int32_t* tcount, int32_t* trowptr, int32_t* tcursor, int32_t* tdst,
-                      int32_t* tdst_sorted, ScanScratch sc, cudaStream_t s) {
-    device_scan(TCountF{st, h, tcount}, TRowW{st, h, tcount, trowptr, tcursor}, sc, s);
+                      int32_t* tdst_sorted, int64_t max_src, ScanScratch sc, cudaStream_t s) {
+    device_scan(TCountF{st, h, tcount}, TRowW{st, h, tcount, trowptr, tcursor}, max_src, sc, s);
     k_transpose_fill<<<kWarpGrid, 256, 0, s>>>(h, st, blk_rowptr, blk_col, tcursor, tdst);
     k_transpose_sort<<<kWarpGrid, 256, 0, s>>>(h, st, trowptr, tdst, tdst_sorted);
 }
 
 void launch_induce(int hs, int slot, StepState* st, const int32_t* nodes, const int64_t* row_ptr,
                    const int32_t* col, const int32_t* map, int32_t* icount, int32_t* ind_rowptr,
-                   int32_t* ind_col, int32_t* tcount, ScanScratch sc, cudaStream_t s) {
+                   int32_t* ind_col, int32_t* tcount, int64_t max_src, ScanScratch sc, cudaStream_t s) {
     k_induce_count<<<kWarpGrid, 256, 0, s>>>(hs, st, nodes, row_ptr, col, map, icount);
-    device_scan(ICountF{st, hs, icount}, IRowW{st, hs, slot, ind_rowptr}, sc, s);
+    device_scan(ICountF{st, hs, icount}, IRowW{st, hs, slot, ind_rowptr}, max_src, sc, s);
     k_induce_fill<<<kWarpGrid, 256, 0, s>>>(hs, st, nodes, row_ptr, col, map, ind_rowptr, ind_col, tcount);
 }
 
