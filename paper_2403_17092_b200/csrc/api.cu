@@ -79,7 +79,7 @@ struct HopBufs {
     int64_t cap_dst = 0, cap_edges = 0, cap_src = 0;
     bool need_t = false;
     int32_t *rowptr = nullptr, *col = nullptr, *nbr = nullptr;
-    int32_t *trowptr = nullptr, *tcursor = nullptr, *tdst = nullptr, *tdst_s = nullptr;
+    int32_t *tcount = nullptr, *trowptr = nullptr, *tcursor = nullptr, *tdst = nullptr, *tdst_s = nullptr;
 };
 
 struct Layer {
@@ -108,10 +108,12 @@ struct gnn_model {
     std::vector<void*> owned;
 
     StepState* st = nullptr;
-    int32_t *nodes = nullptr, *map = nullptr, *tcount = nullptr, *icount = nullptr;
+    int32_t *nodes = nullptr, *map = nullptr, *icount = nullptr;
+    unsigned long long* status = nullptr;
+    GridBarrier* bar = nullptr;
+    SampleParams sp{};
     uint32_t* bits = nullptr;
-    int64_t nwords = 0, nodes_cap = 0, tcap = 0;
-    ScanScratch sc{};
+    int64_t nwords = 0, nodes_cap = 0;
     HopBufs hb[kMaxHops + 1];
     std::vector<Layer> layers;
     float *params = nullptr, *grads = nullptr;
@@ -200,39 +202,9 @@ const int32_t* rows_ptr(gnn_model* m, int li) {   // output rows of layer li (0-
 }
 
 // ---------------------------------------------------------------- step body
+// Sampling, relabel, ShaDow induce, transposed blocks, map reset: one persistent launch.
 void enqueue_sampling(gnn_model* m) {
-    gnn_graph* g = m->g;
-    cudaStream_t s = m->stream;
-    for (int h = 0; h < m->hops; ++h) {
-        const int k = m->cfg.fanouts[m->hops - 1 - h];
-        HopBufs& b = m->hb[h];
-        K(m, GNN_K_SCAN, [&] { launch_hop_rowptr(h, k, m->st, m->nodes, g->row_ptr, b.rowptr, b.cap_dst, m->sc, s); });
-        K(m, GNN_K_SAMPLE, [&] {
-            launch_sample_fill(h, k, m->st, m->nodes, g->row_ptr, g->col, b.rowptr, b.nbr, m->map, m->bits,
-                               m->cfg.seed, s);
-        });
-        K(m, GNN_K_RELABEL, [&] { launch_assign_new(h, m->st, m->bits, m->nwords, m->nodes, m->map, m->sc, s); });
-        K(m, GNN_K_RELABEL, [&] {
-            launch_relabel_edges(h, m->st, b.nbr, b.col, m->map, b.need_t ? m->tcount : nullptr, s);
-        });
-        if (b.need_t)
-            K(m, GNN_K_TRANSPOSE, [&] {
-                launch_transpose(h, m->st, b.rowptr, b.col, m->tcount, b.trowptr, b.tcursor, b.tdst, b.tdst_s,
-                                 b.cap_src, m->sc, s);
-            });
-    }
-    if (m->shadow) {
-        HopBufs& b = m->hb[m->slot];
-        K(m, GNN_K_INDUCE, [&] {
-            launch_induce(m->hops - 1, m->slot, m->st, m->nodes, g->row_ptr, g->col, m->map, m->icount,
-                          b.rowptr, b.col, m->tcount, b.cap_src, m->sc, s);
-        });
-        K(m, GNN_K_TRANSPOSE, [&] {
-            launch_transpose(m->slot, m->st, b.rowptr, b.col, m->tcount, b.trowptr, b.tcursor, b.tdst,
-                             b.tdst_s, b.cap_src, m->sc, s);
-        });
-    }
-    K(m, GNN_K_OTHER, [&] { launch_reset_map(m->hops - 1, m->st, m->nodes, m->map, s); });
+    K(m, GNN_K_SAMPLE, [&] { launch_sample_step(m->sp, m->stream); });
 }
 
 void enqueue_training(gnn_model* m) {
@@ -500,22 +472,32 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         b.need_t = true;
     }
     m->nwords = (g->N + 31) / 32;
-    m->tcap = m->nodes_cap + 1;
     AL(m->st, 1);
     AL(m->nodes, m->nodes_cap);
     AL(m->map, g->N);
     AL(m->bits, m->nwords);
-    AL(m->tcount, m->tcap);
     AL(m->icount, m->nodes_cap);
-    {   // single-pass scan state, sized for the largest scan (bitmap words or node lists)
-        const int64_t items = std::max<int64_t>(m->nwords, m->nodes_cap + 1);
-        m->sc.max_tiles = (int)((items + 2047) / 2048);
-        AL(m->sc.ctrl, 2);
-        AL(m->sc.status, m->sc.max_tiles);
-        CK(cudaMemset(m->sc.ctrl, 0, 2 * sizeof(uint32_t)));
-        CK(cudaMemset(m->sc.status, 0, sizeof(unsigned long long) * m->sc.max_tiles));
-    }
     AL(m->seeds_in, c.batch_size);
+    const int sgrid = sample_step_grid();
+    AL(m->status, (int64_t)sample_step_sites(m->hops) * sgrid);
+    CK(cudaMemset(m->status, 0, sizeof(unsigned long long) * sample_step_sites(m->hops) * sgrid));
+    AL(m->bar, 1);
+    CK(cudaMemset(m->bar, 0, sizeof(GridBarrier)));
+    m->sp = SampleParams{};
+    m->sp.st = m->st;
+    m->sp.row_ptr = g->row_ptr;
+    m->sp.col = g->col;
+    m->sp.nodes = m->nodes;
+    m->sp.map = m->map;
+    m->sp.bits = m->bits;
+    m->sp.nwords = (int)m->nwords;
+    m->sp.seed = c.seed;
+    m->sp.hops = m->hops;
+    m->sp.shadow = m->shadow ? 1 : 0;
+    m->sp.slot = m->shadow ? m->slot : -1;
+    m->sp.icount = m->icount;
+    m->sp.status = m->status;
+    m->sp.bar = m->bar;
     for (int h = 0; h <= m->hops; ++h) {
         if (h == m->hops && !m->shadow) break;
         HopBufs& b = m->hb[h];
@@ -523,15 +505,21 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         AL(b.col, b.cap_edges);
         if (h < m->hops) AL(b.nbr, b.cap_edges);
         if (b.need_t) {
+            AL(b.tcount, b.cap_src + 1);
             AL(b.trowptr, b.cap_src + 1);
             AL(b.tcursor, b.cap_src + 1);
             AL(b.tdst, b.cap_edges);
             AL(b.tdst_s, b.cap_edges);
+            CK(cudaMemset(b.tcount, 0, sizeof(int32_t) * (b.cap_src + 1)));
         }
+        HopIO& io = m->sp.hop[h];
+        io.k = h < m->hops ? c.fanouts[m->hops - 1 - h] : 0;
+        io.rowptr = b.rowptr; io.nbr = b.nbr; io.col = b.col;
+        io.tcount = b.need_t ? b.tcount : nullptr;
+        io.trowptr = b.trowptr; io.tcursor = b.tcursor; io.tdst = b.tdst; io.tdst_s = b.tdst_s;
     }
     CK(cudaMemset(m->map, 0xff, sizeof(int32_t) * g->N));
     CK(cudaMemset(m->bits, 0, sizeof(uint32_t) * m->nwords));
-    CK(cudaMemset(m->tcount, 0, sizeof(int32_t) * m->tcap));
     CK(cudaMemset(m->st, 0, sizeof(StepState)));
 
     // ---- layers
@@ -877,6 +865,19 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
         if (need)
             CK(cudaMemcpy2D(out_host, sizeof(float) * ly.out, ly.H, sizeof(float) * ly.n_pad, sizeof(float) * ly.out,
                             st.batch_n, cudaMemcpyDeviceToHost));
+        return GNN_OK;
+    }
+    if (what == GNN_DBG_PHASES) {   // sampling-kernel phase durations of the last step (us)
+        GridBarrier hb{};
+        CK(cudaMemcpy(&hb, m->bar, sizeof(GridBarrier), cudaMemcpyDeviceToHost));
+        const int nb = 2 * m->hops + 3 + (m->shadow ? 1 : 0);
+        if (n < nb) return fail(GNN_ERR_BUFFER, "need " + std::to_string(nb));
+        unsigned long long prev = hb.t0;
+        for (int i = 0; i < nb; ++i) {
+            const unsigned long long t = hb.ts[(hb.nts - nb + i) & 31u];
+            out_host[i] = (float)((double)(t - prev) * 1e-3);
+            prev = t;
+        }
         return GNN_OK;
     }
     if (what >= GNN_DBG_ACT && what < GNN_DBG_ACT + m->L) {

@@ -19,7 +19,8 @@ struct StepState {
     uint32_t g;           // global batch index (sampling key, R3)
     float loss;           // this rank's Σ ℓ_i / b_total
     uint32_t ce_done;     // CE blocks finished (reset by the last one)
-    int32_t pad[2];
+    uint32_t seq;         // step sequence number (tags the sampling kernel's scan words)
+    int32_t pad;
     float row_loss[1024]; // ℓ_i of the batch rows (batch_size <= 1024)
 };
 

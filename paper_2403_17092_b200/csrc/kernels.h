@@ -9,10 +9,7 @@
 
 namespace gs {
 
-// ------------------------------------------------------------------ sampling side (sample.cu)
-// Single-pass scan state: ctrl[0] = tile ticket, ctrl[1] = blocks done; status[t] = look-back
-// word of tile t (flag << 32 | value).  All zero between scans.
-struct ScanScratch { uint32_t* ctrl; unsigned long long* status; int max_tiles; };
+// ------------------------------------------------------------------ sampling side (sample.cu, sample_step.cu)
 constexpr int kWarpGrid = 148 * 16;          // blocks of 256 threads for warp-per-item kernels
 
 // Epoch permutation keys (Philox tag 1): keys[i] = (w0<<32)|w1 of (train[i], 0, epoch).
@@ -21,30 +18,41 @@ void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t ep
 // Start of a step: state fields, seeds -> nodes[0:n), map[seed] = i.
 void launch_begin_step(StepState* st, const int32_t* seed_src, int32_t n, int32_t b_total,
                        uint32_t epoch, uint32_t g, int32_t* nodes, int32_t* map, cudaStream_t s);
-// Hop h: counts min(deg, k) -> blk_rowptr (exclusive scan), n_edges[h].
-void launch_hop_rowptr(int h, int k, StepState* st, const int32_t* nodes, const int64_t* row_ptr,
-                       int32_t* blk_rowptr, int64_t max_dst, ScanScratch sc, cudaStream_t s);
-// Hop h: Floyd k-of-d per dst node (warp per node), blk_nbr, bitmap of unseen nbrs.
-void launch_sample_fill(int h, int k, const StepState* st, const int32_t* nodes,
-                        const int64_t* row_ptr, const int32_t* col, const int32_t* blk_rowptr,
-                        int32_t* blk_nbr, const int32_t* map, uint32_t* bits, uint64_t seed,
-                        cudaStream_t s);
-// Hop h: new nodes in ascending global id (bitmap rank), nodes[n_dst + r], map, n_src.
-void launch_assign_new(int h, StepState* st, uint32_t* bits, int64_t nwords, int32_t* nodes,
-                       int32_t* map, ScanScratch sc, cudaStream_t s);
-// Hop h: blk_col[e] = map[blk_nbr[e]]; optional transposed counts.
-void launch_relabel_edges(int h, const StepState* st, const int32_t* blk_nbr, int32_t* blk_col,
-                          const int32_t* map, int32_t* tcount, cudaStream_t s);
-// Transposed block CSR (rows = local src ids), deterministic (ascending dst index).
-void launch_transpose(int h, StepState* st, const int32_t* blk_rowptr, const int32_t* blk_col,
-                      int32_t* tcount, int32_t* trowptr, int32_t* tcursor, int32_t* tdst,
-                      int32_t* tdst_sorted, int64_t max_src, ScanScratch sc, cudaStream_t s);
-// ShaDow: induced block over S = nodes[0:n_src[hs]] -> state slot `slot`.
-void launch_induce(int hs, int slot, StepState* st, const int32_t* nodes, const int64_t* row_ptr,
-                   const int32_t* col, const int32_t* map, int32_t* icount, int32_t* ind_rowptr,
-                   int32_t* ind_col, int32_t* tcount, int64_t max_src, ScanScratch sc, cudaStream_t s);
-// map[nodes[i]] = -1 for i < n_src[h].
-void launch_reset_map(int h, const StepState* st, const int32_t* nodes, int32_t* map, cudaStream_t s);
+
+struct GridBarrier {
+    unsigned count, gen;
+    unsigned nts, pad;
+    unsigned long long t0;        // kernel start (globaltimer, ns)
+    unsigned long long ts[32];    // ring of barrier-release times
+};
+// Per block (hop h, or the ShaDow induced block at index `slot`): CSR of the block
+// (rowptr over dst, nbr = global source ids, col = local source ids) and, when tcount is
+// non-null, its transposed CSR (trowptr over local sources, tdst_s = dst indices ascending).
+struct HopIO {
+    int k;
+    int32_t *rowptr, *nbr, *col;
+    int32_t *tcount, *trowptr, *tcursor, *tdst, *tdst_s;
+};
+struct SampleParams {
+    StepState* st;
+    const int64_t* row_ptr;
+    const int32_t* col;
+    int32_t* nodes;      // the batch's node list: src_h = nodes[0:n_src[h]]
+    int32_t* map;        // global -> local id, -1 outside the batch
+    uint32_t* bits;      // N-bit set of unseen neighbours (all zero between phases)
+    int nwords;
+    uint64_t seed;
+    int hops, shadow, slot;
+    int32_t* icount;     // ShaDow: induced edges per node of S
+    unsigned long long* status;   // look-back words [sample_step_sites(hops) x grid], tagged by StepState::seq
+    GridBarrier* bar;
+    HopIO hop[kMaxHops + 1];
+};
+// One persistent launch: every hop's sampling + relabel, the ShaDow induced block, the
+// transposed blocks, the map reset.  Grid = co-resident blocks (occupancy x SMs).
+void launch_sample_step(const SampleParams& p, cudaStream_t s);
+int sample_step_grid();
+int sample_step_sites(int hops);
 
 // ------------------------------------------------------------------ training side (dense.cu)
 // Layouts: fp32 activations are row-major with row stride = padded

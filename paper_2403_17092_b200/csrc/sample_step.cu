@@ -1,0 +1,356 @@
+// The sampling half of a training step as ONE persistent kernel (sm_100a): neighbour
+// sampling of every hop (§2.2), dedup + relabel, the ShaDow induced
+// block (lines 170-171), the transposed blocks of the backward pass, and the map reset.
+//
+// The phases depend on each other through whole-grid results ("all neighbours marked", "all
+// new ids assigned"), so they are separated by a software grid barrier instead of kernel
+// boundaries: one launch replaces ~20.  Prefix sums inside a
+// phase use decoupled look-back between the blocks' contiguous chunks (no extra barrier).
+// One block per SM (all co-resident).  Every extent is read from the device StepState, so
+// the launch replays inside the step's CUDA graph.
+//
+// Data produced inside the kernel is read with plain (coherent) loads after a barrier; the
+// graph (row_ptr, col) is read through the read-only path.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+#include <climits>
+
+#include "kernels.h"
+
+namespace gs {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kThreads = 1024;   // one block per SM: a cheaper grid barrier
+constexpr int kWarps = kThreads / 32;
+
+using BlockScan = cub::BlockScan<int, kThreads>;
+using BlockReduce = cub::BlockReduce<int, kThreads>;
+
+struct Smem {
+    union {
+        typename BlockScan::TempStorage scan;
+        typename BlockReduce::TempStorage reduce;
+    } cub;
+    int carry;
+    int excl;
+    int total;
+};
+
+// Grid barrier (all blocks are resident): one atomic per block; block 0 adds 2^31 - (nb-1),
+// the others 1, so the last arrival flips bit 31 of the counter (low bits return to 0).  The
+// gpu-scope fences order the phases' global writes and invalidate this SM's L1.
+__device__ __forceinline__ void grid_sync(GridBarrier* b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned nb = gridDim.x;
+        const unsigned inc = blockIdx.x == 0 ? (0x80000000u - (nb - 1u)) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(&b->count, inc);
+        if (((old ^ (old + inc)) & 0x80000000u) != 0u) {   // last arrival: phase timestamp (debug)
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            b->ts[b->nts & 31u] = t;
+            b->nts = b->nts + 1u;
+        } else {
+            volatile unsigned* vc = &b->count;
+            while (((old ^ *vc) & 0x80000000u) == 0u) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void chunk_of(int n, int& beg, int& end) {
+    const int c = (n + gridDim.x - 1) / gridDim.x;
+    beg = min(n, (int)blockIdx.x * c);
+    end = min(n, beg + c);
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// Exclusive scan of f over [0, n), each block owning a contiguous chunk, in ONE phase:
+// the block publishes its chunk sum, looks back over its predecessors' published sums
+// (status words tagged with the step's sequence number, so no reset is needed), publishes
+// its inclusive prefix, then scans its chunk: put(i, excl, v).  Returns the grid total in
+// the last block (-1 elsewhere).  Deterministic (integer sums).
+template <class F, class PUT>
+__device__ int chunk_scan(Smem& sm, int n, F f, PUT put, unsigned long long* status, uint32_t tag) {
+    int beg, end;
+    chunk_of(n, beg, end);
+    int s = 0;
+    for (int i = beg + threadIdx.x; i < end; i += kThreads) s += f(i);
+    const int agg = BlockReduce(sm.cub.reduce).Sum(s);
+    const unsigned long long tg = (unsigned long long)(tag & 0xFFFFFFu) << 40;
+    if (threadIdx.x == 0) {   // publish this chunk's sum
+        __threadfence();
+        atomicExch(&status[blockIdx.x], tg | (1ull << 32) | (unsigned)agg);
+    }
+    // read every predecessor's published sum in parallel (one thread each; grid <= threads)
+    int pre = 0;
+    for (int j = threadIdx.x; j < (int)blockIdx.x; j += kThreads) {
+        unsigned long long w = ld_volatile_u64(&status[j]);
+        while ((w & ~0xFFFFFFFFFFull) != tg) w = ld_volatile_u64(&status[j]);
+        pre += (int)(unsigned)(w & 0xFFFFFFFFull);
+    }
+    __syncthreads();
+    const int excl = BlockReduce(sm.cub.reduce).Sum(pre);
+    if (threadIdx.x == 0) { sm.excl = excl; sm.carry = excl; sm.total = excl + agg; }
+    __syncthreads();
+    for (int base = beg; base < end; base += kThreads) {
+        const int i = base + threadIdx.x;
+        const int v = i < end ? f(i) : 0;
+        int ex, tile;
+        BlockScan(sm.cub.scan).ExclusiveSum(v, ex, tile);
+        const int carry = sm.carry;
+        if (i < end) put(i, carry + ex, v);
+        __syncthreads();
+        if (threadIdx.x == 0) sm.carry = carry + tile;
+        __syncthreads();
+    }
+    return blockIdx.x == gridDim.x - 1 ? sm.total : -1;
+}
+
+__device__ __forceinline__ int min_deg(const int64_t* row_ptr, int v, int k) {
+    const int64_t d = __ldg(row_ptr + v + 1) - __ldg(row_ptr + v);
+    return d < k ? (int)d : k;
+}
+
+// Floyd k-of-d (R4) for 32/GS frontier nodes per warp, one lane group of GS >= k
+// lanes per node: lane i draws t_i = floor(r_i (j_i+1) / 2^32), j_i = d-k+i (all draws are
+// independent of the picks, so they run in parallel); a k-step ballot resolve replaces a
+// taken t_i by j_i; a shuffle rank-sort writes the picks in ascending CSR position.  Rows with
+// d <= k are copied whole.  Several nodes per warp keep more dependent loads in flight.
+template <int GS>
+__device__ __forceinline__ void sample_nodes(const SampleParams& P, int h, int k, int i, bool valid, uint32_t epoch,
+                                             uint32_t g, int lane) {
+    const HopIO& H = P.hop[h];
+    const int lg = lane & (GS - 1);
+    const int gbase = lane & ~(GS - 1);
+    int v = 0, d = 0, out = 0;
+    int64_t start = 0;
+    if (valid) {
+        v = P.nodes[i];
+        start = __ldg(P.row_ptr + v);
+        d = (int)(__ldg(P.row_ptr + v + 1) - start);
+        out = H.rowptr[i];
+    }
+    const bool floyd = d > k;
+    const int j = d - k + lg;
+    uint32_t t = 0;
+    if (floyd && lg < k) {
+        const uint32_t r = method_draw(P.seed, 0u, (uint32_t)v, g, epoch, (uint32_t)h, (uint32_t)lg);
+        t = (uint32_t)(((uint64_t)r * (uint64_t)(j + 1)) >> 32);
+    }
+    int pick = -1;
+    for (int q = 0; q < k; ++q) {                 // k is uniform: every lane runs the resolve
+        const int tq = (int)__shfl_sync(kFull, t, q, GS);
+        const unsigned hit = (__ballot_sync(kFull, lg < q && pick == tq) >> gbase) & ((GS == 32) ? kFull : ((1u << GS) - 1u));
+        if (lg == q) pick = hit ? j : tq;
+    }
+    int rank = 0;
+    for (int q = 0; q < k; ++q) rank += (__shfl_sync(kFull, pick, q, GS) < pick) ? 1 : 0;
+    if (floyd) {
+        if (lg < k) {
+            const int u = __ldg(P.col + start + pick);
+            H.nbr[out + rank] = u;
+            if (P.map[u] < 0) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
+        }
+    } else {
+        for (int q = lg; q < d; q += GS) {
+            const int u = __ldg(P.col + start + q);
+            H.nbr[out + q] = u;
+            if (P.map[u] < 0) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
+        }
+    }
+}
+
+template <int GS>
+__device__ __forceinline__ void sample_chunk(const SampleParams& P, int h, int k, int beg, int end, uint32_t epoch,
+                                             uint32_t g, int lane, int wib) {
+    constexpr int kPerWarp = 32 / GS;
+    for (int i0 = beg + wib * kPerWarp; i0 < end; i0 += kWarps * kPerWarp) {
+        const int i = i0 + lane / GS;
+        sample_nodes<GS>(P, h, k, i, i < end, epoch, g, lane);
+    }
+}
+
+__device__ __forceinline__ void relabel_edges(const SampleParams& P, const HopIO& H, int ne, int gtid, int nthreads) {
+    for (int e = gtid; e < ne; e += nthreads) {
+        const int c = P.map[H.nbr[e]];
+        H.col[e] = c;
+        if (H.tcount) atomicAdd(&H.tcount[c], 1);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
+    __shared__ Smem sm;
+    StepState* st = P.st;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int gtid = blockIdx.x * kThreads + threadIdx.x, nthreads = gridDim.x * kThreads;
+    const uint32_t epoch = st->epoch, g = st->g, tag = st->seq;
+    const int G = gridDim.x;
+    int site = 0;   // scan site index (own status words per scan in the step)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.bar->t0 = t;
+    }
+
+    for (int h = 0; h < P.hops; ++h) {
+        const HopIO& H = P.hop[h];
+        const int k = H.k;
+        // ---- phase 1: relabel the previous hop (its new ids are all assigned); blk_rowptr =
+        //      exclusive scan of min(deg, k); Floyd-sample this block's nodes, mark unseen nbrs
+        if (h > 0) relabel_edges(P, P.hop[h - 1], st->n_edges[h - 1], gtid, nthreads);
+        const int nd = st->n_dst[h];
+        {
+            const int tot = chunk_scan(sm, nd, [&](int i) { return min_deg(P.row_ptr, P.nodes[i], k); },
+                                       [&](int i, int ex, int) { H.rowptr[i] = ex; }, P.status + (site++) * G, tag);
+            if (tot >= 0 && threadIdx.x == 0) { H.rowptr[nd] = tot; st->n_edges[h] = tot; }
+            int beg, end;
+            chunk_of(nd, beg, end);
+            if (k <= 8) sample_chunk<8>(P, h, k, beg, end, epoch, g, lane, wib);
+            else if (k <= 16) sample_chunk<16>(P, h, k, beg, end, epoch, g, lane, wib);
+            else sample_chunk<32>(P, h, k, beg, end, epoch, g, lane, wib);
+        }
+        grid_sync(P.bar);
+        // ---- phase 2: new nodes in ascending global id (R6): nodes[n_dst + rank], map
+        {
+            const int tot = chunk_scan(sm, P.nwords, [&](int w) { return __popc(P.bits[w]); },
+                                       [&](int w, int ex, int cnt) {
+                                           if (!cnt) return;
+                                           uint32_t word = P.bits[w];
+                                           const int base = nd + ex;
+                                           int r = 0;
+                                           while (word) {
+                                               const int b = __ffs(word) - 1;
+                                               const int u = w * 32 + b;
+                                               P.nodes[base + r] = u;
+                                               P.map[u] = base + r;
+                                               ++r;
+                                               word &= word - 1;
+                                           }
+                                           P.bits[w] = 0u;
+                                       }, P.status + (site++) * G, tag);
+            if (tot >= 0 && threadIdx.x == 0) {
+                st->n_src[h] = nd + tot;
+                st->n_dst[h + 1] = nd + tot;
+            }
+        }
+        grid_sync(P.bar);
+    }
+
+    // ---- relabel the last hop; ShaDow: count the induced edges of every node of S
+    const int L1 = P.hops - 1;
+    relabel_edges(P, P.hop[L1], st->n_edges[L1], gtid, nthreads);
+    const int nS = st->n_src[L1];
+    if (P.shadow) {
+        for (int i = blockIdx.x * kWarps + wib; i < nS; i += G * kWarps) {   // |{u in row v : u in S}|
+            const int v = P.nodes[i];
+            int c = 0;
+            for (int64_t p = __ldg(P.row_ptr + v) + lane; p < __ldg(P.row_ptr + v + 1); p += 32)
+                c += P.map[__ldg(P.col + p)] >= 0;
+            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+            if (lane == 0) P.icount[i] = c;
+        }
+        grid_sync(P.bar);
+        const HopIO& S = P.hop[P.slot];
+        const int tot = chunk_scan(sm, nS, [&](int i) { return P.icount[i]; },
+                                   [&](int i, int ex, int) { S.rowptr[i] = ex; }, P.status + (site++) * G, tag);
+        if (tot >= 0 && threadIdx.x == 0) {
+            S.rowptr[nS] = tot;
+            st->n_dst[P.slot] = nS; st->n_src[P.slot] = nS; st->n_edges[P.slot] = tot;
+        }
+        __syncthreads();
+        // edges (local(u) -> i) in CSR order of row S[i] (R20)
+        int beg, end;
+        chunk_of(nS, beg, end);
+        for (int i = beg + wib; i < end; i += kWarps) {
+            const int v = P.nodes[i];
+            int out = S.rowptr[i];
+            const int64_t rb = __ldg(P.row_ptr + v), re = __ldg(P.row_ptr + v + 1);
+            for (int64_t p0 = rb; p0 < re; p0 += 32) {
+                const int64_t p = p0 + lane;
+                const int m = p < re ? P.map[__ldg(P.col + p)] : -1;
+                const unsigned bal = __ballot_sync(kFull, m >= 0);
+                if (m >= 0) {
+                    S.col[out + __popc(bal & ((1u << lane) - 1u))] = m;
+                    atomicAdd(&S.tcount[m], 1);
+                }
+                out += __popc(bal);
+            }
+        }
+    }
+    grid_sync(P.bar);
+
+    // ---- transposed blocks (rows = local src ids), all needed blocks together
+    for (int h = 0; h <= P.hops; ++h) {
+        const HopIO& H = P.hop[h];
+        if (!H.tcount) continue;
+        const int ns = st->n_src[h];
+        const int tot = chunk_scan(sm, ns, [&](int u) { return H.tcount[u]; },
+                                   [&](int u, int ex, int) { H.trowptr[u] = ex; H.tcursor[u] = ex; H.tcount[u] = 0; },
+                                   P.status + (site++) * G, tag);
+        if (tot >= 0 && threadIdx.x == 0) H.trowptr[ns] = tot;
+    }
+    grid_sync(P.bar);
+    for (int h = 0; h <= P.hops; ++h) {
+        const HopIO& H = P.hop[h];
+        if (!H.tcount) continue;
+        const int nd = st->n_dst[h];
+        for (int i = blockIdx.x * kWarps + wib; i < nd; i += G * kWarps)
+            for (int e = H.rowptr[i] + lane; e < H.rowptr[i + 1]; e += 32) H.tdst[atomicAdd(&H.tcursor[H.col[e]], 1)] = i;
+    }
+    grid_sync(P.bar);
+    // rank-sort every transposed row (fixed summation order); reset map
+    for (int h = 0; h <= P.hops; ++h) {
+        const HopIO& H = P.hop[h];
+        if (!H.tcount) continue;
+        const int ns = st->n_src[h];
+        for (int u = blockIdx.x * kWarps + wib; u < ns; u += G * kWarps) {
+            const int b0 = H.trowptr[u];
+            const int len = H.trowptr[u + 1] - b0;
+            if (len <= 32) {
+                const int x = lane < len ? H.tdst[b0 + lane] : INT_MAX;
+                int rank = 0;
+                for (int q = 0; q < len; ++q) rank += (__shfl_sync(kFull, x, q) < x) ? 1 : 0;
+                if (lane < len) H.tdst_s[b0 + rank] = x;
+            } else {
+                for (int a = lane; a < len; a += 32) {
+                    const int x = H.tdst[b0 + a];
+                    int rank = 0;
+                    for (int b = 0; b < len; ++b) rank += (H.tdst[b0 + b] < x) ? 1 : 0;
+                    H.tdst_s[b0 + rank] = x;
+                }
+            }
+        }
+    }
+    for (int i = gtid; i < nS; i += nthreads) P.map[P.nodes[i]] = -1;
+}
+
+}  // namespace
+
+int sample_step_grid() {
+    static int grid = 0;
+    if (!grid) {
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_step, kThreads, 0);
+        grid = std::max(1, std::min(per_sm, 1)) * std::max(sms, 1);
+    }
+    return grid;
+}
+
+// scan sites per step: 2 per hop + 1 induce + 1 per transposed block
+int sample_step_sites(int hops) { return 2 * hops + 1 + (hops + 1); }
+
+void launch_sample_step(const SampleParams& p, cudaStream_t s) {
+    k_sample_step<<<sample_step_grid(), kThreads, 0, s>>>(p);
+}
+
+}  // namespace gs

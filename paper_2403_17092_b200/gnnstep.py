@@ -294,3 +294,13 @@ class Model:
     @property
     def launches_per_step(self) -> int:
         return lib().gnn_launches_per_step(self.h)
+
+
+def _phases(self, n=32):
+    out = np.zeros(n, dtype=np.float32)
+    _check(lib().gnn_debug_get(self.h, 8, _ptr(out), n))
+    nb = 2 * len(self.fanouts) + 3 + (1 if self.sampler == "shadow" else 0)
+    return out[:nb]
+
+
+Model.sampling_phases_us = _phases
