@@ -112,8 +112,10 @@ def kernel_work(w, sz, kind, terms=3, splits=None):
     L = w.num_layers
     byt, flo = 0.0, 0.0
     for li, (fi, fo, in_pad, k_pad, n_pad) in enumerate(layer_dims(w)):
-        h = L - 1 - li if w.sampler == "neighbor" else L  # ShaDow: the induced block slot
+        h = L - 1 - li if w.sampler == "neighbor" else len(w.fanouts)  # ShaDow: the induced block slot
         M, S, E = sz["n_dst"][h], sz["n_src"][h], sz["n_edges"][h]
+        if w.sampler == "shadow" and li == L - 1:
+            M = sz["n_dst"][0]                     # last layer: the seeds' rows only (R19)
         if kind == "agg_l1" and li == 0 or kind == "agg" and li > 0:
             byt += S * in_pad * 4 + M * k_pad * 4 + E * 4 + (M + 1) * 4
         elif kind == "gemm_fwd":

@@ -78,6 +78,23 @@ gnn_status gnn_graph_create(int64_t num_nodes, const int64_t* row_ptr_host,
                             int32_t num_classes, int32_t device, gnn_graph** out);
 gnn_status gnn_graph_destroy(gnn_graph* g);
 
+/* Row-sharded feature table (BASELINE.json configs[4]: papers100M-scale features split across
+ * the GPUs of a box).  Rows are split into nshards uniform blocks of rps = ceil(N/nshards);
+ * this process holds block `shard`, i.e. rows [shard*rps, min(N, (shard+1)*rps)), given in
+ * shard_features_host (row-major, feat_stride).  CSR and labels are full (replicated).
+ * gnn_shard_export writes the CUDA IPC handle (64 bytes) of the local block; after all
+ * processes exchanged handles (the caller's collective), gnn_shard_import(handles = nshards
+ * x 64 bytes, in shard order) maps every peer block; the layer-1 gather then reads row r
+ * from block r / rps with direct peer loads (NVLink on a multi-GPU box).  Training a
+ * sharded graph before the import returns STATE. */
+gnn_status gnn_graph_create_sharded(int64_t num_nodes, const int64_t* row_ptr_host,
+                                    const int32_t* col_idx_host, int32_t feat_dim, int32_t feat_stride,
+                                    int32_t nshards, int32_t shard, const float* shard_features_host,
+                                    const int32_t* labels_host, int32_t num_classes, int32_t device,
+                                    gnn_graph** out);
+gnn_status gnn_shard_export(gnn_graph* g, uint8_t handle_out_host[64]);
+gnn_status gnn_shard_import(gnn_graph* g, const uint8_t* handles_host);
+
 /* ---------------------------------------------------------------- model
  * Layers l = 1..L are numbered input-first; dims = [F, hidden, ..., hidden, C].
  * fanouts are listed input-layer-first (R1): hop h (seeds = hop 0)
@@ -121,6 +138,13 @@ gnn_status gnn_set_params(gnn_model* m, const float* in_host, int64_t n);
  * Rank 0 calls gnn_comm_get_unique_id; the caller broadcasts the 128 bytes (e.g.
  * torch.distributed); every rank then calls gnn_comm_init (collective). */
 gnn_status gnn_comm_get_unique_id(uint8_t out_host[128]);
+/* Host-only plan of one synchronous-SGD step (the engine's own batch -> rank rule):
+ * g = step*world + rank; n = seeds of global batch g (0 if g >= ceil(n_train/B));
+ * offset = g*B into the epoch permutation; b_total = seeds of the step over all ranks.
+ * steps_per_epoch = ceil(ceil(n_train/B) / world).  PARAM on invalid sizes. */
+gnn_status gnn_plan_step(int64_t n_train, int32_t batch_size, int32_t world, int32_t rank, int64_t step,
+                         int64_t* g_out, int32_t* n_out, int64_t* offset_out, int32_t* b_total_out);
+int64_t gnn_steps_per_epoch(int64_t n_train, int32_t batch_size, int32_t world);
 gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_t id_host[128]);
 
 /* The epoch's seed order (§2.2; SPEC.md partition_seeds lines 107-115):

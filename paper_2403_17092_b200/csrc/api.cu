@@ -69,9 +69,16 @@ struct gnn_graph {
     int F = 0, stride = 0, C = 0;
     int64_t* row_ptr = nullptr;
     int32_t* col = nullptr;
-    float* X = nullptr;
+    float* X = nullptr;        // full table, or this process's shard (rows [row_begin, row_end))
     int32_t* y = nullptr;
+    int64_t row_begin = 0, row_end = 0;
+    // row-sharded features (config 4): peer shard pointers (device array) after gnn_shard_import
+    int nshards = 0;
+    int64_t rps = 0;
+    const float** shard_ptrs = nullptr;
+    std::vector<void*> ipc_opened;
     std::vector<void*> owned;
+    FeatRows rows() const { return FeatRows{X, nshards ? shard_ptrs : nullptr, rps}; }
 };
 
 namespace {
@@ -216,18 +223,19 @@ void enqueue_training(gnn_model* m) {
         Layer& ly = m->layers[li];
         HopBufs& b = m->hb[ly.blk];
         const int32_t* rows = rows_ptr(m, li);
-        const float* Hin = li == 0 ? g->X : m->layers[li - 1].H;
+        // layer 1 reads the feature table (local or row-sharded over peers); later layers H_{l-1}
+        const FeatRows Hrows = li == 0 ? g->rows() : FeatRows{m->layers[li - 1].H, nullptr, 0};
         const int kid = li == 0 ? GNN_K_AGG_L1 : GNN_K_AGG;
         if (m->sage) {
             // layer 1 of the neighbour sampler reads X rows directly by global neighbour id
             const bool direct = li == 0 && !m->shadow;
             K(m, kid, [&] {
-                launch_agg_sage(rows, Hin, ly.in_pad, direct ? nullptr : (li == 0 ? m->nodes : nullptr),
+                launch_agg_sage(rows, Hrows, ly.in_pad, direct ? nullptr : (li == 0 ? m->nodes : nullptr),
                                 li == 0 ? m->nodes : nullptr, b.rowptr, direct ? b.nbr : b.col, ly.A, s);
             });
         } else {
             K(m, kid, [&] {
-                launch_agg_gcn(rows, &m->st->n_dst[ly.blk], Hin, ly.in_pad, ly.k_pad, li == 0 ? m->nodes : nullptr,
+                launch_agg_gcn(rows, &m->st->n_dst[ly.blk], Hrows, ly.in_pad, ly.k_pad, li == 0 ? m->nodes : nullptr,
                                li == 0 ? m->nodes : nullptr, b.rowptr, b.col, b.trowptr, ly.A, s);
             });
         }
@@ -310,6 +318,13 @@ gnn_status build_graph(gnn_model* m, bool prof) {
     return GNN_OK;
 }
 
+// Checked before k_begin_step marks the seeds in the map (a step that starts must finish).
+gnn_status check_ready(gnn_model* m) {
+    if (m->g->nshards && !m->g->shard_ptrs)
+        return fail(GNN_ERR_STATE, "row-sharded features: call gnn_shard_import before training");
+    return GNN_OK;
+}
+
 gnn_status run_body(gnn_model* m) {
     if (m->cfg.use_graph && !m->profiling) {
         TRY(build_graph(m, false));
@@ -354,15 +369,23 @@ gnn_status set_device(int dev) {
 }
 
 // Step for this rank: global batch g = step*world + rank.
+// Batch -> rank rule of synchronous SGD (R8/R9; §2.2).
+void plan_step(int64_t n_train, int64_t B, int64_t world, int64_t rank, int64_t step, int64_t* g, int32_t* n,
+               int64_t* offset, int32_t* b_total) {
+    const int64_t nb = (n_train + B - 1) / B;
+    *g = step * world + rank;
+    *n = *g < nb ? (int32_t)std::min<int64_t>(B, n_train - *g * B) : 0;
+    *offset = *g * B;
+    const int64_t done = step * world * B;
+    *b_total = (int32_t)std::max<int64_t>(0, std::min<int64_t>(n_train - done, world * B));
+}
+
 gnn_status begin_step_from_perm(gnn_model* m, int64_t epoch, int64_t step) {
     TRY(ensure_perm(m, epoch));
-    const int64_t B = m->cfg.batch_size;
-    const int64_t g = step * m->world + m->rank;
-    const int64_t nb = num_batches(m);
-    const int32_t n = g < nb ? (int32_t)std::min<int64_t>(B, m->n_train - g * B) : 0;
-    const int64_t done = step * m->world * B;
-    const int32_t b_total = (int32_t)std::max<int64_t>(0, std::min<int64_t>(m->n_train - done, m->world * B));
-    launch_begin_step(m->st, n > 0 ? m->perm + g * B : m->perm, n, b_total, (uint32_t)epoch, (uint32_t)g,
+    int64_t g, offset;
+    int32_t n, b_total;
+    plan_step(m->n_train, m->cfg.batch_size, m->world, m->rank, step, &g, &n, &offset, &b_total);
+    launch_begin_step(m->st, n > 0 ? m->perm + offset : m->perm, n, b_total, (uint32_t)epoch, (uint32_t)g,
                       m->nodes, m->map, m->stream);
     return GNN_OK;
 }
@@ -374,9 +397,64 @@ extern "C" {
 const char* gnn_last_error(void) { return g_err.c_str(); }
 int32_t gnn_abi_version(void) { return GNN_ABI_VERSION; }
 
+static gnn_status graph_create(int64_t num_nodes, const int64_t* row_ptr_host, const int32_t* col_idx_host,
+                               int32_t feat_dim, int32_t feat_stride, const float* features_host,
+                               const int32_t* labels_host, int32_t num_classes, int32_t device, int32_t nshards,
+                               int32_t shard, gnn_graph** out);
+
 gnn_status gnn_graph_create(int64_t num_nodes, const int64_t* row_ptr_host, const int32_t* col_idx_host,
                             int32_t feat_dim, int32_t feat_stride, const float* features_host,
                             const int32_t* labels_host, int32_t num_classes, int32_t device, gnn_graph** out) {
+    return graph_create(num_nodes, row_ptr_host, col_idx_host, feat_dim, feat_stride, features_host, labels_host,
+                        num_classes, device, 1, 0, out);
+}
+
+gnn_status gnn_graph_create_sharded(int64_t num_nodes, const int64_t* row_ptr_host, const int32_t* col_idx_host,
+                                    int32_t feat_dim, int32_t feat_stride, int32_t nshards, int32_t shard,
+                                    const float* shard_features_host, const int32_t* labels_host,
+                                    int32_t num_classes, int32_t device, gnn_graph** out) {
+    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(GNN_ERR_PARAM, "bad shard index");
+    return graph_create(num_nodes, row_ptr_host, col_idx_host, feat_dim, feat_stride, shard_features_host,
+                        labels_host, num_classes, device, nshards, shard, out);
+}
+
+gnn_status gnn_shard_export(gnn_graph* g, uint8_t handle_out_host[64]) {
+    if (!g || !handle_out_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    TRY(set_device(g->dev));
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    CK(cudaIpcGetMemHandle(&h, g->X));
+    std::memcpy(handle_out_host, &h, 64);
+    return GNN_OK;
+}
+
+gnn_status gnn_shard_import(gnn_graph* g, const uint8_t* handles_host) {
+    if (!g || !handles_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    if (g->nshards < 1) return fail(GNN_ERR_STATE, "graph is not sharded");
+    TRY(set_device(g->dev));
+    std::vector<const float*> ptrs(g->nshards, nullptr);
+    const int mine = (int)(g->row_begin / g->rps);
+    for (int s = 0; s < g->nshards; ++s) {
+        if (s == mine) { ptrs[s] = g->X; continue; }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles_host + 64 * s, 64);
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        g->ipc_opened.push_back(p);
+        ptrs[s] = static_cast<const float*>(p);
+    }
+    if (!g->shard_ptrs) {
+        gnn_status st = dalloc(&g->shard_ptrs, g->nshards, g->owned);
+        if (st != GNN_OK) return st;
+    }
+    CK(cudaMemcpy(g->shard_ptrs, ptrs.data(), sizeof(float*) * g->nshards, cudaMemcpyHostToDevice));
+    return GNN_OK;
+}
+
+static gnn_status graph_create(int64_t num_nodes, const int64_t* row_ptr_host, const int32_t* col_idx_host,
+                               int32_t feat_dim, int32_t feat_stride, const float* features_host,
+                               const int32_t* labels_host, int32_t num_classes, int32_t device, int32_t nshards,
+                               int32_t shard, gnn_graph** out) {
     if (!out) return fail(GNN_ERR_PARAM, "out is NULL");
     *out = nullptr;
     if (num_nodes <= 0 || num_nodes >= INT32_MAX) return fail(GNN_ERR_PARAM, "num_nodes out of (0, 2^31-1)");
@@ -399,19 +477,25 @@ gnn_status gnn_graph_create(int64_t num_nodes, const int64_t* row_ptr_host, cons
     TRY(set_device(device));
     auto* g = new gnn_graph();
     g->dev = device; g->N = num_nodes; g->nnz = nnz; g->F = feat_dim; g->stride = feat_stride; g->C = num_classes;
+    g->rps = (num_nodes + nshards - 1) / nshards;      // uniform row blocks (config 4 sharding)
+    g->row_begin = std::min<int64_t>(num_nodes, (int64_t)shard * g->rps);
+    g->row_end = std::min<int64_t>(num_nodes, g->row_begin + g->rps);
+    g->nshards = nshards > 1 ? nshards : 0;
+    const int64_t local_rows = g->row_end - g->row_begin;
     auto cleanup = [&](gnn_status s) { for (void* p : g->owned) cudaFree(p); delete g; return s; };
     gnn_status s;
     if ((s = dalloc(&g->row_ptr, num_nodes + 1, g->owned)) != GNN_OK) return cleanup(s);
     if ((s = dalloc(&g->col, nnz, g->owned)) != GNN_OK) return cleanup(s);
-    if ((s = dalloc(&g->X, num_nodes * feat_stride, g->owned)) != GNN_OK) return cleanup(s);
+    if ((s = dalloc(&g->X, std::max<int64_t>(local_rows, 1) * feat_stride, g->owned)) != GNN_OK) return cleanup(s);
     if ((s = dalloc(&g->y, num_nodes, g->owned)) != GNN_OK) return cleanup(s);
     cudaError_t e = cudaMemcpy(g->row_ptr, row_ptr_host, sizeof(int64_t) * (num_nodes + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && nnz) e = cudaMemcpy(g->col, col_idx_host, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(g->X, features_host, sizeof(float) * num_nodes * feat_stride, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && local_rows)
+        e = cudaMemcpy(g->X, features_host, sizeof(float) * local_rows * feat_stride, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->y, labels_host, sizeof(int32_t) * num_nodes, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && feat_stride > feat_dim)   // padding columns are zero (DESIGN.md layout)
+    if (e == cudaSuccess && feat_stride > feat_dim && local_rows)   // padding columns are zero (DESIGN.md layout)
         e = cudaMemset2D(g->X + feat_dim, sizeof(float) * feat_stride, 0, sizeof(float) * (feat_stride - feat_dim),
-                         num_nodes);
+                         local_rows);
     if (e != cudaSuccess) return cleanup(fail(GNN_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e)));
     *out = g;
     return GNN_OK;
@@ -420,6 +504,7 @@ gnn_status gnn_graph_create(int64_t num_nodes, const int64_t* row_ptr_host, cons
 gnn_status gnn_graph_destroy(gnn_graph* g) {
     if (!g) return GNN_OK;
     cudaSetDevice(g->dev);
+    for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
     for (void* p : g->owned) cudaFree(p);
     delete g;
     return GNN_OK;
@@ -689,6 +774,21 @@ gnn_status gnn_comm_get_unique_id(uint8_t out_host[128]) {
     return GNN_OK;
 }
 
+gnn_status gnn_plan_step(int64_t n_train, int32_t batch_size, int32_t world, int32_t rank, int64_t step,
+                         int64_t* g_out, int32_t* n_out, int64_t* offset_out, int32_t* b_total_out) {
+    if (n_train < 0 || batch_size < 1 || world < 1 || rank < 0 || rank >= world || step < 0)
+        return fail(GNN_ERR_PARAM, "bad arguments");
+    if (!g_out || !n_out || !offset_out || !b_total_out) return fail(GNN_ERR_PARAM, "NULL output");
+    plan_step(n_train, batch_size, world, rank, step, g_out, n_out, offset_out, b_total_out);
+    return GNN_OK;
+}
+
+int64_t gnn_steps_per_epoch(int64_t n_train, int32_t batch_size, int32_t world) {
+    if (n_train < 0 || batch_size < 1 || world < 1) return -1;
+    const int64_t nb = (n_train + batch_size - 1) / batch_size;
+    return (nb + world - 1) / world;
+}
+
 gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_t id_host[128]) {
     if (!m || !id_host || world < 1 || rank < 0 || rank >= world) return fail(GNN_ERR_PARAM, "bad arguments");
     TRY(set_device(m->g->dev));
@@ -774,6 +874,7 @@ gnn_status gnn_train_minibatch(gnn_model* m, int64_t epoch, int64_t step, float*
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
     if (step < 0 || epoch < 0) return fail(GNN_ERR_PARAM, "negative epoch/step");
     TRY(set_device(m->g->dev));
+    TRY(check_ready(m));
     TRY(begin_step_from_perm(m, epoch, step));
     TRY(run_body(m));
     if (loss_out_host) {
@@ -789,6 +890,7 @@ gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t
     if (n_seeds < 0 || n_seeds > m->cfg.batch_size) return fail(GNN_ERR_SHAPE, "n_seeds must be 0..batch_size");
     if (b_total < n_seeds) return fail(GNN_ERR_PARAM, "b_total < n_seeds");
     TRY(set_device(m->g->dev));
+    TRY(check_ready(m));
     if (n_seeds)
         CK(cudaMemcpyAsync(m->seeds_in, seeds_host, sizeof(int32_t) * n_seeds, cudaMemcpyHostToDevice, m->stream));
     launch_begin_step(m->st, m->seeds_in, n_seeds, b_total, (uint32_t)epoch, (uint32_t)g, m->nodes, m->map, m->stream);
@@ -803,6 +905,7 @@ gnn_status gnn_train_epoch(gnn_model* m, int64_t epoch, gnn_epoch_stats* out_hos
     TRY(set_device(m->g->dev));
     const int64_t nb = num_batches(m);
     const int64_t steps = (nb + m->world - 1) / m->world;
+    TRY(check_ready(m));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));

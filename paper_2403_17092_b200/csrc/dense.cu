@@ -49,7 +49,7 @@ constexpr float4 kZero4 = {0.f, 0.f, 0.f, 0.f};
 // sum runs in CSR row order with plain fp32 adds, then a true division by the degree.
 template <int CPL>
 __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ rows_ptr,
-        const float* __restrict__ H, int in_pad, const int32_t* __restrict__ gmap,
+        FeatRows H, int in_pad, const int32_t* __restrict__ gmap,
         const int32_t* __restrict__ smap, const int32_t* __restrict__ rowptr,
         const int32_t* __restrict__ col, Split A) {
     const int n = *rows_ptr;
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             int q = 0;
             for (; q + 2 <= m; q += 2) {
                 const int r0 = __shfl_sync(kFull, myidx, q), r1 = __shfl_sync(kFull, myidx, q + 1);
-                const float4* p0 = reinterpret_cast<const float4*>(H + (int64_t)r0 * in_pad);
-                const float4* p1 = reinterpret_cast<const float4*>(H + (int64_t)r1 * in_pad);
+                const float4* p0 = reinterpret_cast<const float4*>(H.row(r0, in_pad));
+                const float4* p1 = reinterpret_cast<const float4*>(H.row(r1, in_pad));
                 float4 v0[CPL], v1[CPL];
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             }
             if (q < m) {
                 const int r0 = __shfl_sync(kFull, myidx, q);
-                const float4* p0 = reinterpret_cast<const float4*>(H + (int64_t)r0 * in_pad);
+                const float4* p0 = reinterpret_cast<const float4*>(H.row(r0, in_pad));
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
         }
         const int deg = end - beg;
         const int self = smap ? smap[i] : i;
-        const float4* ps = reinterpret_cast<const float4*>(H + (int64_t)self * in_pad);
+        const float4* ps = reinterpret_cast<const float4*>(H.row(self, in_pad));
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
 // d_in(i) = deg(i) + 1, d_out(c) = outdeg_blk(c) + [c < n_dst]  (R12).
 template <int CPL>
 __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ rows_ptr,
-        const int32_t* __restrict__ ndst_ptr, const float* __restrict__ H, int in_pad, int lda,
+        const int32_t* __restrict__ ndst_ptr, FeatRows H, int in_pad, int lda,
         const int32_t* __restrict__ gmap, const int32_t* __restrict__ smap,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
         const int32_t* __restrict__ trowptr, Split A) {
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
             for (int q = 0; q < m; ++q) {
                 const int r = __shfl_sync(kFull, myrow, q);
                 const float w = __shfl_sync(kFull, myw, q);
-                const float4* p = reinterpret_cast<const float4*>(H + (int64_t)r * in_pad);
+                const float4* p = reinterpret_cast<const float4*>(H.row(r, in_pad));
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
         const float dself = (float)(trowptr[i + 1] - trowptr[i] + 1);
         const float ws = 1.0f / sqrtf(din * dself);
         const int self = smap ? smap[i] : i;
-        const float4* ps = reinterpret_cast<const float4*>(H + (int64_t)self * in_pad);
+        const float4* ps = reinterpret_cast<const float4*>(H.row(self, in_pad));
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
@@ -355,13 +355,13 @@ int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
         default: KERNEL<8><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;           \
     }
 
-void launch_agg_sage(const int32_t* rows_ptr, const float* H, int in_pad, const int32_t* gmap,
+void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A,
                      cudaStream_t s) {
     GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A);
 }
 
-void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const float* H, int in_pad, int lda,
+void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,
                     const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
                     const int32_t* col, const int32_t* trowptr, Split A, cudaStream_t s) {
     GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_gcn, rows_ptr, ndst_ptr, H, in_pad, lda, gmap, smap, blk_rowptr,

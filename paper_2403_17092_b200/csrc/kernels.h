@@ -63,15 +63,29 @@ int sample_step_sites(int hops);
 // (GCN: Â H) columns.
 struct Split { __nv_bfloat16* hi; __nv_bfloat16* lo; };
 
+// Rows of an aggregation input: a local buffer (shards == nullptr), or the feature table
+// row-sharded over peers (config 4): row r lives in shard r / rps at local row r % rps; the
+// shard pointers are CUDA-IPC mappings of the peers' HBM (NVLink peer loads).
+struct FeatRows {
+    const float* base;
+    const float* const* shards;
+    int64_t rps;
+    __device__ __forceinline__ const float* row(int r, int ld) const {
+        if (!shards) return base + (int64_t)r * ld;
+        const int s = (int)(r / rps);
+        return shards[s] + (int64_t)(r - s * rps) * ld;
+    }
+};
+
 // SAGE-mean aggregation into A = [H_self | mean] for rows i < *rows_ptr.  Neighbour row of
 // source c is gmap ? gmap[c] : c, self row smap ? smap[i] : i (layer 1 reads X by global id:
 // the fused feature gather).
-void launch_agg_sage(const int32_t* rows_ptr, const float* H, int in_pad, const int32_t* gmap,
+void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A,
                      cudaStream_t s);
 // GCN aggregation A = Â H (self loop included) for rows i < *rows_ptr of a block with
 // *ndst_ptr destinations; d_out from the transposed row pointer.  col must be local ids.
-void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, const float* H, int in_pad, int lda,
+void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,
                     const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
                     const int32_t* col, const int32_t* trowptr, Split A, cudaStream_t s);
 // grads[r*out + c] = Σ_z part[z][rpad(r)*n_pad + c]   (fixed z order; unpads rows/cols)

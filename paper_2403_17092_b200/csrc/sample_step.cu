@@ -114,6 +114,28 @@ __device__ int chunk_scan(Smem& sm, int n, F f, PUT put, unsigned long long* sta
     return blockIdx.x == gridDim.x - 1 ? sm.total : -1;
 }
 
+constexpr int kWarpSort = 1024;                   // ints per warp slice of shared memory
+constexpr int kBlockSort = kWarps * kWarpSort;    // 32768 ints = 128 KB
+
+// In-place ascending bitonic sort of s[0:n2) (n2 a power of two) by `nthr` cooperating
+// threads (thread index t), `sync` separating the stages.
+template <class SYNC>
+__device__ __forceinline__ void bitonic_sort(int* s, int n2, int t, int nthr, SYNC sync) {
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = t; i < n2; i += nthr) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const int a = s[i], b = s[ixj];
+                    const bool asc = (i & k) == 0;
+                    if ((a > b) == asc) { s[i] = b; s[ixj] = a; }
+                }
+            }
+            sync();
+        }
+    }
+}
+
 __device__ __forceinline__ int min_deg(const int64_t* row_ptr, int v, int k) {
     const int64_t d = __ldg(row_ptr + v + 1) - __ldg(row_ptr + v);
     return d < k ? (int)d : k;
@@ -306,7 +328,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
             for (int e = H.rowptr[i] + lane; e < H.rowptr[i + 1]; e += 32) H.tdst[atomicAdd(&H.tcursor[H.col[e]], 1)] = i;
     }
     grid_sync(P.bar);
-    // rank-sort every transposed row (fixed summation order); reset map
+    // sort every transposed row ascending (fixed summation order):
+    // <= 32 entries: shuffle rank sort; <= kWarpSort: bitonic sort in the warp's shared slice;
+    // longer rows (hubs): the whole block sorts them in shared memory, one at a time.
+    extern __shared__ int dyn[];
+    int* wbuf = dyn + wib * kWarpSort;
     for (int h = 0; h <= P.hops; ++h) {
         const HopIO& H = P.hop[h];
         if (!H.tcount) continue;
@@ -319,8 +345,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
                 int rank = 0;
                 for (int q = 0; q < len; ++q) rank += (__shfl_sync(kFull, x, q) < x) ? 1 : 0;
                 if (lane < len) H.tdst_s[b0 + rank] = x;
-            } else {
-                for (int a = lane; a < len; a += 32) {
+            } else if (len <= kWarpSort) {
+                int n2 = 64;
+                while (n2 < len) n2 <<= 1;
+                for (int a = lane; a < n2; a += 32) wbuf[a] = a < len ? H.tdst[b0 + a] : INT_MAX;
+                __syncwarp();
+                bitonic_sort(wbuf, n2, lane, 32, [] { __syncwarp(); });
+                for (int a = lane; a < len; a += 32) H.tdst_s[b0 + a] = wbuf[a];
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        for (int u = blockIdx.x; u < ns; u += G) {       // long rows: block-wide sort
+            const int b0 = H.trowptr[u];
+            const int len = H.trowptr[u + 1] - b0;
+            if (len <= kWarpSort) continue;
+            if (len <= kBlockSort) {
+                int n2 = 2 * kWarpSort;
+                while (n2 < len) n2 <<= 1;
+                for (int a = threadIdx.x; a < n2; a += kThreads) dyn[a] = a < len ? H.tdst[b0 + a] : INT_MAX;
+                __syncthreads();
+                bitonic_sort(dyn, n2, threadIdx.x, kThreads, [] { __syncthreads(); });
+                for (int a = threadIdx.x; a < len; a += kThreads) H.tdst_s[b0 + a] = dyn[a];
+                __syncthreads();
+            } else {                                       // beyond shared memory: rank counting
+                for (int a = threadIdx.x; a < len; a += kThreads) {
                     const int x = H.tdst[b0 + a];
                     int rank = 0;
                     for (int b = 0; b < len; ++b) rank += (H.tdst[b0 + b] < x) ? 1 : 0;
@@ -334,13 +383,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
 
 }  // namespace
 
+constexpr int kSortSmem = kBlockSort * (int)sizeof(int);
+
 int sample_step_grid() {
     static int grid = 0;
     if (!grid) {
         int per_sm = 0, dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_step, kThreads, 0);
+        cudaFuncSetAttribute(k_sample_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_step, kThreads, kSortSmem);
         grid = std::max(1, std::min(per_sm, 1)) * std::max(sms, 1);
     }
     return grid;
@@ -350,7 +402,7 @@ int sample_step_grid() {
 int sample_step_sites(int hops) { return 2 * hops + 1 + (hops + 1); }
 
 void launch_sample_step(const SampleParams& p, cudaStream_t s) {
-    k_sample_step<<<sample_step_grid(), kThreads, 0, s>>>(p);
+    k_sample_step<<<sample_step_grid(), kThreads, kSortSmem, s>>>(p);
 }
 
 }  // namespace gs

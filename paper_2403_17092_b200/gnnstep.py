@@ -304,3 +304,70 @@ def _phases(self, n=32):
 
 
 Model.sampling_phases_us = _phases
+
+
+def plan_step(n_train: int, batch_size: int, world: int, rank: int, step: int):
+    """gnn_plan_step: (g, n, offset, b_total) of `rank` at `step` (host only)."""
+    L = lib()
+    L.gnn_plan_step.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.gnn_plan_step.restype = C.c_int32
+    g, off = C.c_int64(), C.c_int64()
+    n, bt = C.c_int32(), C.c_int32()
+    _check(L.gnn_plan_step(n_train, batch_size, world, rank, step, C.byref(g), C.byref(n), C.byref(off),
+                           C.byref(bt)))
+    return g.value, n.value, off.value, bt.value
+
+
+def steps_per_epoch(n_train: int, batch_size: int, world: int) -> int:
+    L = lib()
+    L.gnn_steps_per_epoch.argtypes = [C.c_int64, C.c_int32, C.c_int32]
+    L.gnn_steps_per_epoch.restype = C.c_int64
+    return L.gnn_steps_per_epoch(n_train, batch_size, world)
+
+
+class ShardedGraph(Graph):
+    """gnn_graph_create_sharded: full CSR + labels, this process's block of feature rows."""
+
+    def __init__(self, row_ptr, col, X_shard, y, num_classes, nshards, shard, feat_dim=None, device=0):
+        row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        col = np.ascontiguousarray(col, dtype=np.int32)
+        X_shard = np.ascontiguousarray(X_shard, dtype=np.float32)
+        y = np.ascontiguousarray(y, dtype=np.int32)
+        n = row_ptr.shape[0] - 1
+        stride = X_shard.shape[1]
+        self.num_nodes, self.num_classes, self.device = n, num_classes, device
+        self.feat_dim = stride if feat_dim is None else feat_dim
+        self.nshards, self.shard = nshards, shard
+        L = lib()
+        L.gnn_graph_create_sharded.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                               C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                                               C.c_int32, C.c_void_p]
+        L.gnn_graph_create_sharded.restype = C.c_int32
+        h = C.c_void_p()
+        _check(L.gnn_graph_create_sharded(n, _ptr(row_ptr), _ptr(col), self.feat_dim, stride, nshards, shard,
+                                          _ptr(X_shard), _ptr(y), num_classes, device, C.byref(h)))
+        self.h = h
+
+    def export_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        L = lib()
+        L.gnn_shard_export.argtypes = [C.c_void_p, C.c_void_p]
+        L.gnn_shard_export.restype = C.c_int32
+        _check(L.gnn_shard_export(self.h, buf))
+        return bytes(buf)
+
+    def import_handles(self, handles):
+        blob = b"".join(handles)
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        L = lib()
+        L.gnn_shard_import.argtypes = [C.c_void_p, C.c_void_p]
+        L.gnn_shard_import.restype = C.c_int32
+        _check(L.gnn_shard_import(self.h, buf))
+
+
+def shard_rows(num_nodes: int, nshards: int, shard: int):
+    """[begin, end) rows of block `shard` (the library's uniform row blocks)."""
+    rps = (num_nodes + nshards - 1) // nshards
+    b = min(num_nodes, shard * rps)
+    return b, min(num_nodes, b + rps)
