@@ -96,7 +96,7 @@ struct Layer {
     int64_t m_cap = 0;     // max rows of this layer's output
     int splits = 1;
     int64_t rows_alloc = 0;  // operand-plane rows (m_cap rounded to the 128-row GEMM tile)
-    Split A{}, dPre{}, Wkn{}, Wnk{};   // bf16 split planes (GEMM operands)
+    Split A{}, dPre{}, Wkn{};   // bf16 split planes (GEMM operands); W as [K_pad x N_pad]
     float *H = nullptr, *dA = nullptr, *wpart = nullptr;
     TcGemmMaps map_fwd{}, map_dgrad{}, map_wgrad{};
 };
@@ -198,7 +198,8 @@ PackAll pack_desc(gnn_model* m) {
     p.sage = m->sage;
     for (int li = 0; li < m->L; ++li) {
         const Layer& ly = m->layers[li];
-        p.l[li] = PackLayer{m->params + ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, ly.k_pad, ly.n_pad, ly.Wkn, ly.Wnk};
+        p.l[li] = PackLayer{ly.poff, ly.rows, ly.out, ly.in, ly.in_pad, ly.k_pad, ly.n_pad, ly.Wkn, ly.wpart,
+                            ly.splits, (int64_t)ly.k_pad * ly.n_pad};
     }
     return p;
 }
@@ -241,7 +242,7 @@ void enqueue_training(gnn_model* m) {
         }
         // Pre = A W (+ReLU) -> H (fp32)
         K(m, GNN_K_GEMM_FWD, [&] {
-            launch_gemm_tc(0, m->bf16x3, ly.map_fwd, rows, 0, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, ly.n_pad,
+            launch_gemm_tc(2, m->bf16x3, ly.map_fwd, rows, 0, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, ly.n_pad,
                            ly.n_pad, li < L - 1, 1, 0, s);
         });
     }
@@ -257,8 +258,6 @@ void enqueue_training(gnn_model* m) {
         K(m, GNN_K_GEMM_WGRAD, [&] {
             launch_gemm_tc(1, m->bf16x3, ly.map_wgrad, rows, ly.k_pad, ly.k_pad, ly.n_pad, 0, ly.wpart, ly.n_pad,
                            ly.n_pad, false, ly.splits, stride, s);
-            launch_wgrad_reduce(ly.wpart, ly.splits, stride, ly.rows, ly.out, ly.in, ly.in_pad, m->sage,
-                                ly.n_pad, m->grads + ly.poff, s);
         });
         if (li == 0) break;
         // dA = dPre W^T (fp32)
@@ -273,13 +272,14 @@ void enqueue_training(gnn_model* m) {
                             prev.H, prev.dPre, s);
         });
     }
+    // ---- split-K partials of every layer -> flat gradient (fixed order)
+    K(m, GNN_K_GEMM_WGRAD, [&] { launch_wgrad_reduce_all(pack_desc(m), m->grads, s); });
     // ---- exchange + update
     if (m->world > 1)
         K(m, GNN_K_ALLREDUCE, [&] {
             ncclAllReduce(m->grads, m->grads, (size_t)m->pcount, ncclFloat, ncclSum, m->comm, s);
         });
-    K(m, GNN_K_SGD, [&] { launch_sgd(m->params, m->grads, m->pcount, m->cfg.lr, s); });
-    K(m, GNN_K_OTHER, [&] { launch_pack_all(pack_desc(m), s); });
+    K(m, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, s); });
 }
 
 void enqueue_body(gnn_model* m) {
@@ -647,18 +647,17 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         if ((s = split(ly.A, ly.rows_alloc * ly.k_pad)) != GNN_OK) return cleanup(s);
         if ((s = split(ly.dPre, ly.rows_alloc * ly.n_pad)) != GNN_OK) return cleanup(s);
         if ((s = split(ly.Wkn, (int64_t)ly.k_pad * ly.n_pad)) != GNN_OK) return cleanup(s);
-        if ((s = split(ly.Wnk, (int64_t)ly.k_pad * ly.n_pad)) != GNN_OK) return cleanup(s);
         AL(ly.H, ly.m_cap * ly.n_pad);
         if (li > 0) AL(ly.dA, ly.m_cap * ly.k_pad);
         AL(ly.wpart, (int64_t)ly.splits * ly.k_pad * ly.n_pad);
         // TMA descriptors (128B swizzle) of this layer's three GEMMs
         auto lo_or_hi = [](const Split& sp) { return sp.lo ? (const void*)sp.lo : (const void*)sp.hi; };
         bool ok = true;
-        const int bn_f = tc_tile_n(ly.n_pad), bn_d = tc_tile_n(ly.k_pad);
+        const int bn_d = tc_tile_n(ly.k_pad);
         ok &= make_tmap_bf16(&ly.map_fwd.a_hi, ly.A.hi, ly.rows_alloc, ly.k_pad, 128);
         ok &= make_tmap_bf16(&ly.map_fwd.a_lo, lo_or_hi(ly.A), ly.rows_alloc, ly.k_pad, 128);
-        ok &= make_tmap_bf16(&ly.map_fwd.b_hi, ly.Wnk.hi, ly.n_pad, ly.k_pad, bn_f);
-        ok &= make_tmap_bf16(&ly.map_fwd.b_lo, lo_or_hi(ly.Wnk), ly.n_pad, ly.k_pad, bn_f);
+        ok &= make_tmap_bf16(&ly.map_fwd.b_hi, ly.Wkn.hi, ly.k_pad, ly.n_pad, 64);     // MN-major B
+        ok &= make_tmap_bf16(&ly.map_fwd.b_lo, lo_or_hi(ly.Wkn), ly.k_pad, ly.n_pad, 64);
         ok &= make_tmap_bf16(&ly.map_dgrad.a_hi, ly.dPre.hi, ly.rows_alloc, ly.n_pad, 128);
         ok &= make_tmap_bf16(&ly.map_dgrad.a_lo, lo_or_hi(ly.dPre), ly.rows_alloc, ly.n_pad, 128);
         ok &= make_tmap_bf16(&ly.map_dgrad.b_hi, ly.Wkn.hi, ly.k_pad, ly.n_pad, bn_d);
@@ -680,7 +679,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         const float bound = std::sqrt(6.0f / (float)(ly.in + ly.out));
         launch_init_params(m->params + ly.poff, ly.pcnt, bound, c.init_seed, (uint32_t)li, m->stream);
     }
-    launch_pack_all(pack_desc(m), m->stream);
+    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, m->stream);
     CK(cudaMemsetAsync(m->grads, 0, sizeof(float) * m->pcount, m->stream));
     CK(cudaStreamSynchronize(m->stream));
     CK(cudaGetLastError());
@@ -760,7 +759,7 @@ gnn_status gnn_set_params(gnn_model* m, const float* in_host, int64_t n) {
     if (n != m->pcount) return fail(GNN_ERR_SHAPE, "n != param_count");
     TRY(set_device(m->g->dev));
     CK(cudaMemcpyAsync(m->params, in_host, sizeof(float) * n, cudaMemcpyHostToDevice, m->stream));
-    launch_pack_all(pack_desc(m), m->stream);
+    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, m->stream);
     CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }

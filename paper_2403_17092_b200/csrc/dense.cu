@@ -238,29 +238,28 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
 }
 
 // ------------------------------------------------------------------ weights, reduce, SGD
-__global__ void k_wgrad_reduce(const float* __restrict__ part, int splits, int64_t split_stride,
-                               int rows, int out, int in, int in_pad, bool sage, int n_pad,
-                               float* __restrict__ grads) {
-    const int64_t total = (int64_t)rows * out;
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
-         f += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(f / out), c = (int)(f % out);
-        const int rp = sage ? (r / in) * in_pad + (r % in) : r;
-        float s = 0.f;
-        for (int z = 0; z < splits; ++z) s += part[z * split_stride + (int64_t)rp * n_pad + c];
-        grads[f] = s;
+// dW of every layer in one launch: grads[off_l + r*out + c] = Σ_z part_l[z][rpad(r)*n_pad + c]
+// (split order fixed: deterministic).
+__global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int l = 0; l < P.n; ++l) {
+        const PackLayer& L = P.l[l];
+        const int64_t total = (int64_t)L.rows * L.out;
+        for (int64_t f = tid; f < total; f += nth) {
+            const int r = (int)(f / L.out), c = (int)(f % L.out);
+            const int rp = P.sage ? (r / L.in) * L.in_pad + (r % L.in) : r;
+            float s = 0.f;
+            for (int z = 0; z < L.splits; ++z) s += L.part[z * L.split_stride + (int64_t)rp * L.n_pad + c];
+            grads[L.poff + f] = s;
+        }
     }
 }
 
-__device__ __forceinline__ float packed_value(const PackLayer& L, bool sage, int rp, int c) {
-    int r = -1;
-    if (sage) { const int half = rp / L.in_pad, j = rp % L.in_pad; if (j < L.in && half < 2) r = half * L.in + j; }
-    else if (rp < L.in) r = rp;
-    return (r >= 0 && c < L.out) ? L.W[(int64_t)r * L.out + c] : 0.f;
-}
-
-// All layers in one launch; both layouts written in their own (coalesced) order.
-__global__ void k_pack_all(PackAll P) {
+// SGD (W <- W - lr G, §2.2) fused with the repack of the GEMM weight planes
+// W [K_pad x N_pad] (coalesced in that order; padding entries stay the zeros written at
+// creation).  Each parameter is visited exactly once.  grads == nullptr: pack only.
+__global__ void k_sgd_pack(PackAll P, float* __restrict__ params, const float* __restrict__ grads, float lr) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int l = 0; l < P.n; ++l) {
@@ -268,11 +267,14 @@ __global__ void k_pack_all(PackAll P) {
         const int64_t total = (int64_t)L.k_pad * L.n_pad;
         for (int64_t f = tid; f < total; f += nth) {
             const int rp = (int)(f / L.n_pad), c = (int)(f % L.n_pad);
-            store_split1(L.Wkn, f, packed_value(L, P.sage, rp, c));
-        }
-        for (int64_t f = tid; f < total; f += nth) {
-            const int c = (int)(f / L.k_pad), rp = (int)(f % L.k_pad);
-            store_split1(L.Wnk, f, packed_value(L, P.sage, rp, c));
+            int r = -1;
+            if (P.sage) { const int half = rp / L.in_pad, j = rp % L.in_pad; if (j < L.in && half < 2) r = half * L.in + j; }
+            else if (rp < L.in) r = rp;
+            if (r < 0 || c >= L.out) continue;
+            const int64_t idx = L.poff + (int64_t)r * L.out + c;
+            float w = params[idx];
+            if (grads) { w = w - lr * grads[idx]; params[idx] = w; }
+            store_split1(L.Wkn, f, w);
         }
     }
 }
@@ -323,12 +325,6 @@ __global__ void __launch_bounds__(256) k_ce(StepState* st, const float* __restri
         st->loss = tot * inv_bt;
         *done = 0u;
     }
-}
-
-__global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = p[i] - lr * g[i];
 }
 
 __global__ void k_init(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer) {
@@ -387,25 +383,17 @@ void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, 
     else spmm_bwd<false>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
 }
 
-void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, int rows, int out, int in,
-                         int in_pad, bool sage, int n_pad, float* grads, cudaStream_t s) {
-    const int64_t total = (int64_t)rows * out;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-    k_wgrad_reduce<<<blocks, 256, 0, s>>>(part, splits, split_stride, rows, out, in, in_pad, sage, n_pad, grads);
+void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s) {
+    k_wgrad_reduce_all<<<148 * 4, 256, 0, s>>>(p, grads);
 }
 
-void launch_pack_all(const PackAll& p, cudaStream_t s) {
-    k_pack_all<<<148 * 2, 256, 0, s>>>(p);
+void launch_sgd_pack(const PackAll& p, float* params, const float* grads, float lr, cudaStream_t s) {
+    k_sgd_pack<<<148 * 2, 256, 0, s>>>(p, params, grads, lr);
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,
                Split dZ, cudaStream_t s) {
     k_ce<<<128, 256, 0, s>>>(st, Z, ldz, C, labels, nodes, dZ, st->row_loss, &st->ce_done);
-}
-
-void launch_sgd(float* params, const float* grads, int64_t n, float lr, cudaStream_t s) {
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
-    k_sgd<<<blocks, 256, 0, s>>>(params, grads, n, lr);
 }
 
 void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer, cudaStream_t s) {

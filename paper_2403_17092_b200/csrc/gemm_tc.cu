@@ -122,7 +122,7 @@ struct TileInfo { int tm, tn, z, kb0, nkb; };
 template <int MODE>
 __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t, int M) {
     TileInfo ti;
-    if (MODE == 0) {
+    if (MODE != 1) {
         ti.tm = t / a.n_tiles;
         ti.tn = t % a.n_tiles;
         ti.z = 0;
@@ -143,13 +143,15 @@ __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t, int M) {
     return ti;
 }
 
-// MODE 0 = fwd/dgrad (A, B K-major), MODE 1 = wgrad (A, B MN-major, split z).
+// MODE 0 = dgrad (A, B K-major), MODE 1 = wgrad (A, B MN-major, split z), MODE 2 = fwd (A K-major,
+// B MN-major: W read as stored, [K x N]).
 template <int BN, int STAGES, int TERMS, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
           const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo, GemmArgs args) {
     using Cfg = TileCfg<BN>;
-    constexpr bool MN = MODE == 1;
+    constexpr bool A_MN = MODE == 1;          // wgrad: A^T read from row-major A
+    constexpr bool B_MN = MODE >= 1;          // wgrad (dPre), fwd mode 2 (W [K x N])
     constexpr int kAPlanes = TERMS == 3 ? 2 : 1;
     constexpr int kStageBytes = kAPlanes * (Cfg::kAStage + Cfg::kBStage);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -159,7 +161,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int M = *args.m_ptr;
-    const int ntiles = MODE == 0 ? ((M + kBM - 1) / kBM) * args.n_tiles
+    const int ntiles = MODE != 1 ? ((M + kBM - 1) / kBM) * args.n_tiles
                                  : ((args.m_static + kBM - 1) / kBM) * args.n_tiles * args.splits;
     if ((int)blockIdx.x >= ntiles) return;
 
@@ -194,21 +196,22 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                     uint8_t* b_hi = st + Cfg::kAStage;
                     uint8_t* a_lo = st + Cfg::kAStage + Cfg::kBStage;
                     uint8_t* b_lo = a_lo + Cfg::kAStage;
-                    mbar_expect_tx(&full_bar[s], kAPlanes * (Cfg::kAStage + (MN ? Cfg::kBBytesMN : Cfg::kBBytesK)));
+                    mbar_expect_tx(&full_bar[s], kAPlanes * (Cfg::kAStage + (B_MN ? Cfg::kBBytesMN : Cfg::kBBytesK)));
                     const int k0 = (ti.kb0 + kb) * kBK;
-                    if (MODE == 0) {
+                    if (!A_MN) {          // K-major: box {64 (k), 128 rows}
                         tma_load_2d(a_hi, &mA_hi, &full_bar[s], k0, tile_m);
-                        tma_load_2d(b_hi, &mB_hi, &full_bar[s], k0, tile_n);
-                        if (TERMS == 3) {
-                            tma_load_2d(a_lo, &mA_lo, &full_bar[s], k0, tile_m);
-                            tma_load_2d(b_lo, &mB_lo, &full_bar[s], k0, tile_n);
-                        }
-                    } else {
+                        if (TERMS == 3) tma_load_2d(a_lo, &mA_lo, &full_bar[s], k0, tile_m);
+                    } else {              // MN-major: boxes {64 (m), 64 (k rows)}, 8 KB apart
 #pragma unroll
                         for (int j = 0; j < kBM / 64; ++j) {
                             tma_load_2d(a_hi + j * 8192, &mA_hi, &full_bar[s], tile_m + 64 * j, k0);
                             if (TERMS == 3) tma_load_2d(a_lo + j * 8192, &mA_lo, &full_bar[s], tile_m + 64 * j, k0);
                         }
+                    }
+                    if (!B_MN) {
+                        tma_load_2d(b_hi, &mB_hi, &full_bar[s], k0, tile_n);
+                        if (TERMS == 3) tma_load_2d(b_lo, &mB_lo, &full_bar[s], k0, tile_n);
+                    } else {
 #pragma unroll
                         for (int j = 0; j < (BN + 63) / 64; ++j) {
                             tma_load_2d(b_hi + j * 8192, &mB_hi, &full_bar[s], tile_n + 64 * j, k0);
@@ -221,7 +224,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     } else if (warp == 1) {
         // ================= MMA issuer (one thread)
         if (lane == 0) {
-            constexpr uint32_t id = idesc<BN, MN, MN>();
+            constexpr uint32_t id = idesc<BN, A_MN, B_MN>();
             int it = 0, j = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 const TileInfo ti = tile_info<MODE>(args, t, M);
@@ -241,12 +244,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         // K-major: +32 B per 16-element k step inside the 128 B swizzle row;
                         // MN-major: +16 rows x 128 B per k step.
-                        const uint32_t off = MN ? kk * 2048 : kk * 32;
-                        const uint32_t lbo = MN ? 8192 : 16, sbo = 1024;
-                        const uint64_t dah = sdesc(a_hi + off, lbo, sbo), dbh = sdesc(b_hi + off, lbo, sbo);
+                        const uint32_t oa = A_MN ? kk * 2048 : kk * 32, ob = B_MN ? kk * 2048 : kk * 32;
+                        const uint32_t la = A_MN ? 8192 : 16, lb = B_MN ? 8192 : 16, sbo = 1024;
+                        const uint64_t dah = sdesc(a_hi + oa, la, sbo), dbh = sdesc(b_hi + ob, lb, sbo);
                         tc_mma(d, dah, dbh, id, (kb > 0 || kk > 0) ? 1u : 0u);
                         if (TERMS == 3) {
-                            const uint64_t dal = sdesc(a_lo + off, lbo, sbo), dbl = sdesc(b_lo + off, lbo, sbo);
+                            const uint64_t dal = sdesc(a_lo + oa, la, sbo), dbl = sdesc(b_lo + ob, lb, sbo);
                             tc_mma(d, dah, dbl, id, 1u);
                             tc_mma(d, dal, dbh, id, 1u);
                         }
@@ -412,10 +415,11 @@ cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const 
     a.relu = relu ? 1 : 0;
     a.split_stride = split_stride;
     int tiles_cap;
-    if (mode == 0) tiles_cap = a.m_tiles_cap * a.n_tiles;
+    if (mode != 1) tiles_cap = a.m_tiles_cap * a.n_tiles;
     else tiles_cap = ((m_static + kBM - 1) / kBM) * a.n_tiles * splits;
     const int grid = std::max(1, std::min(kSMs, tiles_cap));
     if (mode == 0) return bf16x3 ? dispatch_bn<3, 0>(bn, grid, maps, a, s) : dispatch_bn<1, 0>(bn, grid, maps, a, s);
+    if (mode == 2) return bf16x3 ? dispatch_bn<3, 2>(bn, grid, maps, a, s) : dispatch_bn<1, 2>(bn, grid, maps, a, s);
     return bf16x3 ? dispatch_bn<3, 1>(bn, grid, maps, a, s) : dispatch_bn<1, 1>(bn, grid, maps, a, s);
 }
 

@@ -88,14 +88,21 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
 void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,
                     const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
                     const int32_t* col, const int32_t* trowptr, Split A, cudaStream_t s);
-// grads[r*out + c] = Σ_z part[z][rpad(r)*n_pad + c]   (fixed z order; unpads rows/cols)
-void launch_wgrad_reduce(const float* part, int splits, int64_t split_stride, int rows, int out,
-                         int in, int in_pad, bool sage, int n_pad, float* grads, cudaStream_t s);
-// W [K_pad x N_pad] and W^T [N_pad x K_pad] split planes from flat fp32 W (rows x out), all
-// layers in one launch.
-struct PackLayer { const float* W; int rows, out, in, in_pad, k_pad, n_pad; Split Wkn, Wnk; };
+// Per layer: flat fp32 W (rows x out, at params/grads offset poff), its GEMM planes
+// W [K_pad x N_pad] (bf16 split), and the wgrad split-K partials.
+struct PackLayer {
+    int64_t poff;
+    int rows, out, in, in_pad, k_pad, n_pad;
+    Split Wkn;
+    const float* part;
+    int splits;
+    int64_t split_stride;
+};
 struct PackAll { PackLayer l[kMaxHops]; int n; bool sage; };
-void launch_pack_all(const PackAll& p, cudaStream_t s);
+// grads[poff + r*out + c] = Σ_z part[z][rpad(r)*n_pad + c] for every layer, fixed z order.
+void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s);
+// W <- W - lr*G (grads may be nullptr: pack only) and the bf16 planes of W, all layers.
+void launch_sgd_pack(const PackAll& p, float* params, const float* grads, float lr, cudaStream_t s);
 // Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total
 // written as split planes [rows x ldz] (+ zero tail rows).
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels,
@@ -107,7 +114,6 @@ void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* lab
 void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, const float* dA,
                      int in_pad, const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
                      const float* H_prev, Split dPre_prev, cudaStream_t s);
-void launch_sgd(float* params, const float* grads, int64_t n, float lr, cudaStream_t s);
 void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer,
                         cudaStream_t s);
 
@@ -117,8 +123,10 @@ struct TcGemmMaps { CUtensorMap a_hi, a_lo, b_hi, b_lo; };
 bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
 // N tile the GEMM uses for an output width n_pad (TMA box rows of a K-major B operand).
 int tc_tile_n(int n_pad);
-// mode 0 (fwd / dgrad): C[M x n_store] = A[M x k_pad] B^T (B given as [n_pad x k_pad]), M = *m_ptr
-//   (rows >= M not stored), optional ReLU.  A, B K-major; maps: A box rows 128, B box rows tc_tile_n.
+// mode 0 (dgrad): C[M x n_store] = A[M x k_pad] B^T (B given as [n_pad x k_pad]), M = *m_ptr
+//   (rows >= M not stored).  A, B K-major; maps: A box rows 128, B box rows tc_tile_n.
+// mode 2 (fwd): as mode 0 but B given as [k_pad x n_pad] (MN-major, W as stored), box rows 64;
+//   optional ReLU.
 // mode 1 (wgrad): C_z[m_static x n_pad] = Σ_{m in split z} A[m, :]^T B[m, :], reduction length
 //   *m_ptr split into `splits` ranges of 64-row blocks; A, B MN-major, maps with box rows 64.
 // bf16x3: 3-term split product (fp32 parity); else 1 term (bf16 GEMM variant).

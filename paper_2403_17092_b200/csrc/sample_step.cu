@@ -114,8 +114,9 @@ __device__ int chunk_scan(Smem& sm, int n, F f, PUT put, unsigned long long* sta
     return blockIdx.x == gridDim.x - 1 ? sm.total : -1;
 }
 
-constexpr int kWarpSort = 1024;                   // ints per warp slice of shared memory
-constexpr int kBlockSort = kWarps * kWarpSort;    // 32768 ints = 128 KB
+constexpr int kWarpSort = 256;                    // ints per warp slice of shared memory
+constexpr int kBlockSort = kWarps * kWarpSort;    // 8192 ints = 32 KB (keeps most of L1 as cache)
+constexpr int kMaxLong = 256;                     // hub rows queued per block and block
 
 // In-place ascending bitonic sort of s[0:n2) (n2 a power of two) by `nthr` cooperating
 // threads (thread index t), `sync` separating the stages.
@@ -332,14 +333,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
     // <= 32 entries: shuffle rank sort; <= kWarpSort: bitonic sort in the warp's shared slice;
     // longer rows (hubs): the whole block sorts them in shared memory, one at a time.
     extern __shared__ int dyn[];
+    __shared__ int s_long[kMaxLong];
+    __shared__ int s_nlong;
     int* wbuf = dyn + wib * kWarpSort;
     for (int h = 0; h <= P.hops; ++h) {
         const HopIO& H = P.hop[h];
         if (!H.tcount) continue;
         const int ns = st->n_src[h];
+        if (threadIdx.x == 0) s_nlong = 0;
+        __syncthreads();
         for (int u = blockIdx.x * kWarps + wib; u < ns; u += G * kWarps) {
             const int b0 = H.trowptr[u];
             const int len = H.trowptr[u + 1] - b0;
+            if (len > kWarpSort) {                   // hub row: queue it for the block-wide sort
+                int slot = 0;
+                if (lane == 0) slot = atomicAdd(&s_nlong, 1);
+                slot = __shfl_sync(kFull, slot, 0);
+                if (slot < kMaxLong) { if (lane == 0) s_long[slot] = u; continue; }
+                for (int a = lane; a < len; a += 32) {   // queue full: rank counting in the warp
+                    const int x = H.tdst[b0 + a];
+                    int rank = 0;
+                    for (int b = 0; b < len; ++b) rank += (H.tdst[b0 + b] < x) ? 1 : 0;
+                    H.tdst_s[b0 + rank] = x;
+                }
+                continue;
+            }
             if (len <= 32) {
                 const int x = lane < len ? H.tdst[b0 + lane] : INT_MAX;
                 int rank = 0;
@@ -356,10 +374,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
             }
         }
         __syncthreads();
-        for (int u = blockIdx.x; u < ns; u += G) {       // long rows: block-wide sort
+        const int nlong = min(s_nlong, kMaxLong);
+        for (int q = 0; q < nlong; ++q) {                // this block's hub rows: block-wide sort
+            const int u = s_long[q];
             const int b0 = H.trowptr[u];
             const int len = H.trowptr[u + 1] - b0;
-            if (len <= kWarpSort) continue;
             if (len <= kBlockSort) {
                 int n2 = 2 * kWarpSort;
                 while (n2 < len) n2 <<= 1;
