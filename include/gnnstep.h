@@ -123,6 +123,11 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
 gnn_status gnn_model_destroy(gnn_model* m);
 /* stream: a cudaStream_t (as void*) on the graph's device, or NULL for the library's own. */
 gnn_status gnn_set_stream(gnn_model* m, void* stream);
+/* Overlap (default on): gnn_train_minibatch / gnn_train_epoch sample step s+1 of the
+ * epoch on the library's sampling stream while step s trains (two batch buffer sets,
+ * ordered by events; §4.1 lines 256-263 overlap sampling with training).  Off:
+ * every step samples then trains.  Results are identical either way. */
+gnn_status gnn_set_overlap(gnn_model* m, int32_t enable);
 /* The train split (copied).  ids in [0, N), duplicate-free.  n may be 0. */
 gnn_status gnn_set_train_nodes(gnn_model* m, const int32_t* ids_host, int64_t n);
 int64_t gnn_param_count(const gnn_model* m);
@@ -180,12 +185,18 @@ gnn_status gnn_sample_fetch(gnn_model* m, int32_t hop, int32_t what, int32_t* ou
  * enqueueing. */
 gnn_status gnn_train_minibatch(gnn_model* m, int64_t epoch, int64_t step, float* loss_out_host);
 
-/* End-to-end call: the seeds of this rank's batch come from HOST memory (pinned for
- * best speed), are copied to the device, the step runs (sampling keyed by (epoch, g)),
- * and this rank's loss is copied back; synchronous.  b_total = seeds in the step
- * over all ranks. */
+/* End-to-end call: the seeds of this rank's batch come from HOST memory (copied into the
+ * library's pinned staging, then to the device), the step runs (sampling keyed by
+ * (epoch, g)), and this rank's loss is copied back; synchronous.  b_total = seeds in the
+ * step over all ranks.  Optional prefetch: with next_g >= 0 the NEXT call's batch
+ * (next_seeds_host[0:next_n), next_b_total, global index next_g, same epoch) is sampled on
+ * the library's sampling stream while this batch trains; the next call with exactly those
+ * (epoch, g, n_seeds, b_total) reuses it (its seeds_host is then not re-read).  next_g < 0:
+ * no prefetch (next_* ignored).  The seed arrays are not retained after the call. */
 gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t n_seeds,
-                                int32_t b_total, int64_t epoch, int64_t g, float* loss_out_host);
+                                int32_t b_total, int64_t epoch, int64_t g,
+                                const int32_t* next_seeds_host, int32_t next_n, int32_t next_b_total,
+                                int64_t next_g, float* loss_out_host);
 
 typedef struct { double seconds; int64_t steps; int64_t minibatches; double mean_loss; } gnn_epoch_stats;
 /* All steps of an epoch (collective when world > 1). */

@@ -3,8 +3,13 @@
 // One step = the trainer-process work of PAPER.md §3 lines 237-242 (sampling → data
 // fetching → forward/backward → local gradient) + the synchronous-SGD exchange of §2.2
 // lines 173-175.  All buffers are sized once to worst-case bounds (DESIGN.md "Dynamic
-// shapes"); every kernel reads its extent from the device StepState, so the step body is
+// shapes"); every kernel reads its extent from a device StepState, so the training body is
 // captured once as a CUDA graph and replayed per mini-batch.
+//
+// Overlap (the B200 analog of the paper's process-level overlap, §4.1): the
+// batch-side buffers are double-buffered (two BatchSets).  While batch s trains on the
+// model's stream from set A, batch s+1 is sampled into set B on the library's sampling stream;
+// events order "sampled(B) -> train(B)" and "trained(A) -> sample into A".
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -82,11 +87,30 @@ struct gnn_graph {
 };
 
 namespace {
+// Capacities and sampling-kernel scratch of one block (hop h or the ShaDow induced block).
 struct HopBufs {
     int64_t cap_dst = 0, cap_edges = 0, cap_src = 0;
     bool need_t = false;
-    int32_t *rowptr = nullptr, *col = nullptr, *nbr = nullptr;
-    int32_t *tcount = nullptr, *trowptr = nullptr, *tcursor = nullptr, *tdst = nullptr, *tdst_s = nullptr;
+    int32_t *tcount = nullptr, *tcursor = nullptr, *tdst = nullptr;   // shared by both batch sets
+};
+
+// What one batch is made of, double-buffered: sizes, node list, per-block CSR + transposed CSR.
+struct BatchSet {
+    StepState* st = nullptr;
+    int32_t* nodes = nullptr;
+    int32_t* seeds_in = nullptr;     // device copy of host seeds (e2e)
+    int32_t* seeds_stage = nullptr;  // pinned host staging of those seeds
+    int32_t *rowptr[kMaxHops + 1] = {}, *nbr[kMaxHops + 1] = {}, *col[kMaxHops + 1] = {};
+    int32_t *trowptr[kMaxHops + 1] = {}, *tdst_s[kMaxHops + 1] = {};
+    SampleParams sp{};
+    cudaEvent_t sampled = nullptr, trained = nullptr;
+    bool trained_once = false;
+    // the batch this set holds (valid until trained or overwritten)
+    bool valid = false;
+    int64_t epoch = -1, g = -1;
+    int32_t n = -1, b_total = -1;
+    cudaGraphExec_t gexec = nullptr, prof_gexec = nullptr;
+    std::vector<struct ProfPair> prof_pairs;
 };
 
 struct Layer {
@@ -110,36 +134,37 @@ struct gnn_model {
     int L = 0, hops = 0, slot = -1;
     bool sage = true, shadow = false;
     std::vector<int> dims;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;       // training (the caller's, or own_stream)
     cudaStream_t own_stream = nullptr;
+    cudaStream_t sstream = nullptr;      // sampling (library-owned)
     std::vector<void*> owned;
+    std::vector<void*> owned_host;
 
-    StepState* st = nullptr;
-    int32_t *nodes = nullptr, *map = nullptr, *icount = nullptr;
+    BatchSet bs[2];
+    int last = -1;                       // set trained last
+    int fetch_set = 0;                   // set gnn_sample filled
+    int32_t *map = nullptr, *icount = nullptr;
+    uint32_t* seq = nullptr;             // step sequence counter (scan-word tags)
     unsigned long long* status = nullptr;
     GridBarrier* bar = nullptr;
-    SampleParams sp{};
     uint32_t* bits = nullptr;
     int64_t nwords = 0, nodes_cap = 0;
     HopBufs hb[kMaxHops + 1];
     std::vector<Layer> layers;
     float *params = nullptr, *grads = nullptr;
     int64_t pcount = 0;
+    bool overlap = true;                 // prefetch the next batch during training
 
-    int32_t *train = nullptr, *perm = nullptr, *train_sorted = nullptr;
+    int32_t *perm = nullptr, *train_sorted = nullptr;
     uint64_t *keys = nullptr, *keys_alt = nullptr;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
     int64_t n_train = 0, train_cap = 0, perm_epoch = -1;
-    int32_t* seeds_in = nullptr;
 
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
 
-    bool bf16x3 = true;            // fp32 parity mode: 3-term bf16 split GEMMs
-    cudaGraphExec_t gexec = nullptr;
-    cudaGraphExec_t prof_gexec = nullptr;   // instrumented copy (event-record nodes)
-    std::vector<ProfPair> prof_pairs;
+    bool bf16x3 = true;                  // fp32 parity mode: 3-term bf16 split GEMMs
     int64_t launches_per_step = 0;
 
     bool profiling = false;
@@ -163,16 +188,16 @@ cudaEvent_t take_event(gnn_model* m) {
 }
 
 template <class Fn>
-void K(gnn_model* m, int kid, Fn&& fn) {
+void K(gnn_model* m, cudaStream_t s, int kid, Fn&& fn) {
     if (m->profiling) {
         ProfPair p{kid, take_event(m), take_event(m)};
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        cudaStreamIsCapturing(m->stream, &cs);
+        cudaStreamIsCapturing(s, &cs);
         // inside a capture, only an "external" record node really records at replay time
         const unsigned fl = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
-        cudaEventRecordWithFlags(p.a, m->stream, fl);
+        cudaEventRecordWithFlags(p.a, s, fl);
         fn();
-        cudaEventRecordWithFlags(p.b, m->stream, fl);
+        cudaEventRecordWithFlags(p.b, s, fl);
         m->pending.push_back(p);
     } else {
         fn();
@@ -204,100 +229,94 @@ PackAll pack_desc(gnn_model* m) {
     return p;
 }
 
-const int32_t* rows_ptr(gnn_model* m, int li) {   // output rows of layer li (0-based)
-    if (m->shadow && li == m->L - 1) return &m->st->batch_n;
-    return &m->st->n_dst[m->layers[li].blk];
+const int32_t* rows_ptr(gnn_model* m, int set, int li) {   // output rows of layer li (0-based)
+    StepState* st = m->bs[set].st;
+    if (m->shadow && li == m->L - 1) return &st->batch_n;
+    return &st->n_dst[m->layers[li].blk];
 }
 
-// ---------------------------------------------------------------- step body
-// Sampling, relabel, ShaDow induce, transposed blocks, map reset: one persistent launch.
-void enqueue_sampling(gnn_model* m) {
-    K(m, GNN_K_SAMPLE, [&] { launch_sample_step(m->sp, m->stream); });
-}
-
-void enqueue_training(gnn_model* m) {
+// ---------------------------------------------------------------- step bodies
+void enqueue_training(gnn_model* m, int set) {
     gnn_graph* g = m->g;
+    BatchSet& B = m->bs[set];
     cudaStream_t s = m->stream;
     const int L = m->L;
     // ---- forward
     for (int li = 0; li < L; ++li) {
         Layer& ly = m->layers[li];
-        HopBufs& b = m->hb[ly.blk];
-        const int32_t* rows = rows_ptr(m, li);
+        const int blk = ly.blk;
+        const int32_t* rows = rows_ptr(m, set, li);
         // layer 1 reads the feature table (local or row-sharded over peers); later layers H_{l-1}
         const FeatRows Hrows = li == 0 ? g->rows() : FeatRows{m->layers[li - 1].H, nullptr, 0};
         const int kid = li == 0 ? GNN_K_AGG_L1 : GNN_K_AGG;
+        const int32_t* self_ids = li == 0 ? B.nodes : nullptr;
         if (m->sage) {
             // layer 1 of the neighbour sampler reads X rows directly by global neighbour id
             const bool direct = li == 0 && !m->shadow;
-            K(m, kid, [&] {
-                launch_agg_sage(rows, Hrows, ly.in_pad, direct ? nullptr : (li == 0 ? m->nodes : nullptr),
-                                li == 0 ? m->nodes : nullptr, b.rowptr, direct ? b.nbr : b.col, ly.A, s);
+            K(m, s, kid, [&] {
+                launch_agg_sage(rows, Hrows, ly.in_pad, direct ? nullptr : self_ids, self_ids, B.rowptr[blk],
+                                direct ? B.nbr[blk] : B.col[blk], ly.A, s);
             });
         } else {
-            K(m, kid, [&] {
-                launch_agg_gcn(rows, &m->st->n_dst[ly.blk], Hrows, ly.in_pad, ly.k_pad, li == 0 ? m->nodes : nullptr,
-                               li == 0 ? m->nodes : nullptr, b.rowptr, b.col, b.trowptr, ly.A, s);
+            K(m, s, kid, [&] {
+                launch_agg_gcn(rows, &B.st->n_dst[blk], Hrows, ly.in_pad, ly.k_pad, self_ids, self_ids,
+                               B.rowptr[blk], B.col[blk], B.trowptr[blk], ly.A, s);
             });
         }
         // Pre = A W (+ReLU) -> H (fp32)
-        K(m, GNN_K_GEMM_FWD, [&] {
+        K(m, s, GNN_K_GEMM_FWD, [&] {
             launch_gemm_tc(2, m->bf16x3, ly.map_fwd, rows, 0, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, ly.n_pad,
                            ly.n_pad, li < L - 1, 1, 0, s);
         });
     }
     // ---- loss
     Layer& last = m->layers[L - 1];
-    K(m, GNN_K_CE, [&] { launch_ce(m->st, last.H, last.n_pad, g->C, g->y, m->nodes, last.dPre, s); });
+    K(m, s, GNN_K_CE, [&] { launch_ce(B.st, last.H, last.n_pad, g->C, g->y, B.nodes, last.dPre, s); });
     // ---- backward
     for (int li = L - 1; li >= 0; --li) {
         Layer& ly = m->layers[li];
-        const int32_t* rows = rows_ptr(m, li);
+        const int32_t* rows = rows_ptr(m, set, li);
         const int64_t stride = (int64_t)ly.k_pad * ly.n_pad;
-        // dW = A^T dPre (deterministic split over rows) -> grads
-        K(m, GNN_K_GEMM_WGRAD, [&] {
+        // dW = A^T dPre (deterministic split over rows)
+        K(m, s, GNN_K_GEMM_WGRAD, [&] {
             launch_gemm_tc(1, m->bf16x3, ly.map_wgrad, rows, ly.k_pad, ly.k_pad, ly.n_pad, 0, ly.wpart, ly.n_pad,
                            ly.n_pad, false, ly.splits, stride, s);
         });
         if (li == 0) break;
         // dA = dPre W^T (fp32)
-        K(m, GNN_K_GEMM_DGRAD, [&] {
+        K(m, s, GNN_K_GEMM_DGRAD, [&] {
             launch_gemm_tc(0, m->bf16x3, ly.map_dgrad, rows, 0, (int)ly.m_cap, ly.k_pad, ly.n_pad, ly.dA, ly.k_pad,
                            ly.k_pad, false, 1, 0, s);
         });
         Layer& prev = m->layers[li - 1];
-        HopBufs& b = m->hb[ly.blk];
-        K(m, GNN_K_SPMM_BWD, [&] {
-            launch_spmm_bwd(!m->sage, ly.blk, m->st, rows, ly.dA, ly.in_pad, b.rowptr, b.trowptr, b.tdst_s,
+        const int blk = ly.blk;
+        K(m, s, GNN_K_SPMM_BWD, [&] {
+            launch_spmm_bwd(!m->sage, blk, B.st, rows, ly.dA, ly.in_pad, B.rowptr[blk], B.trowptr[blk], B.tdst_s[blk],
                             prev.H, prev.dPre, s);
         });
     }
     // ---- split-K partials of every layer -> flat gradient (fixed order)
-    K(m, GNN_K_GEMM_WGRAD, [&] { launch_wgrad_reduce_all(pack_desc(m), m->grads, s); });
+    K(m, s, GNN_K_GEMM_WGRAD, [&] { launch_wgrad_reduce_all(pack_desc(m), m->grads, s); });
     // ---- exchange + update
     if (m->world > 1)
-        K(m, GNN_K_ALLREDUCE, [&] {
+        K(m, s, GNN_K_ALLREDUCE, [&] {
             ncclAllReduce(m->grads, m->grads, (size_t)m->pcount, ncclFloat, ncclSum, m->comm, s);
         });
-    K(m, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, s); });
+    K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, s); });
 }
 
-void enqueue_body(gnn_model* m) {
-    enqueue_sampling(m);
-    enqueue_training(m);
-}
-
-// Capture the step body once.  With profiling on, the capture also records an event pair
-// around every kernel class launch (event-record nodes), read back after each replay.
-gnn_status build_graph(gnn_model* m, bool prof) {
-    cudaGraphExec_t* target = prof ? &m->prof_gexec : &m->gexec;
+// Capture the training body of batch set `set` once.  With profiling on, the capture also
+// records an event pair around every kernel-class launch (event-record nodes).
+gnn_status build_graph(gnn_model* m, int set, bool prof) {
+    BatchSet& B = m->bs[set];
+    cudaGraphExec_t* target = prof ? &B.prof_gexec : &B.gexec;
     if (*target) return GNN_OK;
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
     const size_t before = m->pending.size();
-    enqueue_body(m);
+    enqueue_training(m, set);
     if (prof) {
-        m->prof_pairs.assign(m->pending.begin() + before, m->pending.end());
+        B.prof_pairs.assign(m->pending.begin() + before, m->pending.end());
         m->pending.resize(before);
     }
     cudaError_t e = cudaStreamEndCapture(m->stream, &graph);
@@ -312,48 +331,33 @@ gnn_status build_graph(gnn_model* m, bool prof) {
         cudaGraphNodeGetType(nd, &t);
         if (t == cudaGraphNodeTypeKernel) ++kernels;
     }
-    if (!prof) m->launches_per_step = kernels + 1;   // + k_begin_step (outside the graph)
+    if (!prof) m->launches_per_step = kernels + 2;   // + k_begin_step + k_sample_step (sampling stream)
     CK(cudaGraphInstantiate(target, graph, 0));
     CK(cudaGraphDestroy(graph));
     return GNN_OK;
 }
 
-// Checked before k_begin_step marks the seeds in the map (a step that starts must finish).
+void drop_graphs(gnn_model* m) {
+    for (auto& B : m->bs) {
+        if (B.gexec) { cudaGraphExecDestroy(B.gexec); B.gexec = nullptr; }
+        if (B.prof_gexec) { cudaGraphExecDestroy(B.prof_gexec); B.prof_gexec = nullptr; }
+    }
+}
+
+// Checked before a batch is sampled into a set (a started batch must be trainable).
 gnn_status check_ready(gnn_model* m) {
     if (m->g->nshards && !m->g->shard_ptrs)
         return fail(GNN_ERR_STATE, "row-sharded features: call gnn_shard_import before training");
     return GNN_OK;
 }
 
-gnn_status run_body(gnn_model* m) {
-    if (m->cfg.use_graph && !m->profiling) {
-        TRY(build_graph(m, false));
-        CK(cudaGraphLaunch(m->gexec, m->stream));
-    } else if (m->cfg.use_graph) {
-        // instrumented replay: the same graph body with event-record nodes; read them back now
-        TRY(build_graph(m, true));
-        CK(cudaGraphLaunch(m->prof_gexec, m->stream));
-        CK(cudaStreamSynchronize(m->stream));
-        for (auto& p : m->prof_pairs) {
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, p.a, p.b));
-            m->prof_ms[p.kid] += ms;
-            m->prof_n[p.kid] += 1;
-        }
-    } else {
-        enqueue_body(m);
-        CK(cudaGetLastError());
-    }
-    return GNN_OK;
-}
-
-gnn_status ensure_perm(gnn_model* m, int64_t epoch) {
+gnn_status ensure_perm(gnn_model* m, int64_t epoch) {   // on the sampling stream
     if (m->perm_epoch == epoch) return GNN_OK;
     if (m->n_train > 0) {
-        launch_perm_keys(m->train_sorted, m->n_train, m->cfg.seed, epoch, m->keys, m->stream);
+        launch_perm_keys(m->train_sorted, m->n_train, m->cfg.seed, epoch, m->keys, m->sstream);
         size_t bytes = m->cub_bytes;
         CK(cub::DeviceRadixSort::SortPairs(m->cub_tmp, bytes, m->keys, m->keys_alt, m->train_sorted, m->perm,
-                                           (int)m->n_train, 0, 64, m->stream));
+                                           (int)m->n_train, 0, 64, m->sstream));
     }
     m->perm_epoch = epoch;
     return GNN_OK;
@@ -363,12 +367,15 @@ int64_t num_batches(const gnn_model* m) {
     return (m->n_train + m->cfg.batch_size - 1) / m->cfg.batch_size;
 }
 
+int64_t steps_per_epoch(const gnn_model* m) {
+    return (num_batches(m) + m->world - 1) / m->world;
+}
+
 gnn_status set_device(int dev) {
     CK(cudaSetDevice(dev));
     return GNN_OK;
 }
 
-// Step for this rank: global batch g = step*world + rank.
 // Batch -> rank rule of synchronous SGD (R8/R9; §2.2).
 void plan_step(int64_t n_train, int64_t B, int64_t world, int64_t rank, int64_t step, int64_t* g, int32_t* n,
                int64_t* offset, int32_t* b_total) {
@@ -380,15 +387,109 @@ void plan_step(int64_t n_train, int64_t B, int64_t world, int64_t rank, int64_t 
     *b_total = (int32_t)std::max<int64_t>(0, std::min<int64_t>(n_train - done, world * B));
 }
 
-gnn_status begin_step_from_perm(gnn_model* m, int64_t epoch, int64_t step) {
+// Sample a batch into set `set` on the sampling stream (after the set's previous training).
+// seeds_dev: device seed list (the epoch permutation slice) or nullptr with seeds_host.
+gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const int32_t* seeds_host, int32_t n,
+                        int32_t b_total, int64_t epoch, int64_t g) {
+    BatchSet& B = m->bs[set];
+    if (B.trained_once) CK(cudaStreamWaitEvent(m->sstream, B.trained, 0));
+    const int32_t* src = seeds_dev;
+    if (!src) {
+        if (n) {
+            CK(cudaEventSynchronize(B.sampled));   // the staging slot's previous copy is done
+            std::memcpy(B.seeds_stage, seeds_host, sizeof(int32_t) * n);
+            CK(cudaMemcpyAsync(B.seeds_in, B.seeds_stage, sizeof(int32_t) * n, cudaMemcpyHostToDevice, m->sstream));
+        }
+        src = B.seeds_in;
+    }
+    launch_begin_step(B.st, src, n, b_total, (uint32_t)epoch, (uint32_t)g, B.nodes, m->map, m->seq, m->sstream);
+    K(m, m->sstream, GNN_K_SAMPLE, [&] { launch_sample_step(B.sp, m->sstream); });
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(B.sampled, m->sstream));
+    B.valid = true;
+    B.epoch = epoch;
+    B.g = g;
+    B.n = n;
+    B.b_total = b_total;
+    return GNN_OK;
+}
+
+gnn_status issue_sample_step(gnn_model* m, int set, int64_t epoch, int64_t step) {
     TRY(ensure_perm(m, epoch));
     int64_t g, offset;
     int32_t n, b_total;
     plan_step(m->n_train, m->cfg.batch_size, m->world, m->rank, step, &g, &n, &offset, &b_total);
-    launch_begin_step(m->st, n > 0 ? m->perm + offset : m->perm, n, b_total, (uint32_t)epoch, (uint32_t)g,
-                      m->nodes, m->map, m->stream);
+    return issue_sample(m, set, n > 0 ? m->perm + offset : m->perm, nullptr, n, b_total, epoch, g);
+}
+
+int find_set(gnn_model* m, int64_t epoch, int64_t g, int32_t n, int32_t b_total) {
+    for (int k = 0; k < 2; ++k) {
+        const BatchSet& B = m->bs[k];
+        if (B.valid && B.epoch == epoch && B.g == g && B.n == n && B.b_total == b_total) return k;
+    }
+    return -1;
+}
+
+int other_set(gnn_model* m) { return m->last < 0 ? 0 : 1 - m->last; }
+
+// Train the batch held by `set` on the model's stream.
+gnn_status train_set(gnn_model* m, int set) {
+    BatchSet& B = m->bs[set];
+    CK(cudaStreamWaitEvent(m->stream, B.sampled, 0));
+    if (m->cfg.use_graph && !m->profiling) {
+        TRY(build_graph(m, set, false));
+        CK(cudaGraphLaunch(B.gexec, m->stream));
+    } else if (m->cfg.use_graph) {
+        // instrumented replay: the same graph body with event-record nodes; read them back now
+        TRY(build_graph(m, set, true));
+        CK(cudaGraphLaunch(B.prof_gexec, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        drain_profile(m);                       // the sampling kernel's pair (eager)
+        for (auto& p : B.prof_pairs) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p.a, p.b));
+            m->prof_ms[p.kid] += ms;
+            m->prof_n[p.kid] += 1;
+        }
+    } else {
+        enqueue_training(m, set);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(B.trained, m->stream));
+    B.trained_once = true;
+    B.valid = false;
+    m->last = set;
     return GNN_OK;
 }
+
+// One step of the epoch loop: use the prefetched sample if it is this step's batch, prefetch
+// the next step's batch into the other set, train.
+gnn_status step_from_perm(gnn_model* m, int64_t epoch, int64_t step) {
+    int64_t g, offset;
+    int32_t n, b_total;
+    plan_step(m->n_train, m->cfg.batch_size, m->world, m->rank, step, &g, &n, &offset, &b_total);
+    int cur = find_set(m, epoch, g, n, b_total);
+    if (cur < 0) {
+        cur = other_set(m);
+        TRY(issue_sample_step(m, cur, epoch, step));
+    }
+    if (m->overlap && !m->profiling && step + 1 < steps_per_epoch(m)) TRY(issue_sample_step(m, 1 - cur, epoch, step + 1));
+    return train_set(m, cur);
+}
+
+gnn_status sync_all(gnn_model* m) {
+    CK(cudaStreamSynchronize(m->sstream));
+    CK(cudaStreamSynchronize(m->stream));
+    return GNN_OK;
+}
+
+gnn_status copy_state(gnn_model* m, int set, StepState* out) {
+    TRY(sync_all(m));
+    CK(cudaMemcpy(out, m->bs[set].st, sizeof(StepState), cudaMemcpyDeviceToHost));
+    return GNN_OK;
+}
+
+int shown_set(gnn_model* m) { return m->last < 0 ? 0 : m->last; }
 }  // namespace
 
 // ====================================================================== C ABI
@@ -533,7 +634,12 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     m->sage = c.model == GNN_SAGE_MEAN; m->shadow = c.sampler == GNN_SHADOW;
     m->slot = m->shadow ? m->hops : -1;
     m->bf16x3 = c.precision == GNN_FP32;
-    auto cleanup = [&](gnn_status s) { for (void* p : m->owned) cudaFree(p); delete m; return s; };
+    auto cleanup = [&](gnn_status s) {
+        for (void* p : m->owned) cudaFree(p);
+        for (void* p : m->owned_host) cudaFreeHost(p);
+        delete m;
+        return s;
+    };
     gnn_status s;
 #define AL(p, n) if ((s = dalloc(&(p), (n), m->owned)) != GNN_OK) return cleanup(s)
 
@@ -557,55 +663,72 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         b.need_t = true;
     }
     m->nwords = (g->N + 31) / 32;
-    AL(m->st, 1);
-    AL(m->nodes, m->nodes_cap);
+    // shared sampling scratch (sampling runs are serialised on the sampling stream)
     AL(m->map, g->N);
     AL(m->bits, m->nwords);
     AL(m->icount, m->nodes_cap);
-    AL(m->seeds_in, c.batch_size);
+    AL(m->seq, 1);
     const int sgrid = sample_step_grid();
     AL(m->status, (int64_t)sample_step_sites(m->hops) * sgrid);
-    CK(cudaMemset(m->status, 0, sizeof(unsigned long long) * sample_step_sites(m->hops) * sgrid));
     AL(m->bar, 1);
+    CK(cudaMemset(m->status, 0, sizeof(unsigned long long) * sample_step_sites(m->hops) * sgrid));
     CK(cudaMemset(m->bar, 0, sizeof(GridBarrier)));
-    m->sp = SampleParams{};
-    m->sp.st = m->st;
-    m->sp.row_ptr = g->row_ptr;
-    m->sp.col = g->col;
-    m->sp.nodes = m->nodes;
-    m->sp.map = m->map;
-    m->sp.bits = m->bits;
-    m->sp.nwords = (int)m->nwords;
-    m->sp.seed = c.seed;
-    m->sp.hops = m->hops;
-    m->sp.shadow = m->shadow ? 1 : 0;
-    m->sp.slot = m->shadow ? m->slot : -1;
-    m->sp.icount = m->icount;
-    m->sp.status = m->status;
-    m->sp.bar = m->bar;
+    CK(cudaMemset(m->seq, 0, sizeof(uint32_t)));
+    CK(cudaMemset(m->map, 0xff, sizeof(int32_t) * g->N));
+    CK(cudaMemset(m->bits, 0, sizeof(uint32_t) * m->nwords));
     for (int h = 0; h <= m->hops; ++h) {
         if (h == m->hops && !m->shadow) break;
         HopBufs& b = m->hb[h];
-        AL(b.rowptr, b.cap_dst + 1);
-        AL(b.col, b.cap_edges);
-        if (h < m->hops) AL(b.nbr, b.cap_edges);
         if (b.need_t) {
             AL(b.tcount, b.cap_src + 1);
-            AL(b.trowptr, b.cap_src + 1);
             AL(b.tcursor, b.cap_src + 1);
             AL(b.tdst, b.cap_edges);
-            AL(b.tdst_s, b.cap_edges);
             CK(cudaMemset(b.tcount, 0, sizeof(int32_t) * (b.cap_src + 1)));
         }
-        HopIO& io = m->sp.hop[h];
-        io.k = h < m->hops ? c.fanouts[m->hops - 1 - h] : 0;
-        io.rowptr = b.rowptr; io.nbr = b.nbr; io.col = b.col;
-        io.tcount = b.need_t ? b.tcount : nullptr;
-        io.trowptr = b.trowptr; io.tcursor = b.tcursor; io.tdst = b.tdst; io.tdst_s = b.tdst_s;
     }
-    CK(cudaMemset(m->map, 0xff, sizeof(int32_t) * g->N));
-    CK(cudaMemset(m->bits, 0, sizeof(uint32_t) * m->nwords));
-    CK(cudaMemset(m->st, 0, sizeof(StepState)));
+    // ---- the two batch sets
+    for (int k = 0; k < 2; ++k) {
+        BatchSet& B = m->bs[k];
+        AL(B.st, 1);
+        CK(cudaMemset(B.st, 0, sizeof(StepState)));
+        AL(B.nodes, m->nodes_cap);
+        AL(B.seeds_in, c.batch_size);
+        CK(cudaMallocHost(&B.seeds_stage, sizeof(int32_t) * c.batch_size));
+        m->owned_host.push_back(B.seeds_stage);
+        CK(cudaEventCreateWithFlags(&B.sampled, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&B.trained, cudaEventDisableTiming));
+        SampleParams& sp = B.sp;
+        sp.st = B.st;
+        sp.row_ptr = g->row_ptr;
+        sp.col = g->col;
+        sp.nodes = B.nodes;
+        sp.map = m->map;
+        sp.bits = m->bits;
+        sp.nwords = (int)m->nwords;
+        sp.seed = c.seed;
+        sp.hops = m->hops;
+        sp.shadow = m->shadow ? 1 : 0;
+        sp.slot = m->shadow ? m->slot : -1;
+        sp.icount = m->icount;
+        sp.status = m->status;
+        sp.bar = m->bar;
+        for (int h = 0; h <= m->hops; ++h) {
+            if (h == m->hops && !m->shadow) break;
+            HopBufs& b = m->hb[h];
+            AL(B.rowptr[h], b.cap_dst + 1);
+            AL(B.col[h], b.cap_edges);
+            if (h < m->hops) AL(B.nbr[h], b.cap_edges);
+            if (b.need_t) {
+                AL(B.trowptr[h], b.cap_src + 1);
+                AL(B.tdst_s[h], b.cap_edges);
+            }
+            HopIO& io = sp.hop[h];
+            io.k = h < m->hops ? c.fanouts[m->hops - 1 - h] : 0;
+            io.rowptr = B.rowptr[h]; io.nbr = B.nbr[h]; io.col = B.col[h];
+            io.tcount = b.need_t ? b.tcount : nullptr;
+            io.trowptr = B.trowptr[h]; io.tcursor = b.tcursor; io.tdst = b.tdst; io.tdst_s = B.tdst_s[h];
+        }
+    }
 
     // ---- layers
     m->dims.push_back(g->F);
@@ -672,6 +795,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     AL(m->grads, m->pcount);
 #undef AL
     CK(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&m->sstream, cudaStreamNonBlocking));
     m->stream = m->own_stream;
     // ---- Glorot-uniform init (per layer block)
     for (int li = 0; li < m->L; ++li) {
@@ -682,6 +806,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, m->stream);
     CK(cudaMemsetAsync(m->grads, 0, sizeof(float) * m->pcount, m->stream));
     CK(cudaStreamSynchronize(m->stream));
+    CK(cudaDeviceSynchronize());
     CK(cudaGetLastError());
     *out = m;
     return GNN_OK;
@@ -691,15 +816,22 @@ gnn_status gnn_model_destroy(gnn_model* m) {
     if (!m) return GNN_OK;
     cudaSetDevice(m->g->dev);
     if (m->stream) cudaStreamSynchronize(m->stream);
+    if (m->sstream) cudaStreamSynchronize(m->sstream);
     drain_profile(m);
     for (auto e : m->free_events) cudaEventDestroy(e);
-    if (m->gexec) cudaGraphExecDestroy(m->gexec);
-    if (m->prof_gexec) cudaGraphExecDestroy(m->prof_gexec);
-    for (auto& p : m->prof_pairs) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    drop_graphs(m);
+    for (auto& B : m->bs) {
+        for (auto& p : B.prof_pairs) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+        if (B.sampled) cudaEventDestroy(B.sampled);
+        if (B.trained) cudaEventDestroy(B.trained);
+    }
     if (m->comm) ncclCommDestroy(m->comm);
     for (void* p : m->owned) cudaFree(p);
-    if (m->cub_tmp) cudaFree(m->cub_tmp);
+    for (void* p : m->owned_host) cudaFreeHost(p);
+    for (void* p : {(void*)m->train_sorted, (void*)m->perm, (void*)m->keys, (void*)m->keys_alt, m->cub_tmp})
+        if (p) cudaFree(p);
     if (m->own_stream) cudaStreamDestroy(m->own_stream);
+    if (m->sstream) cudaStreamDestroy(m->sstream);
     delete m;
     return GNN_OK;
 }
@@ -707,8 +839,14 @@ gnn_status gnn_model_destroy(gnn_model* m) {
 gnn_status gnn_set_stream(gnn_model* m, void* stream) {
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
     TRY(set_device(m->g->dev));
-    CK(cudaStreamSynchronize(m->stream));
+    TRY(sync_all(m));
     m->stream = stream ? (cudaStream_t)stream : m->own_stream;
+    return GNN_OK;
+}
+
+gnn_status gnn_set_overlap(gnn_model* m, int32_t enable) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    m->overlap = enable != 0;
     return GNN_OK;
 }
 
@@ -722,7 +860,7 @@ gnn_status gnn_set_train_nodes(gnn_model* m, const int32_t* ids_host, int64_t n)
         if (i && ids[i] == ids[i - 1]) return fail(GNN_ERR_PARAM, "duplicate train id");
     }
     TRY(set_device(m->g->dev));
-    CK(cudaStreamSynchronize(m->stream));
+    TRY(sync_all(m));
     if (n > m->train_cap) {
         for (void* p : {(void*)m->train_sorted, (void*)m->perm, (void*)m->keys, (void*)m->keys_alt, m->cub_tmp})
             if (p) cudaFree(p);
@@ -732,13 +870,14 @@ gnn_status gnn_set_train_nodes(gnn_model* m, const int32_t* ids_host, int64_t n)
         CK(cudaMalloc(&m->keys_alt, sizeof(uint64_t) * n));
         m->cub_bytes = 0;
         CK(cub::DeviceRadixSort::SortPairs(nullptr, m->cub_bytes, m->keys, m->keys_alt, m->train_sorted, m->perm,
-                                           (int)n, 0, 64, m->stream));
+                                           (int)n, 0, 64, m->sstream));
         CK(cudaMalloc(&m->cub_tmp, m->cub_bytes));
         m->train_cap = n;
     }
     if (n) CK(cudaMemcpy(m->train_sorted, ids.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     m->n_train = n;
     m->perm_epoch = -1;
+    for (auto& B : m->bs) B.valid = false;
     return GNN_OK;
 }
 
@@ -791,6 +930,7 @@ int64_t gnn_steps_per_epoch(int64_t n_train, int32_t batch_size, int32_t world) 
 gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_t id_host[128]) {
     if (!m || !id_host || world < 1 || rank < 0 || rank >= world) return fail(GNN_ERR_PARAM, "bad arguments");
     TRY(set_device(m->g->dev));
+    TRY(sync_all(m));
     if (m->comm) { ncclCommDestroy(m->comm); m->comm = nullptr; }
     if (world > 1) {
         ncclUniqueId id;
@@ -799,8 +939,8 @@ gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_
     }
     m->rank = rank;
     m->world = world;
-    if (m->gexec) { cudaGraphExecDestroy(m->gexec); m->gexec = nullptr; }
-    if (m->prof_gexec) { cudaGraphExecDestroy(m->prof_gexec); m->prof_gexec = nullptr; }
+    drop_graphs(m);
+    for (auto& B : m->bs) B.valid = false;
     return GNN_OK;
 }
 
@@ -810,8 +950,8 @@ gnn_status gnn_epoch_permutation(gnn_model* m, int64_t epoch, int32_t* out_host,
     TRY(set_device(m->g->dev));
     TRY(ensure_perm(m, epoch));
     if (m->n_train)
-        CK(cudaMemcpyAsync(out_host, m->perm, sizeof(int32_t) * m->n_train, cudaMemcpyDeviceToHost, m->stream));
-    CK(cudaStreamSynchronize(m->stream));
+        CK(cudaMemcpyAsync(out_host, m->perm, sizeof(int32_t) * m->n_train, cudaMemcpyDeviceToHost, m->sstream));
+    CK(cudaStreamSynchronize(m->sstream));
     return GNN_OK;
 }
 
@@ -823,15 +963,16 @@ gnn_status gnn_sample(gnn_model* m, int64_t epoch, int64_t g, gnn_batch_sizes* s
     TRY(ensure_perm(m, epoch));
     const int64_t B = m->cfg.batch_size;
     const int32_t n = (int32_t)std::min<int64_t>(B, m->n_train - g * B);
-    launch_begin_step(m->st, m->perm + g * B, n, n, (uint32_t)epoch, (uint32_t)g, m->nodes, m->map, m->stream);
+    const int set = other_set(m);
     const bool prof = m->profiling;
     m->profiling = false;
-    enqueue_sampling(m);
+    gnn_status st_ = issue_sample(m, set, m->perm + g * B, nullptr, n, n, epoch, g);
     m->profiling = prof;
-    CK(cudaGetLastError());
+    TRY(st_);
+    m->bs[set].valid = false;   // a parity sample is not a training batch
+    m->fetch_set = set;
     StepState st;
-    CK(cudaMemcpyAsync(&st, m->st, sizeof(StepState), cudaMemcpyDeviceToHost, m->stream));
-    CK(cudaStreamSynchronize(m->stream));
+    TRY(copy_state(m, set, &st));
     sizes_host->num_hops = m->hops;
     for (int h = 0; h <= kMaxHops; ++h) {
         sizes_host->n_dst[h] = st.n_dst[h];
@@ -846,24 +987,23 @@ gnn_status gnn_sample_fetch(gnn_model* m, int32_t hop, int32_t what, int32_t* ou
     const int maxhop = m->shadow ? m->hops : m->hops - 1;
     if (hop < 0 || hop > maxhop) return fail(GNN_ERR_RANGE, "hop out of range");
     TRY(set_device(m->g->dev));
+    const BatchSet& B = m->bs[m->fetch_set];
     StepState st;
-    CK(cudaMemcpyAsync(&st, m->st, sizeof(StepState), cudaMemcpyDeviceToHost, m->stream));
-    CK(cudaStreamSynchronize(m->stream));
-    const HopBufs& b = m->hb[hop];
+    TRY(copy_state(m, m->fetch_set, &st));
     int64_t len = 0;
     const int32_t* src = nullptr;
     switch (what) {
-        case GNN_SRC_IDS: len = st.n_src[hop]; src = m->nodes; break;
-        case GNN_BLK_ROWPTR: len = st.n_dst[hop] + 1; src = b.rowptr; break;
-        case GNN_BLK_COL: len = st.n_edges[hop]; src = b.col; break;
-        case GNN_BLK_NBR: len = st.n_edges[hop]; src = hop < m->hops ? b.nbr : b.col; break;
+        case GNN_SRC_IDS: len = st.n_src[hop]; src = B.nodes; break;
+        case GNN_BLK_ROWPTR: len = st.n_dst[hop] + 1; src = B.rowptr[hop]; break;
+        case GNN_BLK_COL: len = st.n_edges[hop]; src = B.col[hop]; break;
+        case GNN_BLK_NBR: len = st.n_edges[hop]; src = hop < m->hops ? B.nbr[hop] : B.col[hop]; break;
         default: return fail(GNN_ERR_PARAM, "unknown array");
     }
     if (n < len) return fail(GNN_ERR_BUFFER, "buffer too small: need " + std::to_string(len));
     if (len) CK(cudaMemcpy(out_host, src, sizeof(int32_t) * len, cudaMemcpyDeviceToHost));
     if (what == GNN_BLK_NBR && hop == m->hops && len) {   // induced block: global id of each source
         std::vector<int32_t> ids(st.n_src[hop]);
-        if (!ids.empty()) CK(cudaMemcpy(ids.data(), m->nodes, sizeof(int32_t) * ids.size(), cudaMemcpyDeviceToHost));
+        if (!ids.empty()) CK(cudaMemcpy(ids.data(), B.nodes, sizeof(int32_t) * ids.size(), cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < len; ++i) out_host[i] = ids[out_host[i]];
     }
     return GNN_OK;
@@ -874,27 +1014,34 @@ gnn_status gnn_train_minibatch(gnn_model* m, int64_t epoch, int64_t step, float*
     if (step < 0 || epoch < 0) return fail(GNN_ERR_PARAM, "negative epoch/step");
     TRY(set_device(m->g->dev));
     TRY(check_ready(m));
-    TRY(begin_step_from_perm(m, epoch, step));
-    TRY(run_body(m));
+    TRY(step_from_perm(m, epoch, step));
     if (loss_out_host) {
-        CK(cudaMemcpyAsync(loss_out_host, &m->st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaMemcpyAsync(loss_out_host, &m->bs[m->last].st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
         CK(cudaStreamSynchronize(m->stream));
     }
     return GNN_OK;
 }
 
 gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t n_seeds, int32_t b_total,
-                                int64_t epoch, int64_t g, float* loss_out_host) {
+                                int64_t epoch, int64_t g, const int32_t* next_seeds_host, int32_t next_n,
+                                int32_t next_b_total, int64_t next_g, float* loss_out_host) {
     if (!m || (n_seeds > 0 && !seeds_host) || !loss_out_host) return fail(GNN_ERR_PARAM, "NULL argument");
     if (n_seeds < 0 || n_seeds > m->cfg.batch_size) return fail(GNN_ERR_SHAPE, "n_seeds must be 0..batch_size");
     if (b_total < n_seeds) return fail(GNN_ERR_PARAM, "b_total < n_seeds");
+    const bool prefetch = next_g >= 0;
+    if (prefetch && (next_n < 0 || next_n > m->cfg.batch_size || next_b_total < next_n || (next_n > 0 && !next_seeds_host)))
+        return fail(GNN_ERR_PARAM, "bad next batch");
     TRY(set_device(m->g->dev));
     TRY(check_ready(m));
-    if (n_seeds)
-        CK(cudaMemcpyAsync(m->seeds_in, seeds_host, sizeof(int32_t) * n_seeds, cudaMemcpyHostToDevice, m->stream));
-    launch_begin_step(m->st, m->seeds_in, n_seeds, b_total, (uint32_t)epoch, (uint32_t)g, m->nodes, m->map, m->stream);
-    TRY(run_body(m));
-    CK(cudaMemcpyAsync(loss_out_host, &m->st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
+    int cur = find_set(m, epoch, g, n_seeds, b_total);
+    if (cur < 0) {
+        cur = other_set(m);
+        TRY(issue_sample(m, cur, nullptr, seeds_host, n_seeds, b_total, epoch, g));
+    }
+    if (prefetch && m->overlap && !m->profiling)
+        TRY(issue_sample(m, 1 - cur, nullptr, next_seeds_host, next_n, next_b_total, epoch, next_g));
+    TRY(train_set(m, cur));
+    CK(cudaMemcpyAsync(loss_out_host, &m->bs[cur].st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }
@@ -903,19 +1050,18 @@ gnn_status gnn_train_epoch(gnn_model* m, int64_t epoch, gnn_epoch_stats* out_hos
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
     TRY(set_device(m->g->dev));
     const int64_t nb = num_batches(m);
-    const int64_t steps = (nb + m->world - 1) / m->world;
+    const int64_t steps = steps_per_epoch(m);
     TRY(check_ready(m));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    std::vector<float> losses(steps);
     float* pinned = nullptr;
     CK(cudaMallocHost(&pinned, sizeof(float) * std::max<int64_t>(steps, 1)));
+    TRY(sync_all(m));
     CK(cudaEventRecord(e0, m->stream));
     for (int64_t s = 0; s < steps; ++s) {
-        TRY(begin_step_from_perm(m, epoch, s));
-        TRY(run_body(m));
-        CK(cudaMemcpyAsync(pinned + s, &m->st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
+        TRY(step_from_perm(m, epoch, s));
+        CK(cudaMemcpyAsync(pinned + s, &m->bs[m->last].st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
     }
     CK(cudaEventRecord(e1, m->stream));
     CK(cudaEventSynchronize(e1));
@@ -940,7 +1086,7 @@ gnn_status gnn_train_epoch(gnn_model* m, int64_t epoch, gnn_epoch_stats* out_hos
 gnn_status gnn_synchronize(gnn_model* m) {
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
     TRY(set_device(m->g->dev));
-    CK(cudaStreamSynchronize(m->stream));
+    TRY(sync_all(m));
     return GNN_OK;
 }
 
@@ -948,8 +1094,7 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
     if (!m || !out_host) return fail(GNN_ERR_PARAM, "NULL argument");
     TRY(set_device(m->g->dev));
     StepState st;
-    CK(cudaMemcpyAsync(&st, m->st, sizeof(StepState), cudaMemcpyDeviceToHost, m->stream));
-    CK(cudaStreamSynchronize(m->stream));
+    TRY(copy_state(m, shown_set(m), &st));
     if (what == GNN_DBG_LOSS) {
         if (n < 1) return fail(GNN_ERR_BUFFER, "need 1");
         out_host[0] = st.loss;
@@ -969,7 +1114,7 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
                             st.batch_n, cudaMemcpyDeviceToHost));
         return GNN_OK;
     }
-    if (what == GNN_DBG_PHASES) {   // sampling-kernel phase durations of the last step (us)
+    if (what == GNN_DBG_PHASES) {   // sampling-kernel phase durations of the last sampling run (us)
         GridBarrier hb{};
         CK(cudaMemcpy(&hb, m->bar, sizeof(GridBarrier), cudaMemcpyDeviceToHost));
         const int nb = 2 * m->hops + 3 + (m->shadow ? 1 : 0);
@@ -1000,8 +1145,7 @@ gnn_status gnn_last_sizes(gnn_model* m, gnn_batch_sizes* sizes_host) {
     if (!m || !sizes_host) return fail(GNN_ERR_PARAM, "NULL argument");
     TRY(set_device(m->g->dev));
     StepState st;
-    CK(cudaMemcpyAsync(&st, m->st, sizeof(StepState), cudaMemcpyDeviceToHost, m->stream));
-    CK(cudaStreamSynchronize(m->stream));
+    TRY(copy_state(m, shown_set(m), &st));
     sizes_host->num_hops = m->hops;
     for (int h = 0; h <= kMaxHops; ++h) {
         sizes_host->n_dst[h] = st.n_dst[h];
@@ -1013,6 +1157,9 @@ gnn_status gnn_last_sizes(gnn_model* m, gnn_batch_sizes* sizes_host) {
 
 gnn_status gnn_profile_enable(gnn_model* m, int32_t enable) {
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    TRY(set_device(m->g->dev));
+    TRY(sync_all(m));
+    for (auto& B : m->bs) B.valid = false;   // instrumented steps sample and train serially
     m->profiling = enable != 0;
     return GNN_OK;
 }
@@ -1020,6 +1167,7 @@ gnn_status gnn_profile_enable(gnn_model* m, int32_t enable) {
 gnn_status gnn_profile_read(gnn_model* m, int32_t kid, double* ms_out_host, int64_t* launches_out_host) {
     if (!m || kid < 0 || kid >= GNN_K_COUNT) return fail(GNN_ERR_PARAM, "bad arguments");
     TRY(set_device(m->g->dev));
+    TRY(sync_all(m));
     drain_profile(m);
     if (ms_out_host) *ms_out_host = m->prof_ms[kid];
     if (launches_out_host) *launches_out_host = m->prof_n[kid];
@@ -1028,6 +1176,7 @@ gnn_status gnn_profile_read(gnn_model* m, int32_t kid, double* ms_out_host, int6
 
 gnn_status gnn_profile_reset(gnn_model* m) {
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    TRY(sync_all(m));
     drain_profile(m);
     for (int i = 0; i < GNN_K_COUNT; ++i) { m->prof_ms[i] = 0; m->prof_n[i] = 0; }
     return GNN_OK;

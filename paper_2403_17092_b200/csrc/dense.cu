@@ -62,6 +62,11 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, i * lda + 4 * ch, kZero4);
             continue;
         }
+        // the self row does not depend on the edge chain: issue its loads first
+        const float4* ps = reinterpret_cast<const float4*>(H.row(smap ? smap[i] : i, in_pad));
+        float4 sv[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) sv[c] = (lane + 32 * c) < nch ? __ldg(ps + lane + 32 * c) : kZero4;
         const int beg = rowptr[i], end = rowptr[i + 1];
         float4 acc[CPL];
 #pragma unroll
@@ -96,13 +101,11 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             }
         }
         const int deg = end - beg;
-        const int self = smap ? smap[i] : i;
-        const float4* ps = reinterpret_cast<const float4*>(H.row(self, in_pad));
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
             if (ch < nch) {
-                store_split4(A, i * lda + 4 * ch, __ldg(ps + ch));
+                store_split4(A, i * lda + 4 * ch, sv[c]);
                 store_split4(A, i * lda + 4 * (nch + ch), deg ? f4div(acc[c], (float)deg) : kZero4);
             }
         }
@@ -186,6 +189,16 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
             for (int ch = lane; ch < nch; ch += 32) store_split4(dPre, (int64_t)u * in_pad + 4 * ch, kZero4);
             continue;
         }
+        // rows that do not depend on the edge chain: issue their loads first
+        const float4* hp = reinterpret_cast<const float4*>(Hprev + (int64_t)u * in_pad);
+        const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
+        float4 hv[CPL], sv[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            hv[c] = ch < nch ? __ldg(hp + ch) : kZero4;
+            sv[c] = (ch < nch && u < dlim) ? __ldg(sp + ch) : kZero4;
+        }
         const int beg = trowptr[u], end = trowptr[u + 1];
         const float dout = (float)(end - beg + (u < ndst ? 1 : 0));
         float4 acc[CPL];
@@ -215,8 +228,6 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
                 }
             }
         }
-        const float4* hp = reinterpret_cast<const float4*>(Hprev + (int64_t)u * in_pad);
-        const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
         float wself = 0.f;
         if (GCN && u < dlim) {
             const float din = (float)(rowptr[u + 1] - rowptr[u] + 1);
@@ -227,10 +238,10 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
             const int ch = lane + 32 * c;
             if (ch < nch) {
                 float4 a = acc[c];
-                if (u < dlim) a = GCN ? f4fma(wself, __ldg(sp + ch), a) : f4add(a, __ldg(sp + ch));
-                const float4 hv = __ldg(hp + ch);   // ReLU'(pre) = [H > 0]  (ReLU'(0) = 0)
-                a.x = hv.x > 0.f ? a.x : 0.f; a.y = hv.y > 0.f ? a.y : 0.f;
-                a.z = hv.z > 0.f ? a.z : 0.f; a.w = hv.w > 0.f ? a.w : 0.f;
+                if (u < dlim) a = GCN ? f4fma(wself, sv[c], a) : f4add(a, sv[c]);
+                // ReLU'(pre) = [H > 0]  (ReLU'(0) = 0)
+                a.x = hv[c].x > 0.f ? a.x : 0.f; a.y = hv[c].y > 0.f ? a.y : 0.f;
+                a.z = hv[c].z > 0.f ? a.z : 0.f; a.w = hv[c].w > 0.f ? a.w : 0.f;
                 store_split4(dPre, (int64_t)u * in_pad + 4 * ch, a);
             }
         }
@@ -312,7 +323,7 @@ __global__ void __launch_bounds__(256) k_ce(StepState* st, const float* __restri
         }
         if (lane == 0) row_loss[r] = (m + logf(s)) - z[y];
     }
-    __threadfence();
+    if (lane == 0) __threadfence();   // only the row_loss writers need to publish
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
     __syncthreads();

@@ -17,7 +17,8 @@ void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t ep
                       uint64_t* keys, cudaStream_t s);
 // Start of a step: state fields, seeds -> nodes[0:n), map[seed] = i.
 void launch_begin_step(StepState* st, const int32_t* seed_src, int32_t n, int32_t b_total,
-                       uint32_t epoch, uint32_t g, int32_t* nodes, int32_t* map, cudaStream_t s);
+                       uint32_t epoch, uint32_t g, int32_t* nodes, int32_t* map, uint32_t* seq,
+                       cudaStream_t s);
 
 struct GridBarrier {
     unsigned count, gen;

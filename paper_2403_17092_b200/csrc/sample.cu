@@ -17,7 +17,7 @@ __global__ void k_perm_keys(const int32_t* train, int64_t n, uint64_t seed, uint
 
 // dst_0 = seeds (batch order): nodes[i] = seed_i, map[seed_i] = i; reset the step's sizes.
 __global__ void k_begin_step(StepState* st, const int32_t* seed_src, int32_t n, int32_t b_total, uint32_t epoch,
-                             uint32_t g, int32_t* nodes, int32_t* map) {
+                             uint32_t g, int32_t* nodes, int32_t* map, uint32_t* seq) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int v = seed_src[i];
         nodes[i] = v;
@@ -31,7 +31,7 @@ __global__ void k_begin_step(StepState* st, const int32_t* seed_src, int32_t n, 
         st->epoch = epoch;
         st->g = g;
         st->loss = 0.f;
-        st->seq = st->seq + 1u;
+        st->seq = ++*seq;     // unique across both batch sets (the scan words are shared)
     }
 }
 
@@ -44,8 +44,8 @@ void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t ep
 }
 
 void launch_begin_step(StepState* st, const int32_t* seed_src, int32_t n, int32_t b_total, uint32_t epoch,
-                       uint32_t g, int32_t* nodes, int32_t* map, cudaStream_t s) {
-    k_begin_step<<<1, 1024, 0, s>>>(st, seed_src, n, b_total, epoch, g, nodes, map);
+                       uint32_t g, int32_t* nodes, int32_t* map, uint32_t* seq, cudaStream_t s) {
+    k_begin_step<<<1, 1024, 0, s>>>(st, seed_src, n, b_total, epoch, g, nodes, map, seq);
 }
 
 }  // namespace gs

@@ -67,7 +67,8 @@ def lib():
             "gnn_epoch_permutation": ([P, I64, P, I64], I32),
             "gnn_sample": ([P, I64, I64, P], I32), "gnn_sample_fetch": ([P, I32, I32, P, I64], I32),
             "gnn_train_minibatch": ([P, I64, I64, P], I32),
-            "gnn_train_batch_host": ([P, P, I32, I32, I64, I64, P], I32),
+            "gnn_train_batch_host": ([P, P, I32, I32, I64, I64, P, I32, I32, I64, P], I32),
+            "gnn_set_overlap": ([P, I32], I32),
             "gnn_train_epoch": ([P, I64, P], I32), "gnn_synchronize": ([P], I32),
             "gnn_debug_get": ([P, I32, P, I64], I32), "gnn_last_sizes": ([P, P], I32),
             "gnn_profile_enable": ([P, I32], I32), "gnn_profile_read": ([P, I32, P, P], I32),
@@ -231,19 +232,29 @@ class Model:
         _check(lib().gnn_train_minibatch(self.h, epoch, step, C.byref(loss)))
         return loss.value
 
-    def train_batch_host(self, seeds: np.ndarray, b_total: int, epoch: int, g: int) -> float:
-        """End-to-end call: host seeds -> device, one step, loss -> host (synchronous)."""
+    def train_batch_host(self, seeds: np.ndarray, b_total: int, epoch: int, g: int, next_seeds=None,
+                         next_b_total: int = 0, next_g: int = -1) -> float:
+        """End-to-end call: host seeds -> device, one step, loss -> host (synchronous).  With
+        next_g >= 0 the next call's batch (next_seeds, next_b_total, next_g) is sampled while
+        this one trains."""
         seeds = np.ascontiguousarray(seeds, dtype=np.int32)
+        nxt = np.ascontiguousarray(next_seeds if next_seeds is not None else np.zeros(0), dtype=np.int32)
         loss = C.c_float()
         _check(lib().gnn_train_batch_host(self.h, _ptr(seeds), seeds.shape[0], b_total, epoch, g,
-                                          C.byref(loss)))
+                                          _ptr(nxt), nxt.shape[0], next_b_total, next_g, C.byref(loss)))
         return loss.value
 
     def train_batch_host_ptr(self, seeds_ptr: int, n: int, b_total: int, epoch: int, g: int,
-                             loss_ptr: int):
-        """Same as train_batch_host with raw (pinned) host pointers; no numpy copies."""
+                             loss_ptr: int, next_ptr: int = 0, next_n: int = 0, next_b_total: int = 0,
+                             next_g: int = -1):
+        """Same as train_batch_host with raw host pointers; no numpy copies."""
         _check(lib().gnn_train_batch_host(self.h, C.c_void_p(seeds_ptr), n, b_total, epoch, g,
-                                          C.c_void_p(loss_ptr)))
+                                          C.c_void_p(next_ptr) if next_ptr else None, next_n, next_b_total,
+                                          next_g, C.c_void_p(loss_ptr)))
+
+    def set_overlap(self, enable: bool):
+        """gnn_set_overlap: sample step s+1 while step s trains (default on)."""
+        _check(lib().gnn_set_overlap(self.h, 1 if enable else 0))
 
     def train_epoch(self, epoch: int):
         st = _EpochStats()

@@ -66,6 +66,41 @@ def test_tiny_e2e_host_call_equals_device_call():
     assert np.array_equal(m1.get_params(), m2.get_params())
 
 
+def test_tiny_overlap_is_invisible():
+    """Sampling step s+1 on the sampling stream while step s trains (two batch sets) gives
+    bit-identical results to sample-then-train, also when the caller interleaves parity
+    samples, jumps steps, or changes epoch mid-way."""
+    w, inp, graph = inputs_for("tiny")
+    schedule = [(0, s) for s in range(6)] + [(0, 9), (0, 10), (1, 0), (1, 1), (0, 3)]
+    runs = []
+    for overlap in (False, True):
+        g, m = make_gpu(w, inp)
+        m.set_overlap(overlap)
+        losses = []
+        for i, (e, s) in enumerate(schedule):
+            losses.append(m.train_minibatch(e, s))
+            if i == 3:
+                m.sample(0, 5)              # parity hook between steps clobbers a set
+        runs.append((np.array(losses), m.grads(), m.get_params()))
+        m.close(); g.close()
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)
+
+
+def test_tiny_e2e_prefetch_equals_plain():
+    w, inp, graph = inputs_for("tiny")
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    seeds = [OS.batch_seeds(perm, w.batch_size, s) for s in range(5)]
+    g1, m1 = make_gpu(w, inp)
+    g2, m2 = make_gpu(w, inp)
+    for s in range(5):
+        l1 = m1.train_batch_host(seeds[s], len(seeds[s]), 0, s)
+        nxt = dict(next_seeds=seeds[s + 1], next_b_total=len(seeds[s + 1]), next_g=s + 1) if s < 4 else {}
+        l2 = m2.train_batch_host(seeds[s], len(seeds[s]), 0, s, **nxt)
+        assert l1 == l2
+    assert np.array_equal(m1.get_params(), m2.get_params())
+
+
 def test_tiny_virtual_ranks_inactive_rank_and_ragged_step():
     """A rank with no batch (g >= n_batches) contributes zero gradient; b_total counts only
     the active seeds (reading R8/R9).  Emulated on one GPU through the e2e call."""
