@@ -789,6 +789,10 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         ok &= make_tmap_bf16(&ly.map_wgrad.a_lo, lo_or_hi(ly.A), ly.rows_alloc, ly.k_pad, 64);
         ok &= make_tmap_bf16(&ly.map_wgrad.b_hi, ly.dPre.hi, ly.rows_alloc, ly.n_pad, 64);
         ok &= make_tmap_bf16(&ly.map_wgrad.b_lo, lo_or_hi(ly.dPre), ly.rows_alloc, ly.n_pad, 64);
+        ok &= make_tmap_f32(&ly.map_fwd.c, ly.H, ly.m_cap, ly.n_pad, ly.n_pad, 1, 0);
+        ok &= make_tmap_f32(&ly.map_wgrad.c, ly.wpart, ly.k_pad, ly.n_pad, ly.n_pad, ly.splits,
+                            (int64_t)ly.k_pad * ly.n_pad);
+        if (li > 0) ok &= make_tmap_f32(&ly.map_dgrad.c, ly.dA, ly.m_cap, ly.k_pad, ly.k_pad, 1, 0);
         if (!ok) return cleanup(fail(GNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(li)));
     }
     AL(m->params, m->pcount);

@@ -76,6 +76,25 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             int myidx = 0;
             if (lane < m) { const int c = col[e0 + lane]; myidx = gmap ? gmap[c] : c; }
             int q = 0;
+            // kAggU neighbour rows in flight per warp (memory-level parallelism of the gather);
+            // the adds stay in CSR order
+            constexpr int kAggU = CPL == 1 ? 4 : 2;
+            for (; q + kAggU <= m; q += kAggU) {
+                float4 v[kAggU][CPL];
+#pragma unroll
+                for (int u = 0; u < kAggU; ++u) {
+                    const float4* pu = reinterpret_cast<const float4*>(H.row(__shfl_sync(kFull, myidx, q + u), in_pad));
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        const int ch = lane + 32 * c;
+                        v[u][c] = ch < nch ? __ldg(pu + ch) : kZero4;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kAggU; ++u)
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) acc[c] = f4add(acc[c], v[u][c]);
+            }
             for (; q + 2 <= m; q += 2) {
                 const int r0 = __shfl_sync(kFull, myidx, q), r1 = __shfl_sync(kFull, myidx, q + 1);
                 const float4* p0 = reinterpret_cast<const float4*>(H.row(r0, in_pad));
@@ -171,6 +190,9 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
 // ------------------------------------------------------------------ backward aggregation
 // dA rows >= dlim are not computed (ShaDow last layer: only the seeds' rows carry loss,
 // the exact receptive-field pruning of DESIGN.md R19) and contribute nothing.
+// Software-pipelined over the warp's rows u, u+W, u+2W, ...: the next row's transposed-CSR
+// range and its first 32 destinations are loaded while the current row's dA rows are in flight,
+// so a row costs about one dependent memory round trip instead of three.
 template <int CPL, bool GCN>
 __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __restrict__ st,
         const int32_t* __restrict__ dlim_ptr, const float* __restrict__ dA, int in_pad,
@@ -184,12 +206,21 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
     const int nch = in_pad >> 2;
     const int64_t lda = GCN ? in_pad : 2 * (int64_t)in_pad;
     const int moff = GCN ? 0 : nch;   // dM half of [dSelf | dM]
-    for (int u = global_warp(); u < nr; u += total_warps()) {
+    const int W = total_warps();
+    int u = global_warp();
+    // prologue: row u's edge range and first chunk of destinations
+    int cb = 0, ce = 0, ci = -1;
+    if (u < nsrc) { cb = trowptr[u]; ce = trowptr[u + 1]; }
+    if (lane < ce - cb) ci = tdst[cb + lane];
+    for (; u < nr; u += W) {
         if (u >= nsrc) {
             for (int ch = lane; ch < nch; ch += 32) store_split4(dPre, (int64_t)u * in_pad + 4 * ch, kZero4);
             continue;
         }
-        // rows that do not depend on the edge chain: issue their loads first
+        const int un = u + W;
+        int nb = 0, ne = 0;
+        if (un < nsrc) { nb = trowptr[un]; ne = trowptr[un + 1]; }
+        // rows that do not depend on the edge chain
         const float4* hp = reinterpret_cast<const float4*>(Hprev + (int64_t)u * in_pad);
         const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
         float4 hv[CPL], sv[CPL];
@@ -199,35 +230,58 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
             hv[c] = ch < nch ? __ldg(hp + ch) : kZero4;
             sv[c] = (ch < nch && u < dlim) ? __ldg(sp + ch) : kZero4;
         }
-        const int beg = trowptr[u], end = trowptr[u + 1];
-        const float dout = (float)(end - beg + (u < ndst ? 1 : 0));
+        const float dout = (float)(ce - cb + (u < ndst ? 1 : 0));
         float4 acc[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
-        for (int e0 = beg; e0 < end; e0 += 32) {
-            const int m = min(32, end - e0);
+        for (int e0 = cb; e0 < ce; e0 += 32) {
+            const int m = min(32, ce - e0);
+            const int t = e0 == cb ? ci : (lane < m ? tdst[e0 + lane] : -1);
             int myi = -1;
             float myd = 1.f;
-            if (lane < m && tdst[e0 + lane] < dlim) {
-                myi = tdst[e0 + lane];
-                const float din = (float)(rowptr[myi + 1] - rowptr[myi] + (GCN ? 1 : 0));
+            if (lane < m && t < dlim) {
+                myi = t;
+                const float din = (float)(rowptr[t + 1] - rowptr[t] + (GCN ? 1 : 0));
                 myd = GCN ? 1.0f / sqrtf(din * dout) : din;
             }
-            for (int q = 0; q < m; ++q) {
-                const int i = __shfl_sync(kFull, myi, q);
-                const float d = __shfl_sync(kFull, myd, q);
-                if (i < 0) continue;
-                const float4* p = reinterpret_cast<const float4*>(dA + (int64_t)i * lda) + moff;
+            int q = 0;
+            for (; q + 2 <= m; q += 2) {   // two dA rows in flight; accumulation in edge order
+                const int i0 = __shfl_sync(kFull, myi, q), i1 = __shfl_sync(kFull, myi, q + 1);
+                const float d0 = __shfl_sync(kFull, myd, q), d1 = __shfl_sync(kFull, myd, q + 1);
+                const float4* p0 = reinterpret_cast<const float4*>(dA + (int64_t)max(i0, 0) * lda) + moff;
+                const float4* p1 = reinterpret_cast<const float4*>(dA + (int64_t)max(i1, 0) * lda) + moff;
+                float4 v0[CPL], v1[CPL];
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
-                    if (ch < nch) {
-                        const float4 v = __ldg(p + ch);
-                        acc[c] = GCN ? f4fma(d, v, acc[c]) : f4add(acc[c], f4div(v, d));
+                    v0[c] = (ch < nch && i0 >= 0) ? __ldg(p0 + ch) : kZero4;
+                    v1[c] = (ch < nch && i1 >= 0) ? __ldg(p1 + ch) : kZero4;
+                }
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    if (i0 >= 0) acc[c] = GCN ? f4fma(d0, v0[c], acc[c]) : f4add(acc[c], f4div(v0[c], d0));
+                    if (i1 >= 0) acc[c] = GCN ? f4fma(d1, v1[c], acc[c]) : f4add(acc[c], f4div(v1[c], d1));
+                }
+            }
+            if (q < m) {
+                const int i0 = __shfl_sync(kFull, myi, q);
+                const float d0 = __shfl_sync(kFull, myd, q);
+                if (i0 >= 0) {
+                    const float4* p0 = reinterpret_cast<const float4*>(dA + (int64_t)i0 * lda) + moff;
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        const int ch = lane + 32 * c;
+                        if (ch < nch) {
+                            const float4 v = __ldg(p0 + ch);
+                            acc[c] = GCN ? f4fma(d0, v, acc[c]) : f4add(acc[c], f4div(v, d0));
+                        }
                     }
                 }
             }
         }
+        // next row's first destinations (its range has arrived by now)
+        ci = -1;
+        if (lane < ne - nb) ci = tdst[nb + lane];
         float wself = 0.f;
         if (GCN && u < dlim) {
             const float din = (float)(rowptr[u + 1] - rowptr[u] + 1);
@@ -245,6 +299,8 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
                 store_split4(dPre, (int64_t)u * in_pad + 4 * ch, a);
             }
         }
+        cb = nb;
+        ce = ne;
     }
 }
 

@@ -58,6 +58,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// TMA store of a swizzled shared-memory box (bulk-group completion); C maps are always 3-D.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -102,6 +114,10 @@ struct TileCfg {
     static constexpr int kBBytesK = BN * kBK * 2;                     // K-major: box {64, BN}
     static constexpr int kBBytesMN = ((BN + 63) / 64) * 64 * kBK * 2; // MN-major: boxes {64, 64}
 };
+
+constexpr int kEpiCols = 32;                          // epilogue chunk: 32 fp32 = one 128 B swizzle row
+constexpr int kEpiBuf = 32 * kEpiCols * 4;           // one warp's 32-row chunk (4 KB)
+constexpr int kEpiBytes = 4 * 2 * kEpiBuf;           // 4 epilogue warps x double buffer
 
 struct GemmArgs {
     const int32_t* m_ptr;   // fwd/dgrad: rows of C (dynamic); wgrad: reduction length (dynamic)
@@ -148,7 +164,8 @@ __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t, int M) {
 template <int BN, int STAGES, int TERMS, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
-          const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo, GemmArgs args) {
+          const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
+          const __grid_constant__ CUtensorMap mC, GemmArgs args) {
     using Cfg = TileCfg<BN>;
     constexpr bool A_MN = MODE == 1;          // wgrad: A^T read from row-major A
     constexpr bool B_MN = MODE >= 1;          // wgrad (dPre), fwd mode 2 (W [K x N])
@@ -261,15 +278,19 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
             }
         }
     } else {
-        // ================= epilogue: TMEM -> registers -> fp32 global (+ReLU)
+        // ================= epilogue: TMEM -> registers (+ReLU) -> swizzled smem -> TMA store
+        // Each warp owns one TMEM lane quarter (32 rows of the tile) and moves it out in
+        // 32-column chunks: tcgen05.ld 32x32b.x32 (thread = row), 16-byte smem stores in the
+        // 128B-swizzle pattern (conflict-free), then one bulk tensor store per chunk; rows/columns
+        // outside the tensor map's extent are clipped by the TMA unit.
         const int q = warp & 3;                       // TMEM lane quarter this warp may access
-        int j = 0;
+        uint8_t* ebuf = smem + STAGES * kStageBytes + q * 2 * kEpiBuf;
+        int j = 0, nchunk = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const TileInfo ti = tile_info<MODE>(args, t, M);
-            const int row = ti.tm * kBM + q * 32 + lane;
+            const int row0 = ti.tm * kBM + q * 32;
             const int tile_n = ti.tn * BN;
-            float* Cbase = args.C + (MODE == 1 ? (int64_t)ti.z * args.split_stride : 0);
-            const bool row_ok = MODE == 1 ? row < args.m_static : row < M;
+            const bool rows_ok = MODE == 1 ? row0 < args.m_static : row0 < M;
             const bool has = ti.nkb > 0;
             const int acc = j & 1;
             if (has) {
@@ -277,42 +298,42 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                 tc_fence_after();
             }
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-                uint32_t v[16];
+            for (int c0 = 0; c0 < BN; c0 += kEpiCols, ++nchunk) {
+                uint32_t v[32];
                 if (has) {
                     const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::kAccCols + c0);
                     asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                          "=r"(v[15])
+                          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                         : "r"(taddr));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 } else {
 #pragma unroll
-                    for (int x = 0; x < 16; ++x) v[x] = 0u;
+                    for (int x = 0; x < 32; ++x) v[x] = 0u;
                 }
-                if (row_ok) {
-                    float* crow = Cbase + (int64_t)row * args.ldc + tile_n + c0;
-                    const int lim = args.n_store - tile_n - c0;
-                    if (lim >= 16) {
+                if (!rows_ok) continue;                 // (warp-uniform) nothing of this quarter is stored
+                uint8_t* buf = ebuf + (nchunk & 1) * kEpiBuf;
+                if (lane == 0) bulk_wait_read<1>();     // the store issued from this buffer 2 chunks ago has read it
+                __syncwarp();
+                uint8_t* myrow = buf + lane * 128;
 #pragma unroll
-                        for (int x = 0; x < 16; x += 4) {
-                            float4 f;
-                            f.x = __uint_as_float(v[x]); f.y = __uint_as_float(v[x + 1]);
-                            f.z = __uint_as_float(v[x + 2]); f.w = __uint_as_float(v[x + 3]);
-                            if (args.relu) { f.x = fmaxf(f.x, 0.f); f.y = fmaxf(f.y, 0.f); f.z = fmaxf(f.z, 0.f); f.w = fmaxf(f.w, 0.f); }
-                            *reinterpret_cast<float4*>(crow + x) = f;
-                        }
-                    } else {
-#pragma unroll
-                        for (int x = 0; x < 16; ++x) {
-                            if (x < lim) {
-                                const float f = __uint_as_float(v[x]);
-                                crow[x] = args.relu ? fmaxf(f, 0.f) : f;
-                            }
-                        }
-                    }
+                for (int c = 0; c < 8; ++c) {
+                    float4 f;
+                    f.x = __uint_as_float(v[4 * c]); f.y = __uint_as_float(v[4 * c + 1]);
+                    f.z = __uint_as_float(v[4 * c + 2]); f.w = __uint_as_float(v[4 * c + 3]);
+                    if (args.relu) { f.x = fmaxf(f.x, 0.f); f.y = fmaxf(f.y, 0.f); f.z = fmaxf(f.z, 0.f); f.w = fmaxf(f.w, 0.f); }
+                    *reinterpret_cast<float4*>(myrow + ((c ^ (lane & 7)) << 4)) = f;
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&mC, buf, tile_n + c0, row0, ti.z);
+                    bulk_commit();
                 }
             }
             if (has) {
@@ -322,6 +343,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                 ++j;
             }
         }
+        if (lane == 0) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -362,6 +384,21 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t co
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 [depth x rows x cols] (cols contiguous, row stride ld elements, depth stride dstride
+// elements), box {32, 32, 1}, 128B swizzle: the GEMM epilogue's store target.
+bool make_tmap_f32(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int64_t depth,
+                   int64_t dstride) {
+    EncodeFn fn = encode_fn();
+    if (!fn || !base) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)depth};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)std::max<int64_t>(dstride, rows * ld) * 4};
+    cuuint32_t box[3] = {(cuuint32_t)kEpiCols, 32u, 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box,
+              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 namespace {
 constexpr int kSMs = 148;
 
@@ -369,13 +406,14 @@ template <int BN, int STAGES, int TERMS, int MODE>
 cudaError_t launch_tc(int grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
     using Cfg = TileCfg<BN>;
     constexpr int kAPlanes = TERMS == 3 ? 2 : 1;
-    constexpr int smem = STAGES * kAPlanes * (Cfg::kAStage + Cfg::kBStage) + 1024;
+    constexpr int smem = STAGES * kAPlanes * (Cfg::kAStage + Cfg::kBStage) + kEpiBytes + 1024;
+    static_assert(smem <= 227 * 1024, "shared memory budget");
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, TERMS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_gemm_tc<BN, STAGES, TERMS, MODE><<<grid, kThreads, smem, s>>>(mp.a_hi, mp.a_lo, mp.b_hi, mp.b_lo, a);
+    k_gemm_tc<BN, STAGES, TERMS, MODE><<<grid, kThreads, smem, s>>>(mp.a_hi, mp.a_lo, mp.b_hi, mp.b_lo, mp.c, a);
     return cudaGetLastError();
 }
 

@@ -119,9 +119,13 @@ void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint3
                         cudaStream_t s);
 
 // ------------------------------------------------------------------ tensor-core GEMM (gemm_tc.cu)
-struct TcGemmMaps { CUtensorMap a_hi, a_lo, b_hi, b_lo; };
+struct TcGemmMaps { CUtensorMap a_hi, a_lo, b_hi, b_lo, c; };
 // 2-D bf16 row-major [rows x cols], box {64 cols, box_rows}, 128B swizzle, OOB reads -> 0.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
+// fp32 C of a GEMM: [depth x rows x cols], row stride ld, depth stride dstride (elements); box
+// {32, 32, 1}, 128B swizzle; stores outside [rows x cols] are clipped.
+bool make_tmap_f32(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int64_t depth,
+                   int64_t dstride);
 // N tile the GEMM uses for an output width n_pad (TMA box rows of a K-major B operand).
 int tc_tile_n(int n_pad);
 // mode 0 (dgrad): C[M x n_store] = A[M x k_pad] B^T (B given as [n_pad x k_pad]), M = *m_ptr
