@@ -52,6 +52,8 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
         FeatRows H, int in_pad, const int32_t* __restrict__ gmap,
         const int32_t* __restrict__ smap, const int32_t* __restrict__ rowptr,
         const int32_t* __restrict__ col, Split A) {
+    pdl_trigger();
+    pdl_wait();
     const int n = *rows_ptr;
     const int nr = round64(n);
     const int lane = lane_id();
@@ -139,6 +141,8 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
         const int32_t* __restrict__ gmap, const int32_t* __restrict__ smap,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
         const int32_t* __restrict__ trowptr, Split A) {
+    pdl_trigger();
+    pdl_wait();
     const int n = *rows_ptr;
     const int nr = round64(n);
     const int ndst = *ndst_ptr;
@@ -198,6 +202,8 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
         const int32_t* __restrict__ dlim_ptr, const float* __restrict__ dA, int in_pad,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ trowptr,
         const int32_t* __restrict__ tdst, const float* __restrict__ Hprev, Split dPre) {
+    pdl_trigger();
+    pdl_wait();
     const int nsrc = st->n_src[h];
     const int nr = round64(nsrc);
     const int ndst = st->n_dst[h];
@@ -308,6 +314,8 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
 // dW of every layer in one launch: grads[off_l + r*out + c] = Σ_z part_l[z][rpad(r)*n_pad + c]
 // (split order fixed: deterministic).
 __global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int l = 0; l < P.n; ++l) {
@@ -327,6 +335,8 @@ __global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
 // W [K_pad x N_pad] (coalesced in that order; padding entries stay the zeros written at
 // creation).  Each parameter is visited exactly once.  grads == nullptr: pack only.
 __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, const float* __restrict__ grads, float lr) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int l = 0; l < P.n; ++l) {
@@ -352,6 +362,8 @@ __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, const float* _
 __global__ void __launch_bounds__(256) k_ce(StepState* st, const float* __restrict__ Z, int ldz, int C,
                                             const int32_t* __restrict__ labels, const int32_t* __restrict__ nodes,
                                             Split dZ, float* __restrict__ row_loss, uint32_t* __restrict__ done) {
+    pdl_trigger();
+    pdl_wait();
     using BR = cub::BlockReduce<float, 256>;
     __shared__ typename BR::TempStorage tmp;
     __shared__ bool last;
@@ -408,14 +420,14 @@ int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
 
 #define GS_CPL_DISPATCH(cpl, KERNEL, ...)                                           \
     switch (cpl) {                                                                  \
-        case 1: KERNEL<1><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
-        case 2: KERNEL<2><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
-        case 3: KERNEL<3><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
-        case 4: KERNEL<4><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
-        case 5: KERNEL<5><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
-        case 6: KERNEL<6><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
-        case 7: KERNEL<7><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;            \
-        default: KERNEL<8><<<kWarpGrid, 256, 0, s>>>(__VA_ARGS__); break;           \
+        case 1: launch_pdl(KERNEL<1>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
+        case 2: launch_pdl(KERNEL<2>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
+        case 3: launch_pdl(KERNEL<3>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
+        case 4: launch_pdl(KERNEL<4>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
+        case 5: launch_pdl(KERNEL<5>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
+        case 6: launch_pdl(KERNEL<6>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
+        case 7: launch_pdl(KERNEL<7>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
+        default: launch_pdl(KERNEL<8>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;           \
     }
 
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
@@ -436,10 +448,10 @@ static void spmm_bwd(int h, const StepState* st, const int32_t* dlim, const floa
                      const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
                      const float* H_prev, Split dPre_prev, cudaStream_t s) {
     switch (cpl_of(in_pad)) {
-        case 1: k_spmm_bwd<1, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
-        case 2: k_spmm_bwd<2, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
-        case 3: k_spmm_bwd<3, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
-        default: k_spmm_bwd<4, GCN><<<kWarpGrid, 256, 0, s>>>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+        case 1: launch_pdl(k_spmm_bwd<1, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+        case 2: launch_pdl(k_spmm_bwd<2, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+        case 3: launch_pdl(k_spmm_bwd<3, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+        default: launch_pdl(k_spmm_bwd<4, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
     }
 }
 
@@ -451,16 +463,16 @@ void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, 
 }
 
 void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s) {
-    k_wgrad_reduce_all<<<148 * 4, 256, 0, s>>>(p, grads);
+    launch_pdl(k_wgrad_reduce_all, 148 * 4, 256, 0, s, p, grads);
 }
 
 void launch_sgd_pack(const PackAll& p, float* params, const float* grads, float lr, cudaStream_t s) {
-    k_sgd_pack<<<148 * 2, 256, 0, s>>>(p, params, grads, lr);
+    launch_pdl(k_sgd_pack, 148 * 2, 256, 0, s, p, params, grads, lr);
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,
                Split dZ, cudaStream_t s) {
-    k_ce<<<128, 256, 0, s>>>(st, Z, ldz, C, labels, nodes, dZ, st->row_loss, &st->ce_done);
+    launch_pdl(k_ce, 128, 256, 0, s, st, Z, ldz, C, labels, nodes, dZ, st->row_loss, &st->ce_done);
 }
 
 void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer, cudaStream_t s) {

@@ -177,11 +177,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int M = *args.m_ptr;
-    const int ntiles = MODE != 1 ? ((M + kBM - 1) / kBM) * args.n_tiles
-                                 : ((args.m_static + kBM - 1) / kBM) * args.n_tiles * args.splits;
-    if ((int)blockIdx.x >= ntiles) return;
-
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        for (const CUtensorMap* mp : {&mA_hi, &mA_lo, &mB_hi, &mB_lo, &mC})
+            asm volatile("prefetch.tensormap [%0];" ::"l"(mp) : "memory");
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
@@ -197,6 +197,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
+    // everything above is independent of the predecessor kernel (programmatic launch)
+    pdl_wait();
+    const int M = *args.m_ptr;
+    const int ntiles = MODE != 1 ? ((M + kBM - 1) / kBM) * args.n_tiles
+                                 : ((args.m_static + kBM - 1) / kBM) * args.n_tiles * args.splits;
 
     if (warp == 0) {
         // ================= TMA producer
@@ -413,8 +418,8 @@ cudaError_t launch_tc(int grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStr
         cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, TERMS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_gemm_tc<BN, STAGES, TERMS, MODE><<<grid, kThreads, smem, s>>>(mp.a_hi, mp.a_lo, mp.b_hi, mp.b_lo, mp.c, a);
-    return cudaGetLastError();
+    return launch_pdl(k_gemm_tc<BN, STAGES, TERMS, MODE>, grid, kThreads, smem, s, mp.a_hi, mp.a_lo, mp.b_hi,
+                      mp.b_lo, mp.c, a);
 }
 
 template <int TERMS, int MODE>

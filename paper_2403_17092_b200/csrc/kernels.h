@@ -5,9 +5,36 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace gs {
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Training-stream kernels are launched with programmatic stream serialization: a kernel's CTAs
+// may be scheduled while its predecessor drains (they trigger their dependents on entry), and
+// every kernel calls pdl_wait() before its first global-memory access, which waits for the
+// predecessor grid's completion and memory flush.  Only prologue work that touches no global
+// memory (barrier init, TMEM allocation, descriptor prefetch) precedes pdl_wait().
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------ sampling side (sample.cu, sample_step.cu)
 constexpr int kWarpGrid = 148 * 16;          // blocks of 256 threads for warp-per-item kernels
