@@ -55,6 +55,19 @@ WORKLOADS = {
     # configs[3]: Reddit-shaped, high-degree stress
     "reddit": Workload("reddit", 232_965, 114_615_892, 602, 41, "sage", "neighbor",
                        (25, 10), 2, 256, 1024, 153_431),
+    # the rest of the paper's model x sampler grid (Table 3,
+    # lines 478-493) and its ShaDow depth setting (L' = 3 hops, L = 5 layers)
+    "tiny_gcn": Workload("tiny_gcn", 10_000, 100_000, 32, 8, "gcn", "neighbor", (10, 5), 2, 32, 64, 10_000),
+    "tiny_sage_shadow": Workload("tiny_sage_shadow", 10_000, 100_000, 32, 8, "sage", "shadow", (10, 5), 2, 32,
+                                 64, 10_000),
+    "tiny_shadow_l5": Workload("tiny_shadow_l5", 10_000, 100_000, 32, 8, "gcn", "shadow", (10, 5), 5, 32, 64,
+                               10_000),
+    "products_gcn": Workload("products_gcn", 2_449_029, 61_859_140, 100, 47, "gcn", "neighbor",
+                             (15, 10, 5), 3, 256, 1024, 196_615),
+    "products_sage_shadow": Workload("products_sage_shadow", 2_449_029, 61_859_140, 100, 47, "sage", "shadow",
+                                     (15, 10, 5), 3, 256, 1024, 196_615),
+    "products_shadow_l5": Workload("products_shadow_l5", 2_449_029, 61_859_140, 100, 47, "gcn", "shadow",
+                                   (15, 10, 5), 5, 256, 1024, 196_615),
     # configs[4]: papers100M-shaped (row-sharded features across ranks)
     "papers100m": Workload("papers100m", 111_059_956, 1_615_685_872, 128, 172, "sage", "neighbor",
                            (15, 10, 5), 3, 256, 1024, 1_207_179),

@@ -15,10 +15,14 @@ CASES = {
     "products": dict(batches=(0, 1, 96, 192), steps=3),
     "reddit": dict(batches=(0, 1, 75, 149), steps=2),
     "products_shadow": dict(batches=(0, 192), steps=1),
+    # SURVEY.md §8(f) NEXT-1 grid: same samplers as above (their sampling is covered there)
+    "products_gcn": dict(batches=(), steps=1),
+    "products_sage_shadow": dict(batches=(), steps=1),
+    "products_shadow_l5": dict(batches=(), steps=1),
 }
 
 
-@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("name", [n for n in CASES if CASES[n]["batches"]])
 def test_fullsize_sampling_bitexact(name):
     w, inp, graph = inputs_for(name)
     g, m = make_gpu(w, inp)

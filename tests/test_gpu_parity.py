@@ -151,3 +151,29 @@ def test_epoch_permutation_bitexact():
     g, m = make_gpu(w, inp)
     for epoch in (0, 1, 7):
         assert np.array_equal(m.epoch_permutation(epoch), OS.epoch_perm(graph["train"], w.sampler_seed, epoch))
+
+
+# ---------------------------------------------------------------- the rest of the model x sampler grid
+# (Table 3: GCN and SAGE under both samplers, and
+# the ShaDow depth setting L = 5 layers on L' = 2 hops)
+@pytest.mark.parametrize("name", ["tiny_gcn", "tiny_sage_shadow", "tiny_shadow_l5"])
+def test_grid_sampling_and_training_parity(name):
+    w, inp, graph = inputs_for(name)
+    g, m = make_gpu(w, inp)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    for b in (0, 1, w.n_batches - 1):
+        want, _ = oracle.sample_batch(w, graph, 0, b, perm)
+        got = m.sample(0, b)
+        if w.sampler == "shadow":
+            assert_blocks_equal(got[0], want[0])
+            assert_blocks_equal([got[1]], [want[1]])
+        else:
+            assert_blocks_equal(got, want)
+    params = inp["params"].astype(np.float64)
+    for step in list(range(12)) + [w.n_batches - 1]:
+        if step == w.n_batches - 1:
+            m.set_params(params)          # ragged last batch from the oracle's current params
+        loss = m.train_minibatch(0, step)
+        out = check_train_step(m, w, graph, params, 0, step, perm, loss)
+        params = out["params"]
+        assert rel(m.get_params(), params) <= TOL_FP32
