@@ -36,6 +36,7 @@ def parse():
     p.add_argument("--config", default="products")
     p.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--no-overlap", action="store_true", help="sample each step before training it")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -236,6 +237,7 @@ def main():
               use_graph=not args.no_graph, lr=w.lr, seed=w.sampler_seed, init_seed=w.init_seed)
     m.set_train_nodes(inp["train"])
     m.set_params(inp["params"])
+    m.set_overlap(not args.no_overlap)
     if world > 1:
         obj = [comm_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -333,16 +335,22 @@ def main():
     # ---- instrumented pass (per-kernel CUDA events on the library's stream, eager launches)
     m.profile_enable(True)
     m.profile_reset()
-    sizes = []
     for i in range(args.warmup, args.warmup + args.steps):
         e, s = step_at(i)
         m.train_minibatch(e, s, sync=False)
-        sizes.append(m.last_sizes())
     barrier()
     prof = {k: m.profile_read(k) for k in ["sample", "relabel", "scan", "transpose", "induce", "agg_l1",
                                            "agg", "gemm_fwd", "gemm_dgrad", "gemm_wgrad", "spmm_bwd",
                                            "ce", "allreduce", "sgd", "other"]}
     m.profile_enable(False)
+    # per-batch sizes of the timed batches (the sampling API's full relabel: the training path
+    # of SAGE skips the last hop's unique-node list, which the algorithmic-byte model needs)
+    sizes = []
+    for i in range(args.warmup, args.warmup + args.steps):
+        e, s = step_at(i)
+        if s * world + rank < w.n_batches:
+            sizes.append(m.sample_sizes(e, s * world + rank))
+    barrier()
     tot_ms = sum(v[0] for v in prof.values())
     hbm, bf16, bf16_sus, peak_kind = load_peaks()
     terms = 3 if args.precision == "fp32" else 1

@@ -144,7 +144,9 @@ struct gnn_model {
     int last = -1;                       // set trained last
     int fetch_set = 0;                   // set gnn_sample filled
     int32_t *map = nullptr, *icount = nullptr;
-    uint32_t* seq = nullptr;             // step sequence counter (scan-word tags)
+    uint32_t seq = 0;                    // sampling-launch sequence number (scan-word tags)
+    bool full_train = true;              // training needs the last hop's relabel (GCN, ShaDow)
+    bool last_full = true;               // mode of the last sampling launch (phase readout)
     unsigned long long* status = nullptr;
     GridBarrier* bar = nullptr;
     uint32_t* bits = nullptr;
@@ -263,15 +265,23 @@ void enqueue_training(gnn_model* m, int set) {
                                B.rowptr[blk], B.col[blk], B.trowptr[blk], ly.A, s);
             });
         }
+        if (li == L - 1 && ly.n_pad <= 64) {
+            // logits = A W with the softmax cross-entropy in the GEMM epilogue
+            K(m, s, GNN_K_GEMM_FWD, [&] {
+                launch_gemm_tc_ce(m->bf16x3, ly.map_fwd, rows, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, B.st, g->C,
+                                  g->y, B.nodes, ly.dPre, s);
+            });
+            break;
+        }
         // Pre = A W (+ReLU) -> H (fp32)
         K(m, s, GNN_K_GEMM_FWD, [&] {
             launch_gemm_tc(2, m->bf16x3, ly.map_fwd, rows, 0, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, ly.n_pad,
                            ly.n_pad, li < L - 1, 1, 0, s);
         });
+        if (li == L - 1) {   // ---- loss (wide logits rows: separate kernel)
+            K(m, s, GNN_K_CE, [&] { launch_ce(B.st, ly.H, ly.n_pad, g->C, g->y, B.nodes, ly.dPre, s); });
+        }
     }
-    // ---- loss
-    Layer& last = m->layers[L - 1];
-    K(m, s, GNN_K_CE, [&] { launch_ce(B.st, last.H, last.n_pad, g->C, g->y, B.nodes, last.dPre, s); });
     // ---- backward
     for (int li = L - 1; li >= 0; --li) {
         Layer& ly = m->layers[li];
@@ -295,14 +305,17 @@ void enqueue_training(gnn_model* m, int set) {
                             prev.H, prev.dPre, s);
         });
     }
-    // ---- split-K partials of every layer -> flat gradient (fixed order)
-    K(m, s, GNN_K_GEMM_WGRAD, [&] { launch_wgrad_reduce_all(pack_desc(m), m->grads, s); });
-    // ---- exchange + update
-    if (m->world > 1)
+    if (m->world > 1) {
+        // ---- split-K partials of every layer -> flat gradient (fixed order), exchange, update
+        K(m, s, GNN_K_GEMM_WGRAD, [&] { launch_wgrad_reduce_all(pack_desc(m), m->grads, s); });
         K(m, s, GNN_K_ALLREDUCE, [&] {
             ncclAllReduce(m->grads, m->grads, (size_t)m->pcount, ncclFloat, ncclSum, m->comm, s);
         });
-    K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, s); });
+        K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, false, s); });
+    } else {
+        // ---- one rank: the reduce of the partials is fused into the update
+        K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, true, s); });
+    }
 }
 
 // Capture the training body of batch set `set` once.  With profiling on, the capture also
@@ -331,7 +344,7 @@ gnn_status build_graph(gnn_model* m, int set, bool prof) {
         cudaGraphNodeGetType(nd, &t);
         if (t == cudaGraphNodeTypeKernel) ++kernels;
     }
-    if (!prof) m->launches_per_step = kernels + 2;   // + k_begin_step + k_sample_step (sampling stream)
+    if (!prof) m->launches_per_step = kernels + 1;   // + k_sample_step (sampling stream)
     CK(cudaGraphInstantiate(target, graph, 0));
     CK(cudaGraphDestroy(graph));
     return GNN_OK;
@@ -390,7 +403,7 @@ void plan_step(int64_t n_train, int64_t B, int64_t world, int64_t rank, int64_t 
 // Sample a batch into set `set` on the sampling stream (after the set's previous training).
 // seeds_dev: device seed list (the epoch permutation slice) or nullptr with seeds_host.
 gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const int32_t* seeds_host, int32_t n,
-                        int32_t b_total, int64_t epoch, int64_t g) {
+                        int32_t b_total, int64_t epoch, int64_t g, bool full) {
     BatchSet& B = m->bs[set];
     if (B.trained_once) CK(cudaStreamWaitEvent(m->sstream, B.trained, 0));
     const int32_t* src = seeds_dev;
@@ -402,8 +415,17 @@ gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const i
         }
         src = B.seeds_in;
     }
-    launch_begin_step(B.st, src, n, b_total, (uint32_t)epoch, (uint32_t)g, B.nodes, m->map, m->seq, m->sstream);
-    K(m, m->sstream, GNN_K_SAMPLE, [&] { launch_sample_step(B.sp, m->sstream); });
+    SampleParams sp = B.sp;
+    sp.seed_src = src;
+    sp.n_seeds = n;
+    sp.b_total = b_total;
+    sp.epoch = (uint32_t)epoch;
+    sp.g = (uint32_t)g;
+    if (++m->seq == 0) m->seq = 1;   // 32-bit scan-word tag, never 0
+    sp.tag = m->seq;
+    sp.full = full ? 1 : 0;
+    m->last_full = full;
+    K(m, m->sstream, GNN_K_SAMPLE, [&] { launch_sample_step(sp, m->sstream); });
     CK(cudaGetLastError());
     CK(cudaEventRecord(B.sampled, m->sstream));
     B.valid = true;
@@ -419,7 +441,7 @@ gnn_status issue_sample_step(gnn_model* m, int set, int64_t epoch, int64_t step)
     int64_t g, offset;
     int32_t n, b_total;
     plan_step(m->n_train, m->cfg.batch_size, m->world, m->rank, step, &g, &n, &offset, &b_total);
-    return issue_sample(m, set, n > 0 ? m->perm + offset : m->perm, nullptr, n, b_total, epoch, g);
+    return issue_sample(m, set, n > 0 ? m->perm + offset : m->perm, nullptr, n, b_total, epoch, g, m->full_train);
 }
 
 int find_set(gnn_model* m, int64_t epoch, int64_t g, int32_t n, int32_t b_total) {
@@ -634,6 +656,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     m->sage = c.model == GNN_SAGE_MEAN; m->shadow = c.sampler == GNN_SHADOW;
     m->slot = m->shadow ? m->hops : -1;
     m->bf16x3 = c.precision == GNN_FP32;
+    m->full_train = !(m->sage && !m->shadow);
     auto cleanup = [&](gnn_status s) {
         for (void* p : m->owned) cudaFree(p);
         for (void* p : m->owned_host) cudaFreeHost(p);
@@ -667,13 +690,11 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     AL(m->map, g->N);
     AL(m->bits, m->nwords);
     AL(m->icount, m->nodes_cap);
-    AL(m->seq, 1);
     const int sgrid = sample_step_grid();
     AL(m->status, (int64_t)sample_step_sites(m->hops) * sgrid);
     AL(m->bar, 1);
     CK(cudaMemset(m->status, 0, sizeof(unsigned long long) * sample_step_sites(m->hops) * sgrid));
     CK(cudaMemset(m->bar, 0, sizeof(GridBarrier)));
-    CK(cudaMemset(m->seq, 0, sizeof(uint32_t)));
     CK(cudaMemset(m->map, 0xff, sizeof(int32_t) * g->N));
     CK(cudaMemset(m->bits, 0, sizeof(uint32_t) * m->nwords));
     for (int h = 0; h <= m->hops; ++h) {
@@ -807,7 +828,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         const float bound = std::sqrt(6.0f / (float)(ly.in + ly.out));
         launch_init_params(m->params + ly.poff, ly.pcnt, bound, c.init_seed, (uint32_t)li, m->stream);
     }
-    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, m->stream);
+    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, false, m->stream);
     CK(cudaMemsetAsync(m->grads, 0, sizeof(float) * m->pcount, m->stream));
     CK(cudaStreamSynchronize(m->stream));
     CK(cudaDeviceSynchronize());
@@ -902,7 +923,7 @@ gnn_status gnn_set_params(gnn_model* m, const float* in_host, int64_t n) {
     if (n != m->pcount) return fail(GNN_ERR_SHAPE, "n != param_count");
     TRY(set_device(m->g->dev));
     CK(cudaMemcpyAsync(m->params, in_host, sizeof(float) * n, cudaMemcpyHostToDevice, m->stream));
-    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, m->stream);
+    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, false, m->stream);
     CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }
@@ -970,7 +991,7 @@ gnn_status gnn_sample(gnn_model* m, int64_t epoch, int64_t g, gnn_batch_sizes* s
     const int set = other_set(m);
     const bool prof = m->profiling;
     m->profiling = false;
-    gnn_status st_ = issue_sample(m, set, m->perm + g * B, nullptr, n, n, epoch, g);
+    gnn_status st_ = issue_sample(m, set, m->perm + g * B, nullptr, n, n, epoch, g, true);
     m->profiling = prof;
     TRY(st_);
     m->bs[set].valid = false;   // a parity sample is not a training batch
@@ -1040,10 +1061,10 @@ gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t
     int cur = find_set(m, epoch, g, n_seeds, b_total);
     if (cur < 0) {
         cur = other_set(m);
-        TRY(issue_sample(m, cur, nullptr, seeds_host, n_seeds, b_total, epoch, g));
+        TRY(issue_sample(m, cur, nullptr, seeds_host, n_seeds, b_total, epoch, g, m->full_train));
     }
     if (prefetch && m->overlap && !m->profiling)
-        TRY(issue_sample(m, 1 - cur, nullptr, next_seeds_host, next_n, next_b_total, epoch, next_g));
+        TRY(issue_sample(m, 1 - cur, nullptr, next_seeds_host, next_n, next_b_total, epoch, next_g, m->full_train));
     TRY(train_set(m, cur));
     CK(cudaMemcpyAsync(loss_out_host, &m->bs[cur].st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
@@ -1121,7 +1142,7 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
     if (what == GNN_DBG_PHASES) {   // sampling-kernel phase durations of the last sampling run (us)
         GridBarrier hb{};
         CK(cudaMemcpy(&hb, m->bar, sizeof(GridBarrier), cudaMemcpyDeviceToHost));
-        const int nb = 2 * m->hops + 3 + (m->shadow ? 1 : 0);
+        const int nb = m->last_full ? 2 * m->hops + 3 + (m->shadow ? 1 : 0) : 2 * m->hops + 1;
         if (n < nb) return fail(GNN_ERR_BUFFER, "need " + std::to_string(nb));
         unsigned long long prev = hb.t0;
         for (int i = 0; i < nb; ++i) {

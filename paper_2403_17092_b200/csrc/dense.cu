@@ -334,7 +334,9 @@ __global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
 // SGD (W <- W - lr G, §2.2) fused with the repack of the GEMM weight planes
 // W [K_pad x N_pad] (coalesced in that order; padding entries stay the zeros written at
 // creation).  Each parameter is visited exactly once.  grads == nullptr: pack only.
-__global__ void k_sgd_pack(PackAll P, float* __restrict__ params, const float* __restrict__ grads, float lr) {
+// reduce (single rank, no exchange in between): G is first reduced from the wgrad split-K
+// partials in the fixed split order (the arithmetic of k_wgrad_reduce_all) and stored.
+__global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restrict__ grads, float lr, int reduce) {
     pdl_trigger();
     pdl_wait();
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -350,7 +352,18 @@ __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, const float* _
             if (r < 0 || c >= L.out) continue;
             const int64_t idx = L.poff + (int64_t)r * L.out + c;
             float w = params[idx];
-            if (grads) { w = w - lr * grads[idx]; params[idx] = w; }
+            if (grads) {
+                float gr;
+                if (reduce) {
+                    gr = 0.f;
+                    for (int z = 0; z < L.splits; ++z) gr += L.part[z * L.split_stride + f];
+                    grads[idx] = gr;
+                } else {
+                    gr = grads[idx];
+                }
+                w = w - lr * gr;
+                params[idx] = w;
+            }
             store_split1(L.Wkn, f, w);
         }
     }
@@ -466,8 +479,8 @@ void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s) {
     launch_pdl(k_wgrad_reduce_all, 148 * 4, 256, 0, s, p, grads);
 }
 
-void launch_sgd_pack(const PackAll& p, float* params, const float* grads, float lr, cudaStream_t s) {
-    launch_pdl(k_sgd_pack, 148 * 2, 256, 0, s, p, params, grads, lr);
+void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, cudaStream_t s) {
+    launch_pdl(k_sgd_pack, 148 * 2, 256, 0, s, p, params, grads, lr, reduce ? 1 : 0);
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,

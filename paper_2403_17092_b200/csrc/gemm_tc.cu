@@ -70,6 +70,18 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// 32 consecutive TMEM columns of this warp's lane quarter (thread = lane = row).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -126,11 +138,18 @@ struct GemmArgs {
     int n_tiles;
     int splits;             // wgrad
     int k_blocks;           // fwd/dgrad: reduction in 64-blocks (static)
+    int k_len;              // fwd/dgrad: reduction length (the last block's k16 steps past it are skipped)
     int n_store;            // columns of C to store
     float* C;
     int ldc;
     int relu;
     int64_t split_stride;   // wgrad: C + z * split_stride
+    // MODE 3 (last layer, fwd + softmax cross-entropy): rows of C are logits
+    StepState* st;
+    const int32_t* labels;
+    const int32_t* nodes;
+    Split dz;               // dZ planes [rows x ldc]
+    int classes;
 };
 
 struct TileInfo { int tm, tn, z, kb0, nkb; };
@@ -160,7 +179,8 @@ __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t, int M) {
 }
 
 // MODE 0 = dgrad (A, B K-major), MODE 1 = wgrad (A, B MN-major, split z), MODE 2 = fwd (A K-major,
-// B MN-major: W read as stored, [K x N]).
+// B MN-major: W read as stored, [K x N]), MODE 3 = fwd of the last layer with the softmax
+// cross-entropy in the epilogue (a thread holds a whole logits row: BN = n_pad <= 64).
 template <int BN, int STAGES, int TERMS, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
@@ -175,6 +195,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
+    __shared__ int ce_last;
+    __shared__ float ce_part[kThreads / 32];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pdl_trigger();
@@ -247,6 +269,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         // ================= MMA issuer (one thread)
         if (lane == 0) {
             constexpr uint32_t id = idesc<BN, A_MN, B_MN>();
+            // reduction extent: operands are zero past it, so the k16 steps beyond it are skipped
+            const int klen = MODE == 1 ? M : args.k_len;
             int it = 0, j = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 const TileInfo ti = tile_info<MODE>(args, t, M);
@@ -262,8 +286,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                     const uint32_t a_hi = smem_u32(st), b_hi = smem_u32(st + Cfg::kAStage);
                     const uint32_t a_lo = smem_u32(st + Cfg::kAStage + Cfg::kBStage);
                     const uint32_t b_lo = a_lo + Cfg::kAStage;
+                    const int nkk = min(kBK / 16, (klen - (ti.kb0 + kb) * kBK + 15) / 16);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
+                        if (kk > 0 && kk >= nkk) break;
                         // K-major: +32 B per 16-element k step inside the 128 B swizzle row;
                         // MN-major: +16 rows x 128 B per k step.
                         const uint32_t oa = A_MN ? kk * 2048 : kk * 32, ob = B_MN ? kk * 2048 : kk * 32;
@@ -290,7 +316,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         // outside the tensor map's extent are clipped by the TMA unit.
         const int q = warp & 3;                       // TMEM lane quarter this warp may access
         uint8_t* ebuf = smem + STAGES * kStageBytes + q * 2 * kEpiBuf;
-        int j = 0, nchunk = 0;
+        int j = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const TileInfo ti = tile_info<MODE>(args, t, M);
             const int row0 = ti.tm * kBM + q * 32;
@@ -302,43 +328,90 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                 mbar_wait(&tfull[acc], (j >> 1) & 1);
                 tc_fence_after();
             }
-#pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += kEpiCols, ++nchunk) {
-                uint32_t v[32];
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 2 * kEpiCols) {
+                // two 32-column chunks per TMEM wait; each goes out through its own smem buffer
+                const bool two = c0 + kEpiCols < BN;
+                uint32_t v[2][32];
                 if (has) {
                     const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::kAccCols + c0);
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                        : "r"(taddr));
+                    tmem_ld32(taddr, v[0]);
+                    if (two) tmem_ld32(taddr + kEpiCols, v[1]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 } else {
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) v[x] = 0u;
+                    for (int x = 0; x < 32; ++x) { v[0][x] = 0u; v[1][x] = 0u; }
                 }
                 if (!rows_ok) continue;                 // (warp-uniform) nothing of this quarter is stored
-                uint8_t* buf = ebuf + (nchunk & 1) * kEpiBuf;
-                if (lane == 0) bulk_wait_read<1>();     // the store issued from this buffer 2 chunks ago has read it
+                if (lane == 0) bulk_wait_read<0>();     // the previous stores have read both buffers
                 __syncwarp();
-                uint8_t* myrow = buf + lane * 128;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    float4 f;
-                    f.x = __uint_as_float(v[4 * c]); f.y = __uint_as_float(v[4 * c + 1]);
-                    f.z = __uint_as_float(v[4 * c + 2]); f.w = __uint_as_float(v[4 * c + 3]);
-                    if (args.relu) { f.x = fmaxf(f.x, 0.f); f.y = fmaxf(f.y, 0.f); f.z = fmaxf(f.z, 0.f); f.w = fmaxf(f.w, 0.f); }
-                    *reinterpret_cast<float4*>(myrow + ((c ^ (lane & 7)) << 4)) = f;
+                for (int hb = 0; hb < 2; ++hb) {
+                    if (hb == 1 && !two) break;
+                    uint8_t* myrow = ebuf + hb * kEpiBuf + lane * 128;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        float4 f;
+                        f.x = __uint_as_float(v[hb][4 * c]); f.y = __uint_as_float(v[hb][4 * c + 1]);
+                        f.z = __uint_as_float(v[hb][4 * c + 2]); f.w = __uint_as_float(v[hb][4 * c + 3]);
+                        if (args.relu) { f.x = fmaxf(f.x, 0.f); f.y = fmaxf(f.y, 0.f); f.z = fmaxf(f.z, 0.f); f.w = fmaxf(f.w, 0.f); }
+                        *reinterpret_cast<float4*>(myrow + ((c ^ (lane & 7)) << 4)) = f;
+                    }
                 }
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_3d(&mC, buf, tile_n + c0, row0, ti.z);
+                    tma_store_3d(&mC, ebuf, tile_n + c0, row0, ti.z);
+                    if (two) tma_store_3d(&mC, ebuf + kEpiBuf, tile_n + c0 + kEpiCols, row0, ti.z);
                     bulk_commit();
+                }
+            }
+            if (MODE == 3 && has) {
+                // softmax cross-entropy of this thread's row (R15):
+                // l = max + log sum exp(z - max) - z_y;  dZ = (softmax - onehot) / b_total
+                constexpr int kZ = (BN + 31) / 32 * 32;
+                uint32_t zr[kZ / 32][32];
+#pragma unroll
+                for (int c0 = 0; c0 < kZ; c0 += 32)
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::kAccCols + c0), zr[c0 / 32]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int row = row0 + lane;
+                const int C = args.classes;
+                const float inv_bt = 1.0f / (float)max(args.st->b_total, 1);
+                const int64_t zoff = (int64_t)row * args.ldc;
+                if (row < M) {
+                    const int y = args.labels[args.nodes[row]];
+                    float mx = -INFINITY, zy = 0.f;
+#pragma unroll
+                    for (int c = 0; c < kZ; ++c) {
+                        const float z = __uint_as_float(zr[c >> 5][c & 31]);
+                        if (c < C) mx = fmaxf(mx, z);
+                        if (c == y) zy = z;
+                    }
+                    float s = 0.f;
+#pragma unroll
+                    for (int c = 0; c < kZ; ++c)
+                        if (c < C) s += expf(__uint_as_float(zr[c >> 5][c & 31]) - mx);
+#pragma unroll
+                    for (int c = 0; c < BN; c += 2) {
+                        float d0 = 0.f, d1 = 0.f;
+                        if (c < C) d0 = (expf(__uint_as_float(zr[c >> 5][c & 31]) - mx) / s - (c == y ? 1.f : 0.f)) * inv_bt;
+                        if (c + 1 < C) d1 = (expf(__uint_as_float(zr[(c + 1) >> 5][(c + 1) & 31]) - mx) / s - (c + 1 == y ? 1.f : 0.f)) * inv_bt;
+                        const __nv_bfloat162 hi = __floats2bfloat162_rn(d0, d1);
+                        *reinterpret_cast<__nv_bfloat162*>(args.dz.hi + zoff + c) = hi;
+                        if (args.dz.lo)
+                            *reinterpret_cast<__nv_bfloat162*>(args.dz.lo + zoff + c) =
+                                __floats2bfloat162_rn(d0 - __low2float(hi), d1 - __high2float(hi));
+                    }
+                    args.st->row_loss[row] = (mx + logf(s)) - zy;
+                    __threadfence();
+                } else if (row < ((M + 63) & ~63)) {      // zero tail rows of the dZ planes
+                    const __nv_bfloat162 zz = __floats2bfloat162_rn(0.f, 0.f);
+#pragma unroll
+                    for (int c = 0; c < BN; c += 2) {
+                        *reinterpret_cast<__nv_bfloat162*>(args.dz.hi + zoff + c) = zz;
+                        if (args.dz.lo) *reinterpret_cast<__nv_bfloat162*>(args.dz.lo + zoff + c) = zz;
+                    }
                 }
             }
             if (has) {
@@ -355,6 +428,24 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
+    }
+    if (MODE == 3) {
+        // the last CTA to finish sums the row losses in row order (deterministic)
+        if (threadIdx.x == 0) ce_last = atomicAdd(&args.st->ce_done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (!ce_last) return;
+        __threadfence();
+        float part = 0.f;
+        for (int r = threadIdx.x; r < M; r += kThreads) part += args.st->row_loss[r];
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) ce_part[warp] = part;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float tot = 0.f;
+            for (int w = 0; w < kThreads / 32; ++w) tot += ce_part[w];
+            args.st->loss = tot * (1.0f / (float)max(args.st->b_total, 1));
+            args.st->ce_done = 0u;
+        }
     }
 }
 
@@ -434,6 +525,16 @@ cudaError_t dispatch_bn(int bn, int grid, const TcGemmMaps& mp, const GemmArgs& 
         default: return cudaErrorInvalidValue;
     }
 }
+template <int TERMS>
+cudaError_t dispatch_ce(int bn, int grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
+    switch (bn) {
+        case 16: return launch_tc<16, 4, TERMS, 3>(grid, mp, a, s);
+        case 32: return launch_tc<32, 4, TERMS, 3>(grid, mp, a, s);
+        case 48: return launch_tc<48, 4, TERMS, 3>(grid, mp, a, s);
+        case 64: return launch_tc<64, 4, TERMS, 3>(grid, mp, a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
 }  // namespace
 
 int tc_tile_n(int n_pad) {
@@ -452,6 +553,7 @@ cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const 
     a.n_tiles = (n_pad + bn - 1) / bn;
     a.splits = splits;
     a.k_blocks = (k_pad + kBK - 1) / kBK;
+    a.k_len = k_pad;
     a.n_store = n_store;
     a.C = C;
     a.ldc = ldc;
@@ -466,4 +568,29 @@ cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const 
     return bf16x3 ? dispatch_bn<3, 1>(bn, grid, maps, a, s) : dispatch_bn<1, 1>(bn, grid, maps, a, s);
 }
 
+}  // namespace gs
+
+namespace gs {
+cudaError_t launch_gemm_tc_ce(bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_cap, int n_pad,
+                              int k_pad, float* Z, StepState* st, int classes, const int32_t* labels,
+                              const int32_t* nodes, Split dz, cudaStream_t s) {
+    if (n_pad > 64) return cudaErrorInvalidValue;
+    GemmArgs a{};
+    a.m_ptr = m_ptr;
+    a.m_tiles_cap = (m_cap + kBM - 1) / kBM;
+    a.n_tiles = 1;
+    a.splits = 1;
+    a.k_blocks = (k_pad + kBK - 1) / kBK;
+    a.k_len = k_pad;
+    a.n_store = n_pad;
+    a.C = Z;
+    a.ldc = n_pad;
+    a.st = st;
+    a.labels = labels;
+    a.nodes = nodes;
+    a.dz = dz;
+    a.classes = classes;
+    const int grid = std::max(1, std::min(kSMs, a.m_tiles_cap));
+    return bf16x3 ? dispatch_ce<3>(n_pad, grid, maps, a, s) : dispatch_ce<1>(n_pad, grid, maps, a, s);
+}
 }  // namespace gs

@@ -42,10 +42,6 @@ constexpr int kWarpGrid = 148 * 16;          // blocks of 256 threads for warp-p
 // Epoch permutation keys (Philox tag 1): keys[i] = (w0<<32)|w1 of (train[i], 0, epoch).
 void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t epoch,
                       uint64_t* keys, cudaStream_t s);
-// Start of a step: state fields, seeds -> nodes[0:n), map[seed] = i.
-void launch_begin_step(StepState* st, const int32_t* seed_src, int32_t n, int32_t b_total,
-                       uint32_t epoch, uint32_t g, int32_t* nodes, int32_t* map, uint32_t* seq,
-                       cudaStream_t s);
 
 struct GridBarrier {
     unsigned count, gen;
@@ -72,9 +68,14 @@ struct SampleParams {
     uint64_t seed;
     int hops, shadow, slot;
     int32_t* icount;     // ShaDow: induced edges per node of S
-    unsigned long long* status;   // look-back words [sample_step_sites(hops) x grid], tagged by StepState::seq
+    unsigned long long* status;   // look-back words [sample_step_sites(hops) x grid]: tag << 32 | chunk sum
     GridBarrier* bar;
     HopIO hop[kMaxHops + 1];
+    // per launch: the batch (the kernel also resets the StepState and writes dst_0)
+    const int32_t* seed_src;
+    int n_seeds, b_total;
+    uint32_t epoch, g, tag;   // tag: step sequence number (unique per launch)
+    int full;                 // 1: relabel the last hop too (sampling API, ShaDow, GCN)
 };
 // One persistent launch: every hop's sampling + relabel, the ShaDow induced block, the
 // transposed blocks, the map reset.  Grid = co-resident blocks (occupancy x SMs).
@@ -130,7 +131,8 @@ struct PackAll { PackLayer l[kMaxHops]; int n; bool sage; };
 // grads[poff + r*out + c] = Σ_z part[z][rpad(r)*n_pad + c] for every layer, fixed z order.
 void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s);
 // W <- W - lr*G (grads may be nullptr: pack only) and the bf16 planes of W, all layers.
-void launch_sgd_pack(const PackAll& p, float* params, const float* grads, float lr, cudaStream_t s);
+// reduce: G = the fixed-order sum of the wgrad partials, written to grads first (one rank).
+void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, cudaStream_t s);
 // Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total
 // written as split planes [rows x ldz] (+ zero tail rows).
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels,
@@ -165,5 +167,13 @@ int tc_tile_n(int n_pad);
 cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_static,
                            int m_cap, int n_pad, int k_pad, float* C, int ldc, int n_store, bool relu, int splits,
                            int64_t split_stride, cudaStream_t s);
+
+// Last layer, fused: Z = A W (logits, stored like mode 2) and, in the epilogue, the softmax
+// cross-entropy of every row < *m_ptr (= batch_n): st->row_loss, dZ split planes [rows x n_pad]
+// (+ zero tail rows to a multiple of 64) and st->loss = Σ ℓ / b_total (last CTA, row order).
+// n_pad <= 64 (one thread holds a row).
+cudaError_t launch_gemm_tc_ce(bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_cap, int n_pad,
+                              int k_pad, float* Z, StepState* st, int classes, const int32_t* labels,
+                              const int32_t* nodes, Split dz, cudaStream_t s);
 
 }  // namespace gs

@@ -84,16 +84,16 @@ __device__ int chunk_scan(Smem& sm, int n, F f, PUT put, unsigned long long* sta
     int s = 0;
     for (int i = beg + threadIdx.x; i < end; i += kThreads) s += f(i);
     const int agg = BlockReduce(sm.cub.reduce).Sum(s);
-    const unsigned long long tg = (unsigned long long)(tag & 0xFFFFFFu) << 40;
+    const unsigned long long tg = (unsigned long long)tag << 32;   // tag != 0 (status words start at 0)
     if (threadIdx.x == 0) {   // publish this chunk's sum
         __threadfence();
-        atomicExch(&status[blockIdx.x], tg | (1ull << 32) | (unsigned)agg);
+        atomicExch(&status[blockIdx.x], tg | (unsigned)agg);
     }
     // read every predecessor's published sum in parallel (one thread each; grid <= threads)
     int pre = 0;
     for (int j = threadIdx.x; j < (int)blockIdx.x; j += kThreads) {
         unsigned long long w = ld_volatile_u64(&status[j]);
-        while ((w & ~0xFFFFFFFFFFull) != tg) w = ld_volatile_u64(&status[j]);
+        while ((w & ~0xFFFFFFFFull) != tg) w = ld_volatile_u64(&status[j]);
         pre += (int)(unsigned)(w & 0xFFFFFFFFull);
     }
     __syncthreads();
@@ -149,14 +149,15 @@ __device__ __forceinline__ int min_deg(const int64_t* row_ptr, int v, int k) {
 // d <= k are copied whole.  Several nodes per warp keep more dependent loads in flight.
 template <int GS>
 __device__ __forceinline__ void sample_nodes(const SampleParams& P, int h, int k, int i, bool valid, uint32_t epoch,
-                                             uint32_t g, int lane) {
+                                             uint32_t g, int lane, bool mark) {
     const HopIO& H = P.hop[h];
+    const int32_t* dst = h == 0 ? P.seed_src : P.nodes;   // hop 0: the seeds, read at their source
     const int lg = lane & (GS - 1);
     const int gbase = lane & ~(GS - 1);
     int v = 0, d = 0, out = 0;
     int64_t start = 0;
     if (valid) {
-        v = P.nodes[i];
+        v = dst[i];
         start = __ldg(P.row_ptr + v);
         d = (int)(__ldg(P.row_ptr + v + 1) - start);
         out = H.rowptr[i];
@@ -180,24 +181,24 @@ __device__ __forceinline__ void sample_nodes(const SampleParams& P, int h, int k
         if (lg < k) {
             const int u = __ldg(P.col + start + pick);
             H.nbr[out + rank] = u;
-            if (P.map[u] < 0) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
+            if (mark && P.map[u] < 0) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
         }
     } else {
         for (int q = lg; q < d; q += GS) {
             const int u = __ldg(P.col + start + q);
             H.nbr[out + q] = u;
-            if (P.map[u] < 0) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
+            if (mark && P.map[u] < 0) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
         }
     }
 }
 
 template <int GS>
 __device__ __forceinline__ void sample_chunk(const SampleParams& P, int h, int k, int beg, int end, uint32_t epoch,
-                                             uint32_t g, int lane, int wib) {
+                                             uint32_t g, int lane, int wib, bool mark) {
     constexpr int kPerWarp = 32 / GS;
     for (int i0 = beg + wib * kPerWarp; i0 < end; i0 += kWarps * kPerWarp) {
         const int i = i0 + lane / GS;
-        sample_nodes<GS>(P, h, k, i, i < end, epoch, g, lane);
+        sample_nodes<GS>(P, h, k, i, i < end, epoch, g, lane, mark);
     }
 }
 
@@ -214,39 +215,72 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
     StepState* st = P.st;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gtid = blockIdx.x * kThreads + threadIdx.x, nthreads = gridDim.x * kThreads;
-    const uint32_t epoch = st->epoch, g = st->g, tag = st->seq;
+    const uint32_t epoch = P.epoch, g = P.g, tag = P.tag;
     const int G = gridDim.x;
     int site = 0;   // scan site index (own status words per scan in the step)
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         P.bar->t0 = t;
+        // the step's state (dst_0 = the seeds, in batch order)
+        for (int h = 0; h <= kMaxHops; ++h) { st->n_dst[h] = 0; st->n_src[h] = 0; st->n_edges[h] = 0; }
+        st->n_dst[0] = P.n_seeds;
+        st->batch_n = P.n_seeds;
+        st->b_total = P.b_total;
+        st->epoch = epoch;
+        st->g = g;
+        st->loss = 0.f;
+        st->seq = tag;
+    }
+    for (int i = gtid; i < P.n_seeds; i += nthreads) {   // nodes[i] = seed_i, map[seed_i] = i
+        const int v = P.seed_src[i];
+        P.nodes[i] = v;
+        P.map[v] = i;
     }
 
     for (int h = 0; h < P.hops; ++h) {
         const HopIO& H = P.hop[h];
         const int k = H.k;
+        // the last hop's new-node list and relabel are needed only by the sampling API, ShaDow
+        // and GCN; SAGE layer 1 reads X by the sampled global ids
+        const bool mark = P.full || h < P.hops - 1;
         // ---- phase 1: relabel the previous hop (its new ids are all assigned); blk_rowptr =
         //      exclusive scan of min(deg, k); Floyd-sample this block's nodes, mark unseen nbrs
         if (h > 0) relabel_edges(P, P.hop[h - 1], st->n_edges[h - 1], gtid, nthreads);
-        const int nd = st->n_dst[h];
+        const int nd = h == 0 ? P.n_seeds : st->n_dst[h];
+        const int32_t* dst = h == 0 ? P.seed_src : P.nodes;
         {
-            const int tot = chunk_scan(sm, nd, [&](int i) { return min_deg(P.row_ptr, P.nodes[i], k); },
+            const int tot = chunk_scan(sm, nd, [&](int i) { return min_deg(P.row_ptr, dst[i], k); },
                                        [&](int i, int ex, int) { H.rowptr[i] = ex; }, P.status + (site++) * G, tag);
             if (tot >= 0 && threadIdx.x == 0) { H.rowptr[nd] = tot; st->n_edges[h] = tot; }
             int beg, end;
             chunk_of(nd, beg, end);
-            if (k <= 8) sample_chunk<8>(P, h, k, beg, end, epoch, g, lane, wib);
-            else if (k <= 16) sample_chunk<16>(P, h, k, beg, end, epoch, g, lane, wib);
-            else sample_chunk<32>(P, h, k, beg, end, epoch, g, lane, wib);
+            if (k <= 8) sample_chunk<8>(P, h, k, beg, end, epoch, g, lane, wib, mark);
+            else if (k <= 16) sample_chunk<16>(P, h, k, beg, end, epoch, g, lane, wib, mark);
+            else sample_chunk<32>(P, h, k, beg, end, epoch, g, lane, wib, mark);
         }
         grid_sync(P.bar);
-        // ---- phase 2: new nodes in ascending global id (R6): nodes[n_dst + rank], map
+        if (!mark) break;
+        // ---- phase 2: new nodes in ascending global id (R6): nodes[n_dst + rank], map.
+        //      Hop 0 was marked while the seeds' map entries were being written: a marked seed
+        //      (map >= 0 by now) is not new.
+        const bool filt = h == 0;
         {
-            const int tot = chunk_scan(sm, P.nwords, [&](int w) { return __popc(P.bits[w]); },
+            auto fresh = [&](int w) {
+                uint32_t word = P.bits[w];
+                if (!filt || !word) return word;
+                uint32_t keep = 0u;
+                for (uint32_t x = word; x; x &= x - 1) {
+                    const int b = __ffs(x) - 1;
+                    if (P.map[w * 32 + b] < 0) keep |= 1u << b;
+                }
+                return keep;
+            };
+            const int tot = chunk_scan(sm, P.nwords, [&](int w) { return __popc(fresh(w)); },
                                        [&](int w, int ex, int cnt) {
+                                           uint32_t word = fresh(w);
+                                           if (filt && P.bits[w]) P.bits[w] = 0u;
                                            if (!cnt) return;
-                                           uint32_t word = P.bits[w];
                                            const int base = nd + ex;
                                            int r = 0;
                                            while (word) {
@@ -269,8 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
 
     // ---- relabel the last hop; ShaDow: count the induced edges of every node of S
     const int L1 = P.hops - 1;
-    relabel_edges(P, P.hop[L1], st->n_edges[L1], gtid, nthreads);
-    const int nS = st->n_src[L1];
+    if (P.full) relabel_edges(P, P.hop[L1], st->n_edges[L1], gtid, nthreads);
+    const int nS = P.full ? st->n_src[L1] : st->n_dst[L1];   // nodes with a map entry
     if (P.shadow) {
         for (int i = blockIdx.x * kWarps + wib; i < nS; i += G * kWarps) {   // |{u in row v : u in S}|
             const int v = P.nodes[i];
@@ -308,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
             }
         }
     }
-    grid_sync(P.bar);
+    if (P.full) grid_sync(P.bar);
 
     // ---- transposed blocks (rows = local src ids), all needed blocks together
     for (int h = 0; h <= P.hops; ++h) {

@@ -265,6 +265,13 @@ class Model:
         _check(lib().gnn_synchronize(self.h))
 
     # ---------------------------------------------------------------- introspection
+    def sample_sizes(self, epoch: int, g: int):
+        """gnn_sample's per-hop sizes of global batch g (full relabel of every hop)."""
+        sz = _Sizes()
+        _check(lib().gnn_sample(self.h, epoch, g, C.byref(sz)))
+        n = sz.num_hops + 1
+        return dict(n_dst=list(sz.n_dst[:n]), n_src=list(sz.n_src[:n]), n_edges=list(sz.n_edges[:n]))
+
     def last_sizes(self):
         sz = _Sizes()
         _check(lib().gnn_last_sizes(self.h, C.byref(sz)))
