@@ -760,7 +760,8 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         Layer ly;
         ly.in = m->dims[li];
         ly.out = m->dims[li + 1];
-        ly.in_pad = (int)round_up(ly.in, 4);
+        // layer 1 reads the feature table in place: its padded width is the table's row stride
+        ly.in_pad = li == 0 ? g->stride : (int)round_up(ly.in, 4);
         ly.rows = (m->sage ? 2 : 1) * ly.in;
         // GEMM reduction width; a multiple of 8 so bf16 rows are 16-byte strided (TMA)
         ly.k_pad = m->sage ? 2 * ly.in_pad : (int)round_up(ly.in_pad, 8);

@@ -41,6 +41,14 @@ __device__ __forceinline__ void store_split1(const Split& o, int64_t idx, float 
     if (o.lo) o.lo[idx] = __float2bfloat16_rn(v - __bfloat162float(h));
 }
 __device__ __forceinline__ int round64(int n) { return (n + 63) & ~63; }
+// L2 prefetch of two rows of `width` floats (b may be null): one 128-byte line per lane.
+__device__ __forceinline__ void prefetch_rows_l2(const float* a, const float* b, int width, int lane) {
+    const int nl = (width * 4 + 127) >> 7;
+    for (int l = lane; l < 2 * nl; l += 32) {
+        const float* p = l < nl ? a + l * 32 : (b ? b + (l - nl) * 32 : nullptr);
+        if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    }
+}
 constexpr float4 kZero4 = {0.f, 0.f, 0.f, 0.f};
 
 // ------------------------------------------------------------------ forward aggregation
@@ -198,7 +206,7 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
 // range and its first 32 destinations are loaded while the current row's dA rows are in flight,
 // so a row costs about one dependent memory round trip instead of three.
 template <int CPL, bool GCN>
-__global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __restrict__ st,
+__global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __restrict__ st,
         const int32_t* __restrict__ dlim_ptr, const float* __restrict__ dA, int in_pad,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ trowptr,
         const int32_t* __restrict__ tdst, const float* __restrict__ Hprev, Split dPre) {
@@ -216,7 +224,11 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
     int u = global_warp();
     // prologue: row u's edge range and first chunk of destinations
     int cb = 0, ce = 0, ci = -1;
-    if (u < nsrc) { cb = trowptr[u]; ce = trowptr[u + 1]; }
+    if (u < nsrc) {
+        cb = trowptr[u];
+        ce = trowptr[u + 1];
+        prefetch_rows_l2(Hprev + (int64_t)u * in_pad, u < dlim ? dA + (int64_t)u * lda : nullptr, in_pad, lane);
+    }
     if (lane < ce - cb) ci = tdst[cb + lane];
     for (; u < nr; u += W) {
         if (u >= nsrc) {
@@ -226,16 +238,10 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
         const int un = u + W;
         int nb = 0, ne = 0;
         if (un < nsrc) { nb = trowptr[un]; ne = trowptr[un + 1]; }
-        // rows that do not depend on the edge chain
-        const float4* hp = reinterpret_cast<const float4*>(Hprev + (int64_t)u * in_pad);
-        const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
-        float4 hv[CPL], sv[CPL];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-            const int ch = lane + 32 * c;
-            hv[c] = ch < nch ? __ldg(hp + ch) : kZero4;
-            sv[c] = (ch < nch && u < dlim) ? __ldg(sp + ch) : kZero4;
-        }
+        // the next row's H_prev and dA-self rows go to L2 now (they are read at the end of
+        // that row: no registers held across its edge loop)
+        if (un < nsrc) prefetch_rows_l2(Hprev + (int64_t)un * in_pad, un < dlim ? dA + (int64_t)un * lda : nullptr,
+                                        in_pad, lane);
         const float dout = (float)(ce - cb + (u < ndst ? 1 : 0));
         float4 acc[CPL];
 #pragma unroll
@@ -292,6 +298,15 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(int h, const StepState* __rest
         if (GCN && u < dlim) {
             const float din = (float)(rowptr[u + 1] - rowptr[u] + 1);
             wself = 1.0f / sqrtf(din * dout);
+        }
+        const float4* hp = reinterpret_cast<const float4*>(Hprev + (int64_t)u * in_pad);
+        const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
+        float4 hv[CPL], sv[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            hv[c] = ch < nch ? __ldg(hp + ch) : kZero4;
+            sv[c] = (ch < nch && u < dlim) ? __ldg(sp + ch) : kZero4;
         }
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
