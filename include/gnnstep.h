@@ -209,8 +209,8 @@ gnn_status gnn_synchronize(gnn_model* m);
  * (layer l's output H^(l) of the last step, 0-based l, rows x out, fp32; its sign pattern
  * is the ReLU decision the backward pass used).  BUFFER if n is too small. */
 enum { GNN_DBG_LOGITS = 0, GNN_DBG_GRADS = 1, GNN_DBG_LOSS = 2, GNN_DBG_PHASES = 8, GNN_DBG_ACT = 16 };
-/* GNN_DBG_PHASES: microseconds of each phase of the last step's sampling kernel
- * (4 per hop, relabel/induce, 3 transposed-block phases; 2 more for ShaDow). */
+/* GNN_DBG_PHASES: microseconds of each phase (between grid barriers, the last one until the
+ * last block ends) of the last sampling-kernel run; BUFFER if n < phases (<= 32). */
 gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n);
 /* Sizes of the last trained batch (synchronizes). */
 gnn_status gnn_last_sizes(gnn_model* m, gnn_batch_sizes* sizes_host);

@@ -1144,13 +1144,14 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
         GridBarrier hb{};
         CK(cudaMemcpy(&hb, m->bar, sizeof(GridBarrier), cudaMemcpyDeviceToHost));
         const int nb = m->last_full ? 2 * m->hops + 3 + (m->shadow ? 1 : 0) : 2 * m->hops + 1;
-        if (n < nb) return fail(GNN_ERR_BUFFER, "need " + std::to_string(nb));
+        if (n < nb + 1) return fail(GNN_ERR_BUFFER, "need " + std::to_string(nb + 1));
         unsigned long long prev = hb.t0;
         for (int i = 0; i < nb; ++i) {
             const unsigned long long t = hb.ts[(hb.nts - nb + i) & 31u];
             out_host[i] = (float)((double)(t - prev) * 1e-3);
             prev = t;
         }
+        out_host[nb] = hb.t_end > prev ? (float)((double)(hb.t_end - prev) * 1e-3) : 0.f;   // last phase
         return GNN_OK;
     }
     if (what >= GNN_DBG_ACT && what < GNN_DBG_ACT + m->L) {

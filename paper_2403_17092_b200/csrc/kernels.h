@@ -47,6 +47,7 @@ struct GridBarrier {
     unsigned count, gen;
     unsigned nts, pad;
     unsigned long long t0;        // kernel start (globaltimer, ns)
+    unsigned long long t_end;     // last block's end (atomicMax)
     unsigned long long ts[32];    // ring of barrier-release times
 };
 // Per block (hop h, or the ShaDow induced block at index `slot`): CSR of the block

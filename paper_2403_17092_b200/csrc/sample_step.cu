@@ -81,8 +81,15 @@ template <class F, class PUT>
 __device__ int chunk_scan(Smem& sm, int n, F f, PUT put, unsigned long long* status, uint32_t tag) {
     int beg, end;
     chunk_of(n, beg, end);
-    int s = 0;
-    for (int i = beg + threadIdx.x; i < end; i += kThreads) s += f(i);
+    // a chunk that fits one pass of the block keeps its values in registers (f evaluated once)
+    const bool one = end - beg <= kThreads;
+    int s = 0, v1 = 0;
+    if (one) {
+        if (beg + (int)threadIdx.x < end) v1 = f(beg + threadIdx.x);
+        s = v1;
+    } else {
+        for (int i = beg + threadIdx.x; i < end; i += kThreads) s += f(i);
+    }
     const int agg = BlockReduce(sm.cub.reduce).Sum(s);
     const unsigned long long tg = (unsigned long long)tag << 32;   // tag != 0 (status words start at 0)
     if (threadIdx.x == 0) {   // publish this chunk's sum
@@ -100,6 +107,14 @@ __device__ int chunk_scan(Smem& sm, int n, F f, PUT put, unsigned long long* sta
     const int excl = BlockReduce(sm.cub.reduce).Sum(pre);
     if (threadIdx.x == 0) { sm.excl = excl; sm.carry = excl; sm.total = excl + agg; }
     __syncthreads();
+    if (one) {
+        const int i = beg + threadIdx.x;
+        int ex, tile;
+        BlockScan(sm.cub.scan).ExclusiveSum(v1, ex, tile);
+        if (i < end) put(i, sm.excl + ex, v1);   // (the reduce result is valid in thread 0 only)
+        __syncthreads();
+        return blockIdx.x == gridDim.x - 1 ? sm.total : -1;
+    }
     for (int base = beg; base < end; base += kThreads) {
         const int i = base + threadIdx.x;
         const int v = i < end ? f(i) : 0;
@@ -181,13 +196,13 @@ __device__ __forceinline__ void sample_nodes(const SampleParams& P, int h, int k
         if (lg < k) {
             const int u = __ldg(P.col + start + pick);
             H.nbr[out + rank] = u;
-            if (mark && P.map[u] < 0) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
+            if (mark) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
         }
     } else {
         for (int q = lg; q < d; q += GS) {
             const int u = __ldg(P.col + start + q);
             H.nbr[out + q] = u;
-            if (mark && P.map[u] < 0) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
+            if (mark) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
         }
     }
 }
@@ -222,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         P.bar->t0 = t;
+        P.bar->t_end = 0ull;
         // the step's state (dst_0 = the seeds, in batch order)
         for (int h = 0; h <= kMaxHops; ++h) { st->n_dst[h] = 0; st->n_src[h] = 0; st->n_edges[h] = 0; }
         st->n_dst[0] = P.n_seeds;
@@ -262,9 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         grid_sync(P.bar);
         if (!mark) break;
         // ---- phase 2: new nodes in ascending global id (R6): nodes[n_dst + rank], map.
-        //      Hop 0 was marked while the seeds' map entries were being written: a marked seed
-        //      (map >= 0 by now) is not new.
-        const bool filt = h == 0;
+        //      Every sampled neighbour was marked (no map lookup on the sampling path): a marked
+        //      node that already has a local id (map >= 0) is not new.
+        const bool filt = true;
         {
             auto fresh = [&](int w) {
                 uint32_t word = P.bits[w];
@@ -432,6 +448,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         }
     }
     for (int i = gtid; i < nS; i += nthreads) P.map[P.nodes[i]] = -1;
+    if (threadIdx.x == 0) {   // end of this block (debug phase readout)
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(&P.bar->t_end, t);
+    }
 }
 
 }  // namespace

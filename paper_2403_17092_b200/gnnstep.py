@@ -317,8 +317,8 @@ class Model:
 def _phases(self, n=32):
     out = np.zeros(n, dtype=np.float32)
     _check(lib().gnn_debug_get(self.h, 8, _ptr(out), n))
-    nb = 2 * len(self.fanouts) + 3 + (1 if self.sampler == "shadow" else 0)
-    return out[:nb]
+    nz = np.nonzero(out)[0]
+    return out[:int(nz[-1]) + 1] if len(nz) else out[:0]
 
 
 Model.sampling_phases_us = _phases
