@@ -137,6 +137,8 @@ struct gnn_model {
     cudaStream_t stream = nullptr;       // training (the caller's, or own_stream)
     cudaStream_t own_stream = nullptr;
     cudaStream_t sstream = nullptr;      // sampling (library-owned)
+    cudaStream_t wstream = nullptr;      // weight-gradient branch of the training step
+    cudaEvent_t ev_dpre[kMaxHops] = {}, ev_join = nullptr;
     std::vector<void*> owned;
     std::vector<void*> owned_host;
 
@@ -282,15 +284,20 @@ void enqueue_training(gnn_model* m, int set) {
             K(m, s, GNN_K_CE, [&] { launch_ce(B.st, ly.H, ly.n_pad, g->C, g->y, B.nodes, ly.dPre, s); });
         }
     }
-    // ---- backward
+    // ---- backward.  The weight gradients are off the critical path (nothing in the step reads
+    // them before the update): they run on a forked stream as soon as their dPre is ready,
+    // concurrently with the dgrad -> backward-aggregation chain, and join before the update.
+    cudaStream_t ws = m->wstream;
     for (int li = L - 1; li >= 0; --li) {
         Layer& ly = m->layers[li];
         const int32_t* rows = rows_ptr(m, set, li);
         const int64_t stride = (int64_t)ly.k_pad * ly.n_pad;
+        cudaEventRecord(m->ev_dpre[li], s);
+        cudaStreamWaitEvent(ws, m->ev_dpre[li], 0);
         // dW = A^T dPre (deterministic split over rows)
-        K(m, s, GNN_K_GEMM_WGRAD, [&] {
+        K(m, ws, GNN_K_GEMM_WGRAD, [&] {
             launch_gemm_tc(1, m->bf16x3, ly.map_wgrad, rows, ly.k_pad, ly.k_pad, ly.n_pad, 0, ly.wpart, ly.n_pad,
-                           ly.n_pad, false, ly.splits, stride, s);
+                           ly.n_pad, false, ly.splits, stride, ws);
         });
         if (li == 0) break;
         // dA = dPre W^T (fp32)
@@ -305,6 +312,8 @@ void enqueue_training(gnn_model* m, int set) {
                             prev.H, prev.dPre, s);
         });
     }
+    cudaEventRecord(m->ev_join, ws);
+    cudaStreamWaitEvent(s, m->ev_join, 0);
     if (m->world > 1) {
         // ---- split-K partials of every layer -> flat gradient (fixed order), exchange, update
         K(m, s, GNN_K_GEMM_WGRAD, [&] { launch_wgrad_reduce_all(pack_desc(m), m->grads, s); });
@@ -822,6 +831,9 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
 #undef AL
     CK(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&m->sstream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&m->wstream, cudaStreamNonBlocking));
+    for (int li = 0; li < m->L; ++li) CK(cudaEventCreateWithFlags(&m->ev_dpre[li], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
     m->stream = m->own_stream;
     // ---- Glorot-uniform init (per layer block)
     for (int li = 0; li < m->L; ++li) {
@@ -858,6 +870,9 @@ gnn_status gnn_model_destroy(gnn_model* m) {
         if (p) cudaFree(p);
     if (m->own_stream) cudaStreamDestroy(m->own_stream);
     if (m->sstream) cudaStreamDestroy(m->sstream);
+    if (m->wstream) cudaStreamDestroy(m->wstream);
+    for (auto e : m->ev_dpre) if (e) cudaEventDestroy(e);
+    if (m->ev_join) cudaEventDestroy(m->ev_join);
     delete m;
     return GNN_OK;
 }
