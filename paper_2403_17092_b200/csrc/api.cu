@@ -92,6 +92,7 @@ struct HopBufs {
     int64_t cap_dst = 0, cap_edges = 0, cap_src = 0;
     bool need_t = false;
     int32_t *tcount = nullptr, *tcursor = nullptr, *tdst = nullptr;   // shared by both batch sets
+    int32_t* erow = nullptr;             // destination row of every edge (transposed fill)
 };
 
 // What one batch is made of, double-buffered: sizes, node list, per-block CSR + transposed CSR.
@@ -712,6 +713,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         if (b.need_t) {
             AL(b.tcount, b.cap_src + 1);
             AL(b.tcursor, b.cap_src + 1);
+            AL(b.erow, b.cap_edges);
             AL(b.tdst, b.cap_edges);
             CK(cudaMemset(b.tcount, 0, sizeof(int32_t) * (b.cap_src + 1)));
         }
@@ -757,6 +759,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
             io.rowptr = B.rowptr[h]; io.nbr = B.nbr[h]; io.col = B.col[h];
             io.tcount = b.need_t ? b.tcount : nullptr;
             io.trowptr = B.trowptr[h]; io.tcursor = b.tcursor; io.tdst = b.tdst; io.tdst_s = B.tdst_s[h];
+            io.erow = b.need_t ? b.erow : nullptr;
         }
     }
 

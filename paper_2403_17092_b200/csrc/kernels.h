@@ -57,6 +57,7 @@ struct HopIO {
     int k;
     int32_t *rowptr, *nbr, *col;
     int32_t *tcount, *trowptr, *tcursor, *tdst, *tdst_s;
+    int32_t* erow;    // destination row of each edge (when tcount is set)
 };
 struct SampleParams {
     StepState* st;

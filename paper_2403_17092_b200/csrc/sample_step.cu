@@ -152,6 +152,29 @@ __device__ __forceinline__ void bitonic_sort(int* s, int n2, int t, int nthr, SY
     }
 }
 
+// Sort len <= 8 ints from src into dst ascending, by one thread (a sorting network on
+// registers, INT_MAX padding).
+__device__ __forceinline__ void lane_sort8(const int32_t* src, int32_t* dst, int len) {
+    if (len <= 1) {
+        if (len == 1) dst[0] = src[0];
+        return;
+    }
+    int x[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) x[a] = a < len ? src[a] : INT_MAX;
+    constexpr int kNet[19][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}, {0, 2}, {1, 3}, {4, 6}, {5, 7}, {1, 2}, {5, 6},
+                                 {0, 4}, {3, 7}, {1, 5}, {2, 6}, {1, 4}, {3, 6}, {2, 4}, {3, 5}, {3, 4}};
+#pragma unroll
+    for (int c = 0; c < 19; ++c) {
+        const int a = x[kNet[c][0]], b = x[kNet[c][1]];
+        x[kNet[c][0]] = min(a, b);
+        x[kNet[c][1]] = max(a, b);
+    }
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+        if (a < len) dst[a] = x[a];
+}
+
 __device__ __forceinline__ int min_deg(const int64_t* row_ptr, int v, int k) {
     const int64_t d = __ldg(row_ptr + v + 1) - __ldg(row_ptr + v);
     return d < k ? (int)d : k;
@@ -196,12 +219,14 @@ __device__ __forceinline__ void sample_nodes(const SampleParams& P, int h, int k
         if (lg < k) {
             const int u = __ldg(P.col + start + pick);
             H.nbr[out + rank] = u;
+            if (H.erow) H.erow[out + rank] = i;
             if (mark) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
         }
     } else {
         for (int q = lg; q < d; q += GS) {
             const int u = __ldg(P.col + start + q);
             H.nbr[out + q] = u;
+            if (H.erow) H.erow[out + q] = i;
             if (mark) atomicOr(&P.bits[u >> 5], 1u << (u & 31));
         }
     }
@@ -351,7 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
                 const int m = p < re ? P.map[__ldg(P.col + p)] : -1;
                 const unsigned bal = __ballot_sync(kFull, m >= 0);
                 if (m >= 0) {
-                    S.col[out + __popc(bal & ((1u << lane) - 1u))] = m;
+                    const int o = out + __popc(bal & ((1u << lane) - 1u));
+                    S.col[o] = m;
+                    S.erow[o] = i;
                     atomicAdd(&S.tcount[m], 1);
                 }
                 out += __popc(bal);
@@ -371,12 +398,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         if (tot >= 0 && threadIdx.x == 0) H.trowptr[ns] = tot;
     }
     grid_sync(P.bar);
-    for (int h = 0; h <= P.hops; ++h) {
+    for (int h = 0; h <= P.hops; ++h) {   // edge-parallel fill (erow = each edge's destination row)
         const HopIO& H = P.hop[h];
         if (!H.tcount) continue;
-        const int nd = st->n_dst[h];
-        for (int i = blockIdx.x * kWarps + wib; i < nd; i += G * kWarps)
-            for (int e = H.rowptr[i] + lane; e < H.rowptr[i + 1]; e += 32) H.tdst[atomicAdd(&H.tcursor[H.col[e]], 1)] = i;
+        const int ne = st->n_edges[h];
+        for (int e = gtid; e < ne; e += nthreads) H.tdst[atomicAdd(&H.tcursor[H.col[e]], 1)] = H.erow[e];
     }
     grid_sync(P.bar);
     // sort every transposed row ascending (fixed summation order):
@@ -392,9 +418,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         const int ns = st->n_src[h];
         if (threadIdx.x == 0) s_nlong = 0;
         __syncthreads();
-        for (int u = blockIdx.x * kWarps + wib; u < ns; u += G * kWarps) {
-            const int b0 = H.trowptr[u];
-            const int len = H.trowptr[u + 1] - b0;
+        // a warp takes 32 consecutive rows: rows of <= 8 entries (almost all) are sorted by their
+        // lane alone (sorting network in registers); longer rows by the whole warp, one by one
+        for (int u0 = (blockIdx.x * kWarps + wib) * 32; u0 < ns; u0 += G * kWarps * 32) {
+            const int ul = u0 + lane;
+            const int lb = ul < ns ? H.trowptr[ul] : 0;
+            const int ll = ul < ns ? H.trowptr[ul + 1] - lb : 0;
+            if (ll <= 8) lane_sort8(H.tdst + lb, H.tdst_s + lb, ll);
+            unsigned longm = __ballot_sync(kFull, ll > 8);
+            while (longm) {
+            const int j = __ffs(longm) - 1;
+            longm &= longm - 1;
+            const int u = u0 + j;
+            const int b0 = __shfl_sync(kFull, lb, j);
+            const int len = __shfl_sync(kFull, ll, j);
             if (len > kWarpSort) {                   // hub row: queue it for the block-wide sort
                 int slot = 0;
                 if (lane == 0) slot = atomicAdd(&s_nlong, 1);
@@ -421,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
                 bitonic_sort(wbuf, n2, lane, 32, [] { __syncwarp(); });
                 for (int a = lane; a < len; a += 32) H.tdst_s[b0 + a] = wbuf[a];
                 __syncwarp();
+            }
             }
         }
         __syncthreads();
