@@ -146,7 +146,7 @@ struct gnn_model {
     BatchSet bs[2];
     int last = -1;                       // set trained last
     int fetch_set = 0;                   // set gnn_sample filled
-    int32_t *map = nullptr, *icount = nullptr;
+    int32_t *map = nullptr, *icount = nullptr, *hubs = nullptr;
     uint32_t seq = 0;                    // sampling-launch sequence number (scan-word tags)
     bool full_train = true;              // training needs the last hop's relabel (GCN, ShaDow)
     bool last_full = true;               // mode of the last sampling launch (phase readout)
@@ -700,6 +700,12 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     AL(m->map, g->N);
     AL(m->bits, m->nwords);
     AL(m->icount, m->nodes_cap);
+    {   // hub-row list of the transposed sort: rows longer than 256 entries, over all blocks
+        int64_t cap = 3;
+        for (int h = 0; h <= m->hops; ++h)
+            if (m->hb[h].need_t && (h < m->hops || m->shadow)) cap += m->hb[h].cap_edges / 257 + 1;
+        AL(m->hubs, cap);
+    }
     const int sgrid = sample_step_grid();
     AL(m->status, (int64_t)sample_step_sites(m->hops) * sgrid);
     AL(m->bar, 1);
@@ -742,6 +748,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         sp.shadow = m->shadow ? 1 : 0;
         sp.slot = m->shadow ? m->slot : -1;
         sp.icount = m->icount;
+        sp.hubs = m->hubs;
         sp.status = m->status;
         sp.bar = m->bar;
         for (int h = 0; h <= m->hops; ++h) {
@@ -1161,7 +1168,7 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
     if (what == GNN_DBG_PHASES) {   // sampling-kernel phase durations of the last sampling run (us)
         GridBarrier hb{};
         CK(cudaMemcpy(&hb, m->bar, sizeof(GridBarrier), cudaMemcpyDeviceToHost));
-        const int nb = m->last_full ? 2 * m->hops + 3 + (m->shadow ? 1 : 0) : 2 * m->hops + 1;
+        const int nb = std::min(32, std::max(0, (int)(hb.nts - hb.pad)));   // barriers of the last launch
         if (n < nb + 1) return fail(GNN_ERR_BUFFER, "need " + std::to_string(nb + 1));
         unsigned long long prev = hb.t0;
         for (int i = 0; i < nb; ++i) {

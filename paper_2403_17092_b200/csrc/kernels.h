@@ -45,7 +45,7 @@ void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t ep
 
 struct GridBarrier {
     unsigned count, gen;
-    unsigned nts, pad;
+    unsigned nts, pad;            // barriers so far; pad = nts at the last launch's start
     unsigned long long t0;        // kernel start (globaltimer, ns)
     unsigned long long t_end;     // last block's end (atomicMax)
     unsigned long long ts[32];    // ring of barrier-release times
@@ -70,6 +70,7 @@ struct SampleParams {
     uint64_t seed;
     int hops, shadow, slot;
     int32_t* icount;     // ShaDow: induced edges per node of S
+    int32_t* hubs;       // [3 + cap]: count, next, any, then (block << 27 | row) of transposed rows > 256
     unsigned long long* status;   // look-back words [sample_step_sites(hops) x grid]: tag << 32 | chunk sum
     GridBarrier* bar;
     HopIO hop[kMaxHops + 1];

@@ -131,7 +131,6 @@ __device__ int chunk_scan(Smem& sm, int n, F f, PUT put, unsigned long long* sta
 
 constexpr int kWarpSort = 256;                    // ints per warp slice of shared memory
 constexpr int kBlockSort = kWarps * kWarpSort;    // 8192 ints = 32 KB (keeps most of L1 as cache)
-constexpr int kMaxLong = 256;                     // hub rows queued per block and block
 
 // In-place ascending bitonic sort of s[0:n2) (n2 a power of two) by `nthr` cooperating
 // threads (thread index t), `sync` separating the stages.
@@ -263,6 +262,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         P.bar->t0 = t;
         P.bar->t_end = 0ull;
+        P.bar->pad = P.bar->nts;   // barrier count at launch (phase readout)
+        P.hubs[0] = 0;   // hub rows of the transposed sort: count, next, any (read after barriers)
+        P.hubs[1] = 0;
+        P.hubs[2] = 0;
         // the step's state (dst_0 = the seeds, in batch order)
         for (int h = 0; h <= kMaxHops; ++h) { st->n_dst[h] = 0; st->n_src[h] = 0; st->n_edges[h] = 0; }
         st->n_dst[0] = P.n_seeds;
@@ -347,11 +350,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
     if (P.full) relabel_edges(P, P.hop[L1], st->n_edges[L1], gtid, nthreads);
     const int nS = P.full ? st->n_src[L1] : st->n_dst[L1];   // nodes with a map entry
     if (P.shadow) {
+        // A warp per node of S walks its CSR row kIndU x 32 entries at a time (all loads of a
+        // round issued before any is used), so hub rows take few dependent round trips.
+        constexpr int kIndU = 8;
         for (int i = blockIdx.x * kWarps + wib; i < nS; i += G * kWarps) {   // |{u in row v : u in S}|
             const int v = P.nodes[i];
             int c = 0;
-            for (int64_t p = __ldg(P.row_ptr + v) + lane; p < __ldg(P.row_ptr + v + 1); p += 32)
-                c += P.map[__ldg(P.col + p)] >= 0;
+            const int64_t rb = __ldg(P.row_ptr + v), re = __ldg(P.row_ptr + v + 1);
+            for (int64_t p0 = rb; p0 < re; p0 += 32 * kIndU) {
+                int u[kIndU];
+#pragma unroll
+                for (int r = 0; r < kIndU; ++r) {
+                    const int64_t p = p0 + 32 * r + lane;
+                    u[r] = p < re ? __ldg(P.col + p) : -1;
+                }
+#pragma unroll
+                for (int r = 0; r < kIndU; ++r) c += (u[r] >= 0 && P.map[u[r]] >= 0) ? 1 : 0;
+            }
             for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
             if (lane == 0) P.icount[i] = c;
         }
@@ -363,25 +378,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
             S.rowptr[nS] = tot;
             st->n_dst[P.slot] = nS; st->n_src[P.slot] = nS; st->n_edges[P.slot] = tot;
         }
-        __syncthreads();
+        grid_sync(P.bar);   // every row offset visible: the fill below is interleaved over the grid
         // edges (local(u) -> i) in CSR order of row S[i] (R20)
-        int beg, end;
-        chunk_of(nS, beg, end);
-        for (int i = beg + wib; i < end; i += kWarps) {
+        for (int i = blockIdx.x * kWarps + wib; i < nS; i += G * kWarps) {
             const int v = P.nodes[i];
             int out = S.rowptr[i];
             const int64_t rb = __ldg(P.row_ptr + v), re = __ldg(P.row_ptr + v + 1);
-            for (int64_t p0 = rb; p0 < re; p0 += 32) {
-                const int64_t p = p0 + lane;
-                const int m = p < re ? P.map[__ldg(P.col + p)] : -1;
-                const unsigned bal = __ballot_sync(kFull, m >= 0);
-                if (m >= 0) {
-                    const int o = out + __popc(bal & ((1u << lane) - 1u));
-                    S.col[o] = m;
-                    S.erow[o] = i;
-                    atomicAdd(&S.tcount[m], 1);
+            for (int64_t p0 = rb; p0 < re; p0 += 32 * kIndU) {
+                int m[kIndU];
+#pragma unroll
+                for (int r = 0; r < kIndU; ++r) {
+                    const int64_t p = p0 + 32 * r + lane;
+                    m[r] = p < re ? __ldg(P.col + p) : -1;
                 }
-                out += __popc(bal);
+#pragma unroll
+                for (int r = 0; r < kIndU; ++r) m[r] = m[r] >= 0 ? P.map[m[r]] : -1;
+#pragma unroll
+                for (int r = 0; r < kIndU; ++r) {
+                    const unsigned bal = __ballot_sync(kFull, m[r] >= 0);
+                    if (m[r] >= 0) {
+                        const int o = out + __popc(bal & ((1u << lane) - 1u));
+                        S.col[o] = m[r];
+                        S.erow[o] = i;
+                        atomicAdd(&S.tcount[m[r]], 1);
+                    }
+                    out += __popc(bal);
+                }
             }
         }
     }
@@ -393,7 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         if (!H.tcount) continue;
         const int ns = st->n_src[h];
         const int tot = chunk_scan(sm, ns, [&](int u) { return H.tcount[u]; },
-                                   [&](int u, int ex, int) { H.trowptr[u] = ex; H.tcursor[u] = ex; H.tcount[u] = 0; },
+                                   [&](int u, int ex, int cnt) {
+                                       H.trowptr[u] = ex; H.tcursor[u] = ex; H.tcount[u] = 0;
+                                       if (cnt > kWarpSort) P.hubs[2] = 1;   // a hub row exists
+                                   },
                                    P.status + (site++) * G, tag);
         if (tot >= 0 && threadIdx.x == 0) H.trowptr[ns] = tot;
     }
@@ -405,83 +430,77 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         for (int e = gtid; e < ne; e += nthreads) H.tdst[atomicAdd(&H.tcursor[H.col[e]], 1)] = H.erow[e];
     }
     grid_sync(P.bar);
-    // sort every transposed row ascending (fixed summation order):
-    // <= 32 entries: shuffle rank sort; <= kWarpSort: bitonic sort in the warp's shared slice;
-    // longer rows (hubs): the whole block sorts them in shared memory, one at a time.
+    // sort every transposed row ascending (fixed summation order).
+    // Pass A: a warp takes 32 consecutive rows; rows of <= 8 entries (almost all) are sorted by
+    // their lane alone (sorting network in registers), rows of <= kWarpSort by the warp; longer
+    // rows (hubs) go to a global list.  Pass B (after a barrier): blocks take hub rows from the
+    // list one at a time (dynamic, so clustered hubs spread over the grid) and sort them
+    // block-wide in shared memory.
     extern __shared__ int dyn[];
-    __shared__ int s_long[kMaxLong];
-    __shared__ int s_nlong;
+    __shared__ int s_item;
+    const bool any_hub = P.hubs[2] != 0;
     int* wbuf = dyn + wib * kWarpSort;
     for (int h = 0; h <= P.hops; ++h) {
         const HopIO& H = P.hop[h];
         if (!H.tcount) continue;
         const int ns = st->n_src[h];
-        if (threadIdx.x == 0) s_nlong = 0;
-        __syncthreads();
-        // a warp takes 32 consecutive rows: rows of <= 8 entries (almost all) are sorted by their
-        // lane alone (sorting network in registers); longer rows by the whole warp, one by one
         for (int u0 = (blockIdx.x * kWarps + wib) * 32; u0 < ns; u0 += G * kWarps * 32) {
             const int ul = u0 + lane;
             const int lb = ul < ns ? H.trowptr[ul] : 0;
             const int ll = ul < ns ? H.trowptr[ul + 1] - lb : 0;
             if (ll <= 8) lane_sort8(H.tdst + lb, H.tdst_s + lb, ll);
-            unsigned longm = __ballot_sync(kFull, ll > 8);
+            if (ll > kWarpSort) P.hubs[3 + atomicAdd(&P.hubs[0], 1)] = (h << 27) | ul;
+            unsigned longm = __ballot_sync(kFull, ll > 8 && ll <= kWarpSort);
             while (longm) {
-            const int j = __ffs(longm) - 1;
-            longm &= longm - 1;
-            const int u = u0 + j;
-            const int b0 = __shfl_sync(kFull, lb, j);
-            const int len = __shfl_sync(kFull, ll, j);
-            if (len > kWarpSort) {                   // hub row: queue it for the block-wide sort
-                int slot = 0;
-                if (lane == 0) slot = atomicAdd(&s_nlong, 1);
-                slot = __shfl_sync(kFull, slot, 0);
-                if (slot < kMaxLong) { if (lane == 0) s_long[slot] = u; continue; }
-                for (int a = lane; a < len; a += 32) {   // queue full: rank counting in the warp
-                    const int x = H.tdst[b0 + a];
+                const int j = __ffs(longm) - 1;
+                longm &= longm - 1;
+                const int b0 = __shfl_sync(kFull, lb, j);
+                const int len = __shfl_sync(kFull, ll, j);
+                if (len <= 32) {
+                    const int x = lane < len ? H.tdst[b0 + lane] : INT_MAX;
                     int rank = 0;
-                    for (int b = 0; b < len; ++b) rank += (H.tdst[b0 + b] < x) ? 1 : 0;
-                    H.tdst_s[b0 + rank] = x;
+                    for (int q = 0; q < len; ++q) rank += (__shfl_sync(kFull, x, q) < x) ? 1 : 0;
+                    if (lane < len) H.tdst_s[b0 + rank] = x;
+                } else {
+                    int n2 = 64;
+                    while (n2 < len) n2 <<= 1;
+                    for (int a = lane; a < n2; a += 32) wbuf[a] = a < len ? H.tdst[b0 + a] : INT_MAX;
+                    __syncwarp();
+                    bitonic_sort(wbuf, n2, lane, 32, [] { __syncwarp(); });
+                    for (int a = lane; a < len; a += 32) H.tdst_s[b0 + a] = wbuf[a];
+                    __syncwarp();
                 }
-                continue;
-            }
-            if (len <= 32) {
-                const int x = lane < len ? H.tdst[b0 + lane] : INT_MAX;
-                int rank = 0;
-                for (int q = 0; q < len; ++q) rank += (__shfl_sync(kFull, x, q) < x) ? 1 : 0;
-                if (lane < len) H.tdst_s[b0 + rank] = x;
-            } else if (len <= kWarpSort) {
-                int n2 = 64;
-                while (n2 < len) n2 <<= 1;
-                for (int a = lane; a < n2; a += 32) wbuf[a] = a < len ? H.tdst[b0 + a] : INT_MAX;
-                __syncwarp();
-                bitonic_sort(wbuf, n2, lane, 32, [] { __syncwarp(); });
-                for (int a = lane; a < len; a += 32) H.tdst_s[b0 + a] = wbuf[a];
-                __syncwarp();
-            }
             }
         }
+    }
+    // pass B only when the transposed scan saw a row longer than kWarpSort (flag read after the
+    // fill's barrier, so every block takes the same branch)
+    const int nhubs = any_hub ? (grid_sync(P.bar), P.hubs[0]) : 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(&P.hubs[1], 1);
         __syncthreads();
-        const int nlong = min(s_nlong, kMaxLong);
-        for (int q = 0; q < nlong; ++q) {                // this block's hub rows: block-wide sort
-            const int u = s_long[q];
-            const int b0 = H.trowptr[u];
-            const int len = H.trowptr[u + 1] - b0;
-            if (len <= kBlockSort) {
-                int n2 = 2 * kWarpSort;
-                while (n2 < len) n2 <<= 1;
-                for (int a = threadIdx.x; a < n2; a += kThreads) dyn[a] = a < len ? H.tdst[b0 + a] : INT_MAX;
-                __syncthreads();
-                bitonic_sort(dyn, n2, threadIdx.x, kThreads, [] { __syncthreads(); });
-                for (int a = threadIdx.x; a < len; a += kThreads) H.tdst_s[b0 + a] = dyn[a];
-                __syncthreads();
-            } else {                                       // beyond shared memory: rank counting
-                for (int a = threadIdx.x; a < len; a += kThreads) {
-                    const int x = H.tdst[b0 + a];
-                    int rank = 0;
-                    for (int b = 0; b < len; ++b) rank += (H.tdst[b0 + b] < x) ? 1 : 0;
-                    H.tdst_s[b0 + rank] = x;
-                }
+        const int q = s_item;
+        __syncthreads();
+        if (q >= nhubs) break;
+        const int item = P.hubs[3 + q];
+        const HopIO& H = P.hop[item >> 27];
+        const int u = item & ((1 << 27) - 1);
+        const int b0 = H.trowptr[u];
+        const int len = H.trowptr[u + 1] - b0;
+        if (len <= kBlockSort) {
+            int n2 = 2 * kWarpSort;
+            while (n2 < len) n2 <<= 1;
+            for (int a = threadIdx.x; a < n2; a += kThreads) dyn[a] = a < len ? H.tdst[b0 + a] : INT_MAX;
+            __syncthreads();
+            bitonic_sort(dyn, n2, threadIdx.x, kThreads, [] { __syncthreads(); });
+            for (int a = threadIdx.x; a < len; a += kThreads) H.tdst_s[b0 + a] = dyn[a];
+            __syncthreads();
+        } else {                                       // beyond shared memory: rank counting
+            for (int a = threadIdx.x; a < len; a += kThreads) {
+                const int x = H.tdst[b0 + a];
+                int rank = 0;
+                for (int b = 0; b < len; ++b) rank += (H.tdst[b0 + b] < x) ? 1 : 0;
+                H.tdst_s[b0 + rank] = x;
             }
         }
     }
