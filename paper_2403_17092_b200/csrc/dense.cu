@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
             if (lane < m && t < dlim) {
                 myi = t;
                 const float din = (float)(rowptr[t + 1] - rowptr[t] + (GCN ? 1 : 0));
-                myd = GCN ? 1.0f / sqrtf(din * dout) : din;
+                // edge weight: GCN 1/sqrt(d_in d_out), SAGE 1/deg(dst) (one division per edge, not
+                // per element: the backward of the mean is fma(1/deg, dM, acc))
+                myd = GCN ? 1.0f / sqrtf(din * dout) : 1.0f / din;
             }
             int q = 0;
             for (; q + 2 <= m; q += 2) {   // two dA rows in flight; accumulation in edge order
@@ -271,8 +273,8 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
                 }
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
-                    if (i0 >= 0) acc[c] = GCN ? f4fma(d0, v0[c], acc[c]) : f4add(acc[c], f4div(v0[c], d0));
-                    if (i1 >= 0) acc[c] = GCN ? f4fma(d1, v1[c], acc[c]) : f4add(acc[c], f4div(v1[c], d1));
+                    if (i0 >= 0) acc[c] = f4fma(d0, v0[c], acc[c]);
+                    if (i1 >= 0) acc[c] = f4fma(d1, v1[c], acc[c]);
                 }
             }
             if (q < m) {
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
                         const int ch = lane + 32 * c;
                         if (ch < nch) {
                             const float4 v = __ldg(p0 + ch);
-                            acc[c] = GCN ? f4fma(d0, v, acc[c]) : f4add(acc[c], f4div(v, d0));
+                            acc[c] = f4fma(d0, v, acc[c]);
                         }
                     }
                 }
