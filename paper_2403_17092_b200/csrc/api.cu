@@ -505,8 +505,11 @@ gnn_status step_from_perm(gnn_model* m, int64_t epoch, int64_t step) {
         cur = other_set(m);
         TRY(issue_sample_step(m, cur, epoch, step));
     }
+    // training is enqueued first, the next step's sampling after it: the GPU then never waits
+    // for the host between steps (the sampling runs while the host comes back for the next call)
+    TRY(train_set(m, cur));
     if (m->overlap && !m->profiling && step + 1 < steps_per_epoch(m)) TRY(issue_sample_step(m, 1 - cur, epoch, step + 1));
-    return train_set(m, cur);
+    return GNN_OK;
 }
 
 gnn_status sync_all(gnn_model* m) {
@@ -1089,10 +1092,10 @@ gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t
         cur = other_set(m);
         TRY(issue_sample(m, cur, nullptr, seeds_host, n_seeds, b_total, epoch, g, m->full_train));
     }
-    if (prefetch && m->overlap && !m->profiling)
-        TRY(issue_sample(m, 1 - cur, nullptr, next_seeds_host, next_n, next_b_total, epoch, next_g, m->full_train));
     TRY(train_set(m, cur));
     CK(cudaMemcpyAsync(loss_out_host, &m->bs[cur].st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
+    if (prefetch && m->overlap && !m->profiling)   // after the training launch (see step_from_perm)
+        TRY(issue_sample(m, 1 - cur, nullptr, next_seeds_host, next_n, next_b_total, epoch, next_g, m->full_train));
     CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }

@@ -16,8 +16,8 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
 __device__ __forceinline__ float4 f4fma(float w, float4 v, float4 a) {   // a + w*v
     return make_float4(a.x + w * v.x, a.y + w * v.y, a.z + w * v.z, a.w + w * v.w);
 }
-__device__ __forceinline__ float4 f4div(float4 a, float d) {
-    return make_float4(a.x / d, a.y / d, a.z / d, a.w / d);
+__device__ __forceinline__ float4 f4scale(float4 a, float w) {
+    return make_float4(a.x * w, a.y * w, a.z * w, a.w * w);
 }
 __device__ __forceinline__ uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
     return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
@@ -130,12 +130,13 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             }
         }
         const int deg = end - beg;
+        const float inv = deg ? 1.0f / (float)deg : 0.f;   // one division per row (R23)
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
             if (ch < nch) {
                 store_split4(A, i * lda + 4 * ch, sv[c]);
-                store_split4(A, i * lda + 4 * (nch + ch), deg ? f4div(acc[c], (float)deg) : kZero4);
+                store_split4(A, i * lda + 4 * (nch + ch), f4scale(acc[c], inv));
             }
         }
     }
