@@ -342,8 +342,15 @@ __global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
         for (int64_t f = tid; f < total; f += nth) {
             const int r = (int)(f / L.out), c = (int)(f % L.out);
             const int rp = P.sage ? (r / L.in) * L.in_pad + (r % L.in) : r;
+            const float* src = L.part + (int64_t)rp * L.n_pad + c;
             float s = 0.f;
-            for (int z = 0; z < L.splits; ++z) s += L.part[z * L.split_stride + (int64_t)rp * L.n_pad + c];
+            for (int z0 = 0; z0 < L.splits; z0 += 8) {   // fixed split order; 8 partials in flight
+                float v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = z0 + j < L.splits ? src[(z0 + j) * L.split_stride] : 0.f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) if (z0 + j < L.splits) s += v[j];
+            }
             grads[L.poff + f] = s;
         }
     }
@@ -372,9 +379,15 @@ __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restr
             float w = params[idx];
             if (grads) {
                 float gr;
-                if (reduce) {
+                if (reduce) {   // fixed split order; 8 partials in flight per round
                     gr = 0.f;
-                    for (int z = 0; z < L.splits; ++z) gr += L.part[z * L.split_stride + f];
+                    for (int z0 = 0; z0 < L.splits; z0 += 8) {
+                        float v[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) v[j] = z0 + j < L.splits ? L.part[(z0 + j) * L.split_stride + f] : 0.f;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) if (z0 + j < L.splits) gr += v[j];
+                    }
                     grads[idx] = gr;
                 } else {
                     gr = grads[idx];
@@ -498,7 +511,7 @@ void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s) {
 }
 
 void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, cudaStream_t s) {
-    launch_pdl(k_sgd_pack, 148 * 2, 256, 0, s, p, params, grads, lr, reduce ? 1 : 0);
+    launch_pdl(k_sgd_pack, reduce ? 148 * 8 : 148 * 2, 256, 0, s, p, params, grads, lr, reduce ? 1 : 0);
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,

@@ -390,27 +390,35 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                     }
                     float s = 0.f;
 #pragma unroll
-                    for (int c = 0; c < kZ; ++c)
-                        if (c < C) s += expf(__uint_as_float(zr[c >> 5][c & 31]) - mx);
+                    for (int c = 0; c < kZ; ++c) {   // e_c = exp(z_c - max) kept in place
+                        const float e = c < C ? expf(__uint_as_float(zr[c >> 5][c & 31]) - mx) : 0.f;
+                        zr[c >> 5][c & 31] = __float_as_uint(e);
+                        s += e;
+                    }
+                    const float inv_s = 1.0f / s;
 #pragma unroll
-                    for (int c = 0; c < BN; c += 2) {
-                        float d0 = 0.f, d1 = 0.f;
-                        if (c < C) d0 = (expf(__uint_as_float(zr[c >> 5][c & 31]) - mx) / s - (c == y ? 1.f : 0.f)) * inv_bt;
-                        if (c + 1 < C) d1 = (expf(__uint_as_float(zr[(c + 1) >> 5][(c + 1) & 31]) - mx) / s - (c + 1 == y ? 1.f : 0.f)) * inv_bt;
-                        const __nv_bfloat162 hi = __floats2bfloat162_rn(d0, d1);
-                        *reinterpret_cast<__nv_bfloat162*>(args.dz.hi + zoff + c) = hi;
-                        if (args.dz.lo)
-                            *reinterpret_cast<__nv_bfloat162*>(args.dz.lo + zoff + c) =
-                                __floats2bfloat162_rn(d0 - __low2float(hi), d1 - __high2float(hi));
+                    for (int c = 0; c < BN; c += 8) {   // dZ = (e/s - onehot)/b_total, 16-byte stores
+                        uint32_t hw[4], lw[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int c0 = c + 2 * q, c1 = c0 + 1;
+                            const float d0 = c0 < C ? (__uint_as_float(zr[c0 >> 5][c0 & 31]) * inv_s - (c0 == y ? 1.f : 0.f)) * inv_bt : 0.f;
+                            const float d1 = c1 < C ? (__uint_as_float(zr[c1 >> 5][c1 & 31]) * inv_s - (c1 == y ? 1.f : 0.f)) * inv_bt : 0.f;
+                            const __nv_bfloat162 hi = __floats2bfloat162_rn(d0, d1);
+                            const __nv_bfloat162 lo = __floats2bfloat162_rn(d0 - __low2float(hi), d1 - __high2float(hi));
+                            hw[q] = *reinterpret_cast<const uint32_t*>(&hi);
+                            lw[q] = *reinterpret_cast<const uint32_t*>(&lo);
+                        }
+                        *reinterpret_cast<uint4*>(args.dz.hi + zoff + c) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                        if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + zoff + c) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
                     }
                     args.st->row_loss[row] = (mx + logf(s)) - zy;
                     __threadfence();
                 } else if (row < ((M + 63) & ~63)) {      // zero tail rows of the dZ planes
-                    const __nv_bfloat162 zz = __floats2bfloat162_rn(0.f, 0.f);
 #pragma unroll
-                    for (int c = 0; c < BN; c += 2) {
-                        *reinterpret_cast<__nv_bfloat162*>(args.dz.hi + zoff + c) = zz;
-                        if (args.dz.lo) *reinterpret_cast<__nv_bfloat162*>(args.dz.lo + zoff + c) = zz;
+                    for (int c = 0; c < BN; c += 8) {
+                        *reinterpret_cast<uint4*>(args.dz.hi + zoff + c) = make_uint4(0u, 0u, 0u, 0u);
+                        if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + zoff + c) = make_uint4(0u, 0u, 0u, 0u);
                     }
                 }
             }
