@@ -258,9 +258,11 @@ void enqueue_training(gnn_model* m, int set) {
         if (m->sage) {
             // layer 1 of the neighbour sampler reads X rows directly by global neighbour id
             const bool direct = li == 0 && !m->shadow;
+            // the training-only sampling run writes the last hop fixed-stride (no count scan)
+            const int fixed_k = direct && !m->full_train ? m->bs[set].sp.hop[blk].k : 0;
             K(m, s, kid, [&] {
                 launch_agg_sage(rows, Hrows, ly.in_pad, direct ? nullptr : self_ids, self_ids, B.rowptr[blk],
-                                direct ? B.nbr[blk] : B.col[blk], ly.A, s);
+                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, s);
             });
         } else {
             K(m, s, kid, [&] {

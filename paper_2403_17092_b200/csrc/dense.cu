@@ -59,7 +59,7 @@ template <int CPL>
 __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ rows_ptr,
         FeatRows H, int in_pad, const int32_t* __restrict__ gmap,
         const int32_t* __restrict__ smap, const int32_t* __restrict__ rowptr,
-        const int32_t* __restrict__ col, Split A) {
+        const int32_t* __restrict__ col, Split A, int fixed_k) {
     pdl_trigger();
     pdl_wait();
     const int n = *rows_ptr;
@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
         float4 sv[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) sv[c] = (lane + 32 * c) < nch ? __ldg(ps + lane + 32 * c) : kZero4;
-        const int beg = rowptr[i], end = rowptr[i + 1];
+        // CSR rows, or fixed-stride rows (row i at col[i*k], count in rowptr[i])
+        const int beg = fixed_k ? i * fixed_k : rowptr[i];
+        const int end = fixed_k ? beg + rowptr[i] : rowptr[i + 1];
         float4 acc[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
@@ -475,9 +477,9 @@ int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
     }
 
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
-                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A,
+                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
                      cudaStream_t s) {
-    GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A);
+    GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A, fixed_k);
 }
 
 void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,

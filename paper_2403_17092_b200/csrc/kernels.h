@@ -112,8 +112,10 @@ struct FeatRows {
 // SAGE-mean aggregation into A = [H_self | mean] for rows i < *rows_ptr.  Neighbour row of
 // source c is gmap ? gmap[c] : c, self row smap ? smap[i] : i (layer 1 reads X by global id:
 // the fused feature gather).
+// fixed_k > 0: the block is fixed-stride (row i's sources at col[i*fixed_k], count in
+// blk_rowptr[i]; the training-only last hop of the sampling kernel).
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
-                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A,
+                     const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
                      cudaStream_t s);
 // GCN aggregation A = Â H (self loop included) for rows i < *rows_ptr of a block with
 // *ndst_ptr destinations; d_out from the transposed row pointer.  col must be local ids.

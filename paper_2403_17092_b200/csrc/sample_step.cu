@@ -184,9 +184,12 @@ __device__ __forceinline__ int min_deg(const int64_t* row_ptr, int v, int k) {
 // independent of the picks, so they run in parallel); a k-step ballot resolve replaces a
 // taken t_i by j_i; a shuffle rank-sort writes the picks in ascending CSR position.  Rows with
 // d <= k are copied whole.  Several nodes per warp keep more dependent loads in flight.
+// fixed: the block is written with a fixed stride of k slots per row (row i at nbr[i*k],
+// its count in rowptr[i]) instead of CSR — the last hop of a training-only run, whose only
+// reader is the layer-1 aggregation; no count scan is needed.
 template <int GS>
 __device__ __forceinline__ void sample_nodes(const SampleParams& P, int h, int k, int i, bool valid, uint32_t epoch,
-                                             uint32_t g, int lane, bool mark) {
+                                             uint32_t g, int lane, bool mark, bool fixed) {
     const HopIO& H = P.hop[h];
     const int32_t* dst = h == 0 ? P.seed_src : P.nodes;   // hop 0: the seeds, read at their source
     const int lg = lane & (GS - 1);
@@ -197,7 +200,8 @@ __device__ __forceinline__ void sample_nodes(const SampleParams& P, int h, int k
         v = dst[i];
         start = __ldg(P.row_ptr + v);
         d = (int)(__ldg(P.row_ptr + v + 1) - start);
-        out = H.rowptr[i];
+        out = fixed ? i * k : H.rowptr[i];
+        if (fixed && (lane & (GS - 1)) == 0) H.rowptr[i] = d < k ? d : k;
     }
     const bool floyd = d > k;
     const int j = d - k + lg;
@@ -233,11 +237,11 @@ __device__ __forceinline__ void sample_nodes(const SampleParams& P, int h, int k
 
 template <int GS>
 __device__ __forceinline__ void sample_chunk(const SampleParams& P, int h, int k, int beg, int end, uint32_t epoch,
-                                             uint32_t g, int lane, int wib, bool mark) {
+                                             uint32_t g, int lane, int wib, bool mark, bool fixed) {
     constexpr int kPerWarp = 32 / GS;
     for (int i0 = beg + wib * kPerWarp; i0 < end; i0 += kWarps * kPerWarp) {
         const int i = i0 + lane / GS;
-        sample_nodes<GS>(P, h, k, i, i < end, epoch, g, lane, mark);
+        sample_nodes<GS>(P, h, k, i, i < end, epoch, g, lane, mark, fixed);
     }
 }
 
@@ -294,14 +298,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
         const int nd = h == 0 ? P.n_seeds : st->n_dst[h];
         const int32_t* dst = h == 0 ? P.seed_src : P.nodes;
         {
-            const int tot = chunk_scan(sm, nd, [&](int i) { return min_deg(P.row_ptr, dst[i], k); },
-                                       [&](int i, int ex, int) { H.rowptr[i] = ex; }, P.status + (site++) * G, tag);
-            if (tot >= 0 && threadIdx.x == 0) { H.rowptr[nd] = tot; st->n_edges[h] = tot; }
+            const bool fixed = !mark;   // training-only last hop: fixed-stride rows, no scan
+            if (!fixed) {
+                const int tot = chunk_scan(sm, nd, [&](int i) { return min_deg(P.row_ptr, dst[i], k); },
+                                           [&](int i, int ex, int) { H.rowptr[i] = ex; }, P.status + (site++) * G, tag);
+                if (tot >= 0 && threadIdx.x == 0) { H.rowptr[nd] = tot; st->n_edges[h] = tot; }
+            } else {
+                ++site;
+            }
             int beg, end;
             chunk_of(nd, beg, end);
-            if (k <= 8) sample_chunk<8>(P, h, k, beg, end, epoch, g, lane, wib, mark);
-            else if (k <= 16) sample_chunk<16>(P, h, k, beg, end, epoch, g, lane, wib, mark);
-            else sample_chunk<32>(P, h, k, beg, end, epoch, g, lane, wib, mark);
+            if (k <= 8) sample_chunk<8>(P, h, k, beg, end, epoch, g, lane, wib, mark, fixed);
+            else if (k <= 16) sample_chunk<16>(P, h, k, beg, end, epoch, g, lane, wib, mark, fixed);
+            else sample_chunk<32>(P, h, k, beg, end, epoch, g, lane, wib, mark, fixed);
         }
         grid_sync(P.bar);
         if (!mark) break;
