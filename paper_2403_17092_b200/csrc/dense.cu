@@ -87,15 +87,6 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             const int m = min(32, end - e0);
             int myidx = 0;
             if (lane < m) { const int c = col[e0 + lane]; myidx = gmap ? gmap[c] : c; }
-            {   // every neighbour row of this chunk to L2 at once (no registers held): the loads
-                // below then wait for L2, not DRAM, after the first batch
-                const int nl = (in_pad * 4 + 127) >> 7;
-                for (int t0 = 0; t0 < m * nl; t0 += 32) {   // warp-uniform trip count
-                    const int t = t0 + lane;
-                    const int r = __shfl_sync(kFull, myidx, min(t / nl, 31));
-                    if (t < m * nl) asm volatile("prefetch.global.L2 [%0];" ::"l"(H.row(r, in_pad) + (t % nl) * 32));
-                }
-            }
             int q = 0;
             // kAggU neighbour rows in flight per warp (memory-level parallelism of the gather);
             // the adds stay in CSR order
