@@ -813,8 +813,11 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
             if (r == GNN_OK) { cudaMemset(sp.hi, 0, 2 * count); if (sp.lo) cudaMemset(sp.lo, 0, 2 * count); }
             return r;
         };
-        if ((s = split(ly.A, ly.rows_alloc * ly.k_pad)) != GNN_OK) return cleanup(s);
-        if ((s = split(ly.dPre, ly.rows_alloc * ly.n_pad)) != GNN_OK) return cleanup(s);
+        // activation / gradient operand planes are k-block-tiled (Split::rows, kernels.h)
+        if ((s = split(ly.A, ly.rows_alloc * round_up(ly.k_pad, 64))) != GNN_OK) return cleanup(s);
+        if ((s = split(ly.dPre, ly.rows_alloc * round_up(ly.n_pad, 64))) != GNN_OK) return cleanup(s);
+        ly.A.rows = ly.rows_alloc;
+        ly.dPre.rows = ly.rows_alloc;
         if ((s = split(ly.Wkn, (int64_t)ly.k_pad * ly.n_pad)) != GNN_OK) return cleanup(s);
         AL(ly.H, ly.m_cap * ly.n_pad);
         if (li > 0) AL(ly.dA, ly.m_cap * ly.k_pad);
@@ -823,18 +826,18 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         auto lo_or_hi = [](const Split& sp) { return sp.lo ? (const void*)sp.lo : (const void*)sp.hi; };
         bool ok = true;
         const int bn_d = tc_tile_n(ly.k_pad);
-        ok &= make_tmap_bf16(&ly.map_fwd.a_hi, ly.A.hi, ly.rows_alloc, ly.k_pad, 128);
-        ok &= make_tmap_bf16(&ly.map_fwd.a_lo, lo_or_hi(ly.A), ly.rows_alloc, ly.k_pad, 128);
+        ok &= make_tmap_bf16_tiled(&ly.map_fwd.a_hi, ly.A.hi, ly.rows_alloc, ly.k_pad, 128);
+        ok &= make_tmap_bf16_tiled(&ly.map_fwd.a_lo, lo_or_hi(ly.A), ly.rows_alloc, ly.k_pad, 128);
         ok &= make_tmap_bf16(&ly.map_fwd.b_hi, ly.Wkn.hi, ly.k_pad, ly.n_pad, 64);     // MN-major B
         ok &= make_tmap_bf16(&ly.map_fwd.b_lo, lo_or_hi(ly.Wkn), ly.k_pad, ly.n_pad, 64);
-        ok &= make_tmap_bf16(&ly.map_dgrad.a_hi, ly.dPre.hi, ly.rows_alloc, ly.n_pad, 128);
-        ok &= make_tmap_bf16(&ly.map_dgrad.a_lo, lo_or_hi(ly.dPre), ly.rows_alloc, ly.n_pad, 128);
+        ok &= make_tmap_bf16_tiled(&ly.map_dgrad.a_hi, ly.dPre.hi, ly.rows_alloc, ly.n_pad, 128);
+        ok &= make_tmap_bf16_tiled(&ly.map_dgrad.a_lo, lo_or_hi(ly.dPre), ly.rows_alloc, ly.n_pad, 128);
         ok &= make_tmap_bf16(&ly.map_dgrad.b_hi, ly.Wkn.hi, ly.k_pad, ly.n_pad, bn_d);
         ok &= make_tmap_bf16(&ly.map_dgrad.b_lo, lo_or_hi(ly.Wkn), ly.k_pad, ly.n_pad, bn_d);
-        ok &= make_tmap_bf16(&ly.map_wgrad.a_hi, ly.A.hi, ly.rows_alloc, ly.k_pad, 64);
-        ok &= make_tmap_bf16(&ly.map_wgrad.a_lo, lo_or_hi(ly.A), ly.rows_alloc, ly.k_pad, 64);
-        ok &= make_tmap_bf16(&ly.map_wgrad.b_hi, ly.dPre.hi, ly.rows_alloc, ly.n_pad, 64);
-        ok &= make_tmap_bf16(&ly.map_wgrad.b_lo, lo_or_hi(ly.dPre), ly.rows_alloc, ly.n_pad, 64);
+        ok &= make_tmap_bf16_tiled(&ly.map_wgrad.a_hi, ly.A.hi, ly.rows_alloc, ly.k_pad, 64);
+        ok &= make_tmap_bf16_tiled(&ly.map_wgrad.a_lo, lo_or_hi(ly.A), ly.rows_alloc, ly.k_pad, 64);
+        ok &= make_tmap_bf16_tiled(&ly.map_wgrad.b_hi, ly.dPre.hi, ly.rows_alloc, ly.n_pad, 64);
+        ok &= make_tmap_bf16_tiled(&ly.map_wgrad.b_lo, lo_or_hi(ly.dPre), ly.rows_alloc, ly.n_pad, 64);
         ok &= make_tmap_f32(&ly.map_fwd.c, ly.H, ly.m_cap, ly.n_pad, ly.n_pad, 1, 0);
         ok &= make_tmap_f32(&ly.map_wgrad.c, ly.wpart, ly.k_pad, ly.n_pad, ly.n_pad, ly.splits,
                             (int64_t)ly.k_pad * ly.n_pad);

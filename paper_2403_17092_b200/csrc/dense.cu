@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
     const int64_t lda = 2 * (int64_t)in_pad;
     for (int i = global_warp(); i < nr; i += total_warps()) {
         if (i >= n) {                                   // zero tail rows of the operand planes
-            for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, i * lda + 4 * ch, kZero4);
+            for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, tix(A, i, 4 * ch), kZero4);
             continue;
         }
         // the self row does not depend on the edge chain: issue its loads first
@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
             if (ch < nch) {
-                store_split4(A, i * lda + 4 * ch, sv[c]);
-                store_split4(A, i * lda + 4 * (nch + ch), f4scale(acc[c], inv));
+                store_split4(A, tix(A, i, 4 * ch), sv[c]);
+                store_split4(A, tix(A, i, 4 * (nch + ch)), f4scale(acc[c], inv));
             }
         }
     }
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
     const int nch = in_pad >> 2;
     for (int i = global_warp(); i < nr; i += total_warps()) {
         if (i >= n) {
-            for (int ch = lane; ch < (lda >> 2); ch += 32) store_split4(A, (int64_t)i * lda + 4 * ch, kZero4);
+            for (int ch = lane; ch < (lda >> 2); ch += 32) store_split4(A, tix(A, i, 4 * ch), kZero4);
             continue;
         }
         const int beg = rowptr[i], end = rowptr[i + 1];
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
-            if (ch < nch) store_split4(A, (int64_t)i * lda + 4 * ch, f4fma(ws, __ldg(ps + ch), acc[c]));
+            if (ch < nch) store_split4(A, tix(A, i, 4 * ch), f4fma(ws, __ldg(ps + ch), acc[c]));
         }
     }
 }
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
     if (lane < ce - cb) ci = tdst[cb + lane];
     for (; u < nr; u += W) {
         if (u >= nsrc) {
-            for (int ch = lane; ch < nch; ch += 32) store_split4(dPre, (int64_t)u * in_pad + 4 * ch, kZero4);
+            for (int ch = lane; ch < nch; ch += 32) store_split4(dPre, tix(dPre, u, 4 * ch), kZero4);
             continue;
         }
         const int un = u + W;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
                 // ReLU'(pre) = [H > 0]  (ReLU'(0) = 0)
                 a.x = hv[c].x > 0.f ? a.x : 0.f; a.y = hv[c].y > 0.f ? a.y : 0.f;
                 a.z = hv[c].z > 0.f ? a.z : 0.f; a.w = hv[c].w > 0.f ? a.w : 0.f;
-                store_split4(dPre, (int64_t)u * in_pad + 4 * ch, a);
+                store_split4(dPre, tix(dPre, u, 4 * ch), a);
             }
         }
         cb = nb;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(256) k_ce(StepState* st, const float* __restri
     const int lane = lane_id();
     for (int r = global_warp(); r < br; r += total_warps()) {
         if (r >= b) {
-            for (int c = lane; c < ldz; c += 32) store_split1(dZ, (int64_t)r * ldz + c, 0.f);
+            for (int c = lane; c < ldz; c += 32) store_split1(dZ, tix(dZ, r, c), 0.f);
             continue;
         }
         const float* z = Z + (int64_t)r * ldz;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256) k_ce(StepState* st, const float* __restri
         for (int c = lane; c < ldz; c += 32) {
             float v = 0.f;
             if (c < C) v = (expf(z[c] - m) / s - (c == y ? 1.f : 0.f)) * inv_bt;
-            store_split1(dZ, (int64_t)r * ldz + c, v);
+            store_split1(dZ, tix(dZ, r, c), v);
         }
         if (lane == 0) row_loss[r] = (m + logf(s)) - z[y];
     }

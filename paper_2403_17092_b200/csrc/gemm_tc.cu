@@ -16,6 +16,7 @@
 // = TMA producer, warp 1 = TMEM allocator + MMA issuer, warps 2..5 = epilogue (one TMEM lane
 // quarter each).  Two TMEM accumulators: the epilogue of tile j overlaps the MMAs of tile j+1.
 #include <cuda.h>
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "kernels.h"
@@ -58,6 +59,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
 // TMA store of a swizzled shared-memory box (bulk-group completion); C maps are always 3-D.
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
@@ -150,6 +159,7 @@ struct GemmArgs {
     const int32_t* nodes;
     Split dz;               // dZ planes [rows x ldc]
     int classes;
+    int diag;               // profiling diagnostics only (env GS_GEMM_DIAG): 1 skip C stores, 2 skip MMAs
 };
 
 struct TileInfo { int tm, tn, z, kb0, nkb; };
@@ -242,20 +252,28 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                     uint8_t* b_lo = a_lo + Cfg::kAStage;
                     mbar_expect_tx(&full_bar[s], kAPlanes * (Cfg::kAStage + (B_MN ? Cfg::kBBytesMN : Cfg::kBBytesK)));
                     const int k0 = (ti.kb0 + kb) * kBK;
-                    if (!A_MN) {          // K-major: box {64 (k), 128 rows}
-                        tma_load_2d(a_hi, &mA_hi, &full_bar[s], k0, tile_m);
-                        if (TERMS == 3) tma_load_2d(a_lo, &mA_lo, &full_bar[s], k0, tile_m);
+                    // A planes are k-block-tiled (3-D maps {64, rows, k-block}): every box is one
+                    // contiguous block of HBM
+                    if (!A_MN) {          // K-major: box {64 (k), 128 rows} of k-block k0/64
+                        tma_load_3d(a_hi, &mA_hi, &full_bar[s], 0, tile_m, k0 >> 6);
+                        if (TERMS == 3) tma_load_3d(a_lo, &mA_lo, &full_bar[s], 0, tile_m, k0 >> 6);
                     } else {              // MN-major: boxes {64 (m), 64 (k rows)}, 8 KB apart
 #pragma unroll
                         for (int j = 0; j < kBM / 64; ++j) {
-                            tma_load_2d(a_hi + j * 8192, &mA_hi, &full_bar[s], tile_m + 64 * j, k0);
-                            if (TERMS == 3) tma_load_2d(a_lo + j * 8192, &mA_lo, &full_bar[s], tile_m + 64 * j, k0);
+                            tma_load_3d(a_hi + j * 8192, &mA_hi, &full_bar[s], 0, k0, (tile_m >> 6) + j);
+                            if (TERMS == 3) tma_load_3d(a_lo + j * 8192, &mA_lo, &full_bar[s], 0, k0, (tile_m >> 6) + j);
                         }
                     }
                     if (!B_MN) {
                         tma_load_2d(b_hi, &mB_hi, &full_bar[s], k0, tile_n);
                         if (TERMS == 3) tma_load_2d(b_lo, &mB_lo, &full_bar[s], k0, tile_n);
-                    } else {
+                    } else if (MODE == 1) {   // dPre planes (tiled), MN-major
+#pragma unroll
+                        for (int j = 0; j < (BN + 63) / 64; ++j) {
+                            tma_load_3d(b_hi + j * 8192, &mB_hi, &full_bar[s], 0, k0, (tile_n >> 6) + j);
+                            if (TERMS == 3) tma_load_3d(b_lo + j * 8192, &mB_lo, &full_bar[s], 0, k0, (tile_n >> 6) + j);
+                        }
+                    } else {                  // W [K x N] as stored, MN-major
 #pragma unroll
                         for (int j = 0; j < (BN + 63) / 64; ++j) {
                             tma_load_2d(b_hi + j * 8192, &mB_hi, &full_bar[s], tile_n + 64 * j, k0);
@@ -295,6 +313,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                         const uint32_t oa = A_MN ? kk * 2048 : kk * 32, ob = B_MN ? kk * 2048 : kk * 32;
                         const uint32_t la = A_MN ? 8192 : 16, lb = B_MN ? 8192 : 16, sbo = 1024;
                         const uint64_t dah = sdesc(a_hi + oa, la, sbo), dbh = sdesc(b_hi + ob, lb, sbo);
+                        if ((args.diag & 2) && (kb > 0 || kk > 0)) continue;
                         tc_mma(d, dah, dbh, id, (kb > 0 || kk > 0) ? 1u : 0u);
                         if (TERMS == 3) {
                             const uint64_t dal = sdesc(a_lo + oa, la, sbo), dbl = sdesc(b_lo + ob, lb, sbo);
@@ -360,7 +379,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                 }
                 fence_async_smem();
                 __syncwarp();
-                if (lane == 0) {
+                if (lane == 0 && !(args.diag & 1)) {
                     tma_store_3d(&mC, ebuf, tile_n + c0, row0, ti.z);
                     if (two) tma_store_3d(&mC, ebuf + kEpiBuf, tile_n + c0 + kEpiCols, row0, ti.z);
                     bulk_commit();
@@ -378,7 +397,6 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                 const int row = row0 + lane;
                 const int C = args.classes;
                 const float inv_bt = 1.0f / (float)max(args.st->b_total, 1);
-                const int64_t zoff = (int64_t)row * args.ldc;
                 if (row < M) {
                     const int y = args.labels[args.nodes[row]];
                     float mx = -INFINITY, zy = 0.f;
@@ -409,16 +427,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                             hw[q] = *reinterpret_cast<const uint32_t*>(&hi);
                             lw[q] = *reinterpret_cast<const uint32_t*>(&lo);
                         }
-                        *reinterpret_cast<uint4*>(args.dz.hi + zoff + c) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                        if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + zoff + c) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                        *reinterpret_cast<uint4*>(args.dz.hi + tix(args.dz, row, c)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                        if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + tix(args.dz, row, c)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
                     }
                     args.st->row_loss[row] = (mx + logf(s)) - zy;
                     __threadfence();
                 } else if (row < ((M + 63) & ~63)) {      // zero tail rows of the dZ planes
 #pragma unroll
                     for (int c = 0; c < BN; c += 8) {
-                        *reinterpret_cast<uint4*>(args.dz.hi + zoff + c) = make_uint4(0u, 0u, 0u, 0u);
-                        if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + zoff + c) = make_uint4(0u, 0u, 0u, 0u);
+                        *reinterpret_cast<uint4*>(args.dz.hi + tix(args.dz, row, c)) = make_uint4(0u, 0u, 0u, 0u);
+                        if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + tix(args.dz, row, c)) = make_uint4(0u, 0u, 0u, 0u);
                     }
                 }
             }
@@ -488,6 +506,19 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t co
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// k-block-tiled bf16 plane: {64, rows, ceil(cols/64)}, box {64, box_rows, 1}, 128B swizzle.
+bool make_tmap_bf16_tiled(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+    EncodeFn fn = encode_fn();
+    if (!fn || !base) return false;
+    cuuint64_t dims[3] = {64u, (cuuint64_t)rows, (cuuint64_t)((cols + 63) / 64)};
+    cuuint64_t strides[2] = {128u, (cuuint64_t)rows * 128u};
+    cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // fp32 [depth x rows x cols] (cols contiguous, row stride ld elements, depth stride dstride
 // elements), box {32, 32, 1}, 128B swizzle: the GEMM epilogue's store target.
 bool make_tmap_f32(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int64_t depth,
@@ -550,6 +581,15 @@ int tc_tile_n(int n_pad) {
     return 128;
 }
 
+static int gemm_diag() {
+    static int d = -1;
+    if (d < 0) {
+        const char* e = getenv("GS_GEMM_DIAG");
+        d = e ? atoi(e) : 0;
+    }
+    return d;
+}
+
 cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_static,
                            int m_cap, int n_pad, int k_pad, float* C, int ldc, int n_store, bool relu, int splits,
                            int64_t split_stride, cudaStream_t s) {
@@ -567,6 +607,7 @@ cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const 
     a.ldc = ldc;
     a.relu = relu ? 1 : 0;
     a.split_stride = split_stride;
+    a.diag = gemm_diag();
     int tiles_cap;
     if (mode != 1) tiles_cap = a.m_tiles_cap * a.n_tiles;
     else tiles_cap = ((m_static + kBM - 1) / kBM) * a.n_tiles * splits;

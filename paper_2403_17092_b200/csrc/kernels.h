@@ -93,7 +93,14 @@ int sample_step_sites(int hops);
 // rows [M, roundup(M, 64)) of every operand plane are written as zeros (the wgrad reduction
 // runs over whole 64-row blocks).  A_l has K_pad = 2*in_pad (SAGE: [H_self | mean]) or in_pad
 // (GCN: Â H) columns.
-struct Split { __nv_bfloat16* hi; __nv_bfloat16* lo; };
+// Operand planes of activations/gradients are stored k-block-tiled: element (r, k) of a plane
+// with `rows` rows at ((k / 64) * rows + r) * 64 + k % 64, so that every 64-column x R-row TMA
+// box the GEMM loads is one contiguous block of HBM.  rows == 0: plain
+// row-major (the weight planes, whose row width is their own).
+struct Split { __nv_bfloat16* hi; __nv_bfloat16* lo; int64_t rows; };
+__host__ __device__ __forceinline__ int64_t tix(const Split& o, int64_t r, int64_t k) {
+    return ((k >> 6) * o.rows + r) * 64 + (k & 63);
+}
 
 // Rows of an aggregation input: a local buffer (shards == nullptr), or the feature table
 // row-sharded over peers (config 4): row r lives in shard r / rps at local row r % rps; the
@@ -156,6 +163,9 @@ void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint3
 struct TcGemmMaps { CUtensorMap a_hi, a_lo, b_hi, b_lo, c; };
 // 2-D bf16 row-major [rows x cols], box {64 cols, box_rows}, 128B swizzle, OOB reads -> 0.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
+// k-block-tiled bf16 plane (Split layout, `rows` rows, `cols` columns): 3-D map {64, rows,
+// ceil(cols/64)}, box {64, box_rows, 1}, 128B swizzle.
+bool make_tmap_bf16_tiled(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
 // fp32 C of a GEMM: [depth x rows x cols], row stride ld, depth stride dstride (elements); box
 // {32, 32, 1}, 128B swizzle; stores outside [rows x cols] are clipped.
 bool make_tmap_f32(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int64_t depth,
