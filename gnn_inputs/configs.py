@@ -68,6 +68,11 @@ WORKLOADS = {
                                      (15, 10, 5), 3, 256, 1024, 196_615),
     "products_shadow_l5": Workload("products_shadow_l5", 2_449_029, 61_859_140, 100, 47, "gcn", "shadow",
                                    (15, 10, 5), 5, 256, 1024, 196_615),
+    # papers100M's layer shapes (F = 128, C = 172: logits wider than one GEMM tile, the separate
+    # cross-entropy kernel) on a graph small enough for the oracle and one GPU; the sharded-table
+    # test runs it too (configs[4]'s code path at a testable size)
+    "papers_small": Workload("papers_small", 200_000, 3_000_000, 128, 172, "sage", "neighbor",
+                             (15, 10, 5), 3, 256, 1024, 20_000),
     # configs[4]: papers100M-shaped (row-sharded features across ranks)
     "papers100m": Workload("papers100m", 111_059_956, 1_615_685_872, 128, 172, "sage", "neighbor",
                            (15, 10, 5), 3, 256, 1024, 1_207_179),

@@ -19,6 +19,7 @@ CASES = {
     "products_gcn": dict(batches=(), steps=1),
     "products_sage_shadow": dict(batches=(), steps=1),
     "products_shadow_l5": dict(batches=(), steps=1),
+    "papers_small": dict(batches=(0, 1, 19), steps=2),
 }
 
 

@@ -63,7 +63,7 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["tiny", "reddit"])
+@pytest.mark.parametrize("name", ["tiny", "reddit", "papers_small"])
 def test_sharded_feature_gather_matches_oracle(name):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
