@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             int q = 0;
             // kAggU neighbour rows in flight per warp (memory-level parallelism of the gather);
             // the adds stay in CSR order
-            constexpr int kAggU = CPL == 1 ? 4 : 2;
+            constexpr int kAggU = CPL <= 2 ? 4 : 2;
             for (; q + kAggU <= m; q += kAggU) {
                 float4 v[kAggU][CPL];
 #pragma unroll

@@ -159,7 +159,7 @@ struct GemmArgs {
     const int32_t* nodes;
     Split dz;               // dZ planes [rows x ldc]
     int classes;
-    int diag;               // profiling diagnostics only (env GS_GEMM_DIAG): 1 skip C stores, 2 skip MMAs
+    int diag;               // profiling diagnostics only (env GS_GEMM_DIAG): 1 skip C stores, 2 skip MMAs, 4 skip loads
 };
 
 struct TileInfo { int tm, tn, z, kb0, nkb; };
@@ -250,6 +250,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                     uint8_t* b_hi = st + Cfg::kAStage;
                     uint8_t* a_lo = st + Cfg::kAStage + Cfg::kBStage;
                     uint8_t* b_lo = a_lo + Cfg::kAStage;
+                    if (args.diag & 4) { mbar_arrive(&full_bar[s]); continue; }   // diagnostics: no loads
                     mbar_expect_tx(&full_bar[s], kAPlanes * (Cfg::kAStage + (B_MN ? Cfg::kBBytesMN : Cfg::kBBytesK)));
                     const int k0 = (ti.kb0 + kb) * kBK;
                     // A planes are k-block-tiled (3-D maps {64, rows, k-block}): every box is one
