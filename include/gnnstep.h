@@ -227,6 +227,10 @@ gnn_status gnn_profile_read(gnn_model* m, int32_t kid, double* ms_out_host, int6
 gnn_status gnn_profile_reset(gnn_model* m);
 /* Number of kernels one step launches (for the bench's gpu_launches). */
 int64_t gnn_launches_per_step(const gnn_model* m);
+/* 1 if every CSR entry v -> u of the graph has its reverse u -> v (checked on the device at
+   creation), 0 if not, -1 for NULL.  A symmetric graph induces symmetric ShaDow blocks
+   (PAPER.md lines 170-171), which serve as their own transpose in the backward pass. */
+int32_t gnn_graph_symmetric(const gnn_graph* g);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <string>
@@ -77,6 +78,7 @@ struct gnn_graph {
     float* X = nullptr;        // full table, or this process's shard (rows [row_begin, row_end))
     int32_t* y = nullptr;
     int64_t row_begin = 0, row_end = 0;
+    bool symmetric = false;    // every entry has its reverse (checked at creation)
     // row-sharded features (config 4): peer shard pointers (device array) after gnn_shard_import
     int nshards = 0;
     int64_t rps = 0;
@@ -147,6 +149,10 @@ struct gnn_model {
     int last = -1;                       // set trained last
     int fetch_set = 0;                   // set gnn_sample filled
     int32_t *map = nullptr, *icount = nullptr, *hubs = nullptr;
+    // ShaDow: balanced-aggregation partials/counters and the last layer's receptive-field mask
+    float* bal_part = nullptr;
+    int32_t* bal_cnt = nullptr;
+    uint32_t* rf_mask = nullptr;
     uint32_t seq = 0;                    // sampling-launch sequence number (scan-word tags)
     bool full_train = true;              // training needs the last hop's relabel (GCN, ShaDow)
     bool last_full = true;               // mode of the last sampling launch (phase readout)
@@ -246,6 +252,44 @@ void enqueue_training(gnn_model* m, int set) {
     BatchSet& B = m->bs[set];
     cudaStream_t s = m->stream;
     const int L = m->L;
+    // ShaDow: rows the last layer reads (layer L-1 computes only these, R19)
+    if (m->shadow && L >= 2)
+        K(m, s, GNN_K_AGG, [&] {
+            launch_rf_mark(&B.st->batch_n, B.rowptr[m->slot], B.col[m->slot], &B.st->seq, m->rf_mask, s);
+        });
+    auto bal = [&](bool bwd, int li, const int32_t* rows) {
+        const Layer& ly = m->layers[li];
+        const int blk = ly.blk;
+        BalLaunch b{};
+        b.bwd = bwd;
+        b.gcn = !m->sage;
+        b.ndst_ptr = &B.st->n_dst[blk];
+        b.rmask = li == L - 2 ? m->rf_mask : nullptr;
+        b.tag_ptr = &B.st->seq;
+        b.in_pad = ly.in_pad;
+        b.part = m->bal_part;
+        b.cnt = m->bal_cnt;
+        if (!bwd) {
+            b.n_ptr = rows;
+            b.rowptr = B.rowptr[blk]; b.col = B.col[blk];
+            b.orow = B.trowptr[blk] ? B.trowptr[blk] : B.rowptr[blk];   // symmetric block: its own transpose
+            b.H = li == 0 ? g->rows() : FeatRows{m->layers[li - 1].H, nullptr, 0};
+            b.gmap = li == 0 ? B.nodes : nullptr;
+            b.out = ly.A;
+            b.out_w = m->sage ? 2 * ly.in_pad : ly.k_pad;
+        } else {
+            b.n_ptr = &B.st->n_src[blk];
+            b.dlim_ptr = rows;
+            b.rowptr = B.trowptr[blk] ? B.trowptr[blk] : B.rowptr[blk];
+            b.col = B.tdst_s[blk] ? B.tdst_s[blk] : B.col[blk];
+            b.orow = B.rowptr[blk];
+            b.dA = ly.dA;
+            b.Hprev = m->layers[li - 1].H;
+            b.out = m->layers[li - 1].dPre;
+            b.out_w = ly.in_pad;
+        }
+        launch_agg_bal(b, s);
+    };
     // ---- forward
     for (int li = 0; li < L; ++li) {
         Layer& ly = m->layers[li];
@@ -255,7 +299,9 @@ void enqueue_training(gnn_model* m, int set) {
         const FeatRows Hrows = li == 0 ? g->rows() : FeatRows{m->layers[li - 1].H, nullptr, 0};
         const int kid = li == 0 ? GNN_K_AGG_L1 : GNN_K_AGG;
         const int32_t* self_ids = li == 0 ? B.nodes : nullptr;
-        if (m->sage) {
+        if (m->shadow) {
+            K(m, s, kid, [&] { bal(false, li, rows); });
+        } else if (m->sage) {
             // layer 1 of the neighbour sampler reads X rows directly by global neighbour id
             const bool direct = li == 0 && !m->shadow;
             // the training-only sampling run writes the last hop fixed-stride (no count scan)
@@ -310,7 +356,8 @@ void enqueue_training(gnn_model* m, int set) {
         });
         Layer& prev = m->layers[li - 1];
         const int blk = ly.blk;
-        K(m, s, GNN_K_SPMM_BWD, [&] {
+        if (m->shadow) K(m, s, GNN_K_SPMM_BWD, [&] { bal(true, li, rows); });
+        else K(m, s, GNN_K_SPMM_BWD, [&] {
             launch_spmm_bwd(!m->sage, blk, B.st, rows, ly.dA, ly.in_pad, B.rowptr[blk], B.trowptr[blk], B.tdst_s[blk],
                             prev.H, prev.dPre, s);
         });
@@ -635,6 +682,8 @@ static gnn_status graph_create(int64_t num_nodes, const int64_t* row_ptr_host, c
         e = cudaMemset2D(g->X + feat_dim, sizeof(float) * feat_stride, 0, sizeof(float) * (feat_stride - feat_dim),
                          local_rows);
     if (e != cudaSuccess) return cleanup(fail(GNN_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e)));
+    if (!check_symmetric(g->row_ptr, g->col, num_nodes, &g->symmetric))
+        return cleanup(fail(GNN_ERR_CUDA, "symmetry check failed"));
     *out = g;
     return GNN_OK;
 }
@@ -698,7 +747,11 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         HopBufs& b = m->hb[m->slot];
         b.cap_dst = b.cap_src = m->nodes_cap;
         b.cap_edges = std::max<int64_t>(1, g->nnz);
-        b.need_t = true;
+        // a symmetric graph induces a symmetric block: it is its own transpose (the backward
+        // sums row u in the block's CSR order, a fixed order), so no transposed build/sort.
+        // GS_SHADOW_TRANSPOSE=1 forces the transposed build (tests of that path).
+        const char* ft = std::getenv("GS_SHADOW_TRANSPOSE");
+        b.need_t = !g->symmetric || (ft && ft[0] == '1');
     }
     m->nwords = (g->N + 31) / 32;
     // shared sampling scratch (sampling runs are serialised on the sampling stream)
@@ -803,6 +856,15 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         m->layers.push_back(ly);
     }
     m->pcount = poff;
+    if (m->shadow) {
+        int maxw = 4;
+        for (const Layer& ly : m->layers) maxw = std::max(maxw, ly.in_pad);
+        AL(m->bal_part, 2 * (int64_t)bal_units_cap() * maxw);
+        AL(m->bal_cnt, m->nodes_cap + 1);
+        AL(m->rf_mask, m->nodes_cap + 1);
+        CK(cudaMemset(m->bal_cnt, 0, sizeof(int32_t) * (m->nodes_cap + 1)));
+        CK(cudaMemset(m->rf_mask, 0, sizeof(uint32_t) * (m->nodes_cap + 1)));
+    }
     for (int li = 0; li < m->L; ++li) {
         Layer& ly = m->layers[li];
         ly.rows_alloc = round_up(ly.m_cap, 128);
@@ -1243,5 +1305,6 @@ gnn_status gnn_profile_reset(gnn_model* m) {
 }
 
 int64_t gnn_launches_per_step(const gnn_model* m) { return m ? m->launches_per_step : -1; }
+int32_t gnn_graph_symmetric(const gnn_graph* g) { return g ? (g->symmetric ? 1 : 0) : -1; }
 
 }  // extern "C"

@@ -330,6 +330,250 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
     }
 }
 
+// ------------------------------------------------------------------ balanced (merge-path) aggregation
+// ShaDow blocks (the induced subgraph) have power-law rows (thousands of entries at
+// the hubs): a warp per row leaves the grid waiting on the hub rows.  Here the rows and edges of
+// the traversed CSR form one merged item sequence (row r owns items [rowptr[r]+r, rowptr[r+1]+r],
+// its edges then an end marker) cut into units of T = max(16, items / 2^16) items; a warp takes a unit, finds its
+// first row by a 32-ary search of rowptr[r]+r, and sums the unit's part of every row it touches.
+// A row inside one unit is finished by that warp.  A row spread over units ua..ub leaves one
+// partial per unit (ua: slot 2ua+1 "out", later units: slot 2u "in"); the warp whose piece
+// completes the per-row count sums the partials in unit order (fixed order: deterministic) and
+// finishes the row.  Counters are reset by the finishing warp.
+//   FWD (SAGE/GCN): traversed CSR = the block, rows = output rows, edges = local sources.
+//   BWD (SAGE/GCN): traversed CSR = the transposed block, rows = sources u, edges = dst rows t.
+// rmask (receptive-field pruning, R19): rows r with rmask[r] != *tag are not computed
+// (FWD), dst rows t with rmask[t] != *tag carry no gradient (BWD).
+constexpr int kBalTmin = 16, kBalUnits = 1 << 16;
+struct BalArgs {
+    const int32_t* n_ptr;      // rows traversed (FWD: output rows; BWD: n_src of the block)
+    const int32_t* ndst_ptr;   // n_dst of the block (GCN self loops)
+    const int32_t* dlim_ptr;   // BWD: dA rows < dlim carry gradient
+    const int32_t* rowptr;     // traversed CSR
+    const int32_t* col;        // FWD: local sources; BWD: destinations (ascending per row)
+    const int32_t* orow;       // the other direction's row pointer (FWD GCN: d_out; BWD: d_in(dst))
+    const uint32_t* rmask;
+    const uint32_t* tag_ptr;
+    FeatRows H;                // FWD input rows
+    const int32_t* gmap;       // FWD: row id of local node c in H (layer 1: global ids)
+    const float* dA;           // BWD
+    const float* Hprev;        // BWD: ReLU mask rows
+    int in_pad;
+    Split out;                 // FWD: A (SAGE [self | mean], GCN Â H); BWD: dPre
+    int out_w;                 // columns of `out` (zero tail rows)
+    float* part;               // partial rows [2 * units][in_pad]
+    int32_t* cnt;              // per-row piece counters (zero between launches)
+};
+
+template <int CPL, int MODE>   // MODE: 0 FWD SAGE, 1 FWD GCN, 2 BWD SAGE, 3 BWD GCN
+__global__ void __launch_bounds__(256) k_agg_bal(BalArgs a) {
+    constexpr bool BWD = MODE >= 2, GCN = (MODE & 1) != 0;
+    pdl_trigger();
+    pdl_wait();
+    const int n = *a.n_ptr;
+    const int lane = lane_id();
+    const int nch = a.in_pad >> 2;
+    const int W = total_warps();
+    for (int i = n + global_warp(); i < round64(n); i += W)
+        for (int ch = lane; ch < (a.out_w >> 2); ch += 32) store_split4(a.out, tix(a.out, i, 4 * ch), kZero4);
+    const int ndst = *a.ndst_ptr;
+    const int dlim = BWD ? *a.dlim_ptr : 0;
+    const uint32_t tag = a.rmask ? *a.tag_ptr : 0u;
+    const int64_t items = (int64_t)n + a.rowptr[n];
+    // unit size: at least kBalTmin items, at most kBalUnits units (the partial-slot capacity)
+    const int T = (int)max((int64_t)kBalTmin, (items + kBalUnits - 1) / kBalUnits);
+    const int nunits = (int)((items + T - 1) / T);
+    const int64_t ldd = GCN ? a.in_pad : 2 * a.in_pad;   // BWD dA row (SAGE: [dSelf | dM])
+
+    // finish row r from its full sum `acc` (fwd: normalise + self term; bwd: self term + ReLU')
+    auto finish = [&](int r, int rb, int re, float4 (&acc)[CPL], bool any) {
+        if constexpr (!BWD) {
+            const int self = a.gmap ? a.gmap[r] : r;
+            const float4* ps = reinterpret_cast<const float4*>(a.H.row(self, a.in_pad));
+            if constexpr (GCN) {
+                const float din = (float)(re - rb + 1);
+                const float dself = (float)(a.orow[r + 1] - a.orow[r] + (r < ndst ? 1 : 0));
+                const float ws = 1.0f / sqrtf(din * dself);
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    if (ch < nch) store_split4(a.out, tix(a.out, r, 4 * ch), f4fma(ws, __ldg(ps + ch), acc[c]));
+                }
+            } else {
+                const int deg = re - rb;
+                const float inv = deg ? 1.0f / (float)deg : 0.f;
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    if (ch < nch) {
+                        store_split4(a.out, tix(a.out, r, 4 * ch), __ldg(ps + ch));
+                        store_split4(a.out, tix(a.out, r, 4 * (nch + ch)), f4scale(acc[c], inv));
+                    }
+                }
+            }
+        } else {
+            const bool self_on = r < dlim && (!a.rmask || a.rmask[r] == tag);
+            float wself = 1.f;
+            if (GCN && self_on) {
+                const float din = (float)(a.orow[r + 1] - a.orow[r] + 1);
+                const float dout = (float)(re - rb + (r < ndst ? 1 : 0));
+                wself = 1.0f / sqrtf(din * dout);
+            }
+            const float4* hp = reinterpret_cast<const float4*>(a.Hprev + (int64_t)r * a.in_pad);
+            const float4* sp = reinterpret_cast<const float4*>(a.dA + (int64_t)r * ldd);
+            if (!any && !self_on) {   // no gradient reaches row r: dPre = 0 (no reads)
+                for (int ch = lane; ch < nch; ch += 32) store_split4(a.out, tix(a.out, r, 4 * ch), kZero4);
+                return;
+            }
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const int ch = lane + 32 * c;
+                if (ch < nch) {
+                    float4 v = acc[c];
+                    if (self_on) v = GCN ? f4fma(wself, __ldg(sp + ch), v) : f4add(v, __ldg(sp + ch));
+                    const float4 h = __ldg(hp + ch);
+                    v.x = h.x > 0.f ? v.x : 0.f; v.y = h.y > 0.f ? v.y : 0.f;
+                    v.z = h.z > 0.f ? v.z : 0.f; v.w = h.w > 0.f ? v.w : 0.f;
+                    store_split4(a.out, tix(a.out, r, 4 * ch), v);
+                }
+            }
+        }
+    };
+
+    for (int u = global_warp(); u < nunits; u += W) {
+        const int64_t d0 = (int64_t)u * T, d1 = min(d0 + (int64_t)T, items);
+        // r0 = max r in [0, n] with rowptr[r] + r <= d0 (32-ary search; f(r) = rowptr[r]+r increases)
+        int lo = 0, hi = n;
+        while (hi > lo) {
+            const int step = (hi - lo + 31) / 32;
+            const int c = lo + (lane + 1) * step;
+            const bool ok = c <= hi && (int64_t)a.rowptr[c] + c <= d0;
+            const int k = __popc(__ballot_sync(kFull, ok));
+            lo += k * step;
+            hi = min(hi, lo + step - 1);
+        }
+        int wb = lo;                                   // window of 32 row pointers from wb
+        int rpw = a.rowptr[min(wb + lane, n)];
+        for (int r = lo;; ++r) {
+            if (r - wb >= 31) { wb = r; rpw = a.rowptr[min(wb + lane, n)]; }
+            const int rb = __shfl_sync(kFull, rpw, r - wb), re = __shfl_sync(kFull, rpw, r - wb + 1);
+            const int64_t fr = (int64_t)rb + r, fr1 = (int64_t)re + r + 1;
+            if (r >= n || fr >= d1) break;
+            if constexpr (!BWD) {
+                if (a.rmask && a.rmask[r] != tag) continue;   // row outside the receptive field
+            }
+            const int eb = max(rb, (int)(d0 - r)), ee = min(re, (int)(d1 - r));
+            float4 acc[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
+            const float din_r = (float)(re - rb + 1);                       // FWD GCN: d_in(r)
+            const float dout_r = (float)(re - rb + (r < ndst ? 1 : 0));     // BWD GCN: d_out(u)
+            bool any = false;   // a contributing edge was seen (else the row sum is exactly 0)
+            for (int e0 = eb; e0 < ee; e0 += 32) {
+                const int m = min(32, ee - e0);
+                int myrow = -1;
+                float myw = 0.f;
+                if (lane < m) {
+                    const int c = a.col[e0 + lane];
+                    if constexpr (!BWD) {
+                        myrow = a.gmap ? a.gmap[c] : c;
+                        if (GCN) {
+                            const float dout = (float)(a.orow[c + 1] - a.orow[c] + (c < ndst ? 1 : 0));
+                            myw = 1.0f / sqrtf(din_r * dout);
+                        }
+                    } else if (c < dlim && (!a.rmask || a.rmask[c] == tag)) {
+                        myrow = c;
+                        const float din = (float)(a.orow[c + 1] - a.orow[c] + (GCN ? 1 : 0));
+                        myw = GCN ? 1.0f / sqrtf(din * dout_r) : 1.0f / din;
+                    }
+                }
+                int mv = m;
+                if constexpr (BWD) {   // compact the contributing edges (order kept) to the low lanes
+                    const unsigned vb = __ballot_sync(kFull, myrow >= 0);
+                    mv = __popc(vb);
+                    if (mv == 0) continue;
+                    const int src = (int)(__fns(vb, 0, lane + 1) & 31u);
+                    myrow = __shfl_sync(kFull, myrow, src);
+                    myw = __shfl_sync(kFull, myw, src);
+                }
+                any = true;
+                // kU rows in flight; accumulation in edge order
+                constexpr int kU = CPL <= 2 ? 4 : 2;
+                for (int q = 0; q < mv; q += kU) {
+                    float4 v[kU][CPL];
+                    int rr[kU];
+                    float ww[kU];
+#pragma unroll
+                    for (int j = 0; j < kU; ++j) {
+                        rr[j] = __shfl_sync(kFull, myrow, min(q + j, 31));
+                        ww[j] = __shfl_sync(kFull, myw, min(q + j, 31));
+                        if (q + j >= mv) rr[j] = -1;
+                        const float4* p;
+                        if constexpr (!BWD) p = reinterpret_cast<const float4*>(a.H.row(max(rr[j], 0), a.in_pad));
+                        else p = reinterpret_cast<const float4*>(a.dA + (int64_t)max(rr[j], 0) * ldd) + (GCN ? 0 : nch);
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) {
+                            const int ch = lane + 32 * c;
+                            v[j][c] = (ch < nch && rr[j] >= 0) ? __ldg(p + ch) : kZero4;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < kU; ++j) {
+                        if (rr[j] < 0) continue;
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c)
+                            acc[c] = (GCN || BWD) ? f4fma(ww[j], v[j][c], acc[c]) : f4add(acc[c], v[j][c]);
+                    }
+                }
+            }
+            const bool started = fr >= d0, completed = fr1 <= d1;
+            if (started && completed) { finish(r, rb, re, acc, any); continue; }
+            // a piece of a row spread over several units
+            float* slot = a.part + (int64_t)(started ? 2 * u + 1 : 2 * u) * a.in_pad;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const int ch = lane + 32 * c;
+                if (ch < nch) __stcg(reinterpret_cast<float4*>(slot) + ch, acc[c]);
+            }
+            __threadfence();
+            __syncwarp();
+            int prev = 0;
+            if (lane == 0) prev = atomicAdd(a.cnt + r, 1);
+            prev = __shfl_sync(kFull, prev, 0);
+            const int ua = (int)(fr / T), ub = (int)((fr1 - 1) / T);
+            if (prev != ub - ua) continue;
+            __threadfence();
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
+            for (int uu = ua; uu <= ub; ++uu) {   // unit order
+                const float4* ps = reinterpret_cast<const float4*>(a.part + (int64_t)(uu == ua ? 2 * uu + 1 : 2 * uu) * a.in_pad);
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    if (ch < nch) acc[c] = f4add(acc[c], __ldcg(ps + ch));
+                }
+            }
+            if (lane == 0) a.cnt[r] = 0;
+            finish(r, rb, re, acc, true);
+        }
+    }
+}
+
+// mask[r] = tag for the rows the last layer reads: the seeds r < *nseed_ptr and their
+// in-neighbours in the block (ShaDow receptive field of the last layer, R19).
+__global__ void __launch_bounds__(256) k_rf_mark(const int32_t* __restrict__ nseed_ptr, const int32_t* __restrict__ rowptr,
+                                                 const int32_t* __restrict__ col, const uint32_t* __restrict__ tag_ptr,
+                                                 uint32_t* __restrict__ mask) {
+    pdl_trigger();
+    pdl_wait();
+    const int b = *nseed_ptr;
+    const uint32_t tag = *tag_ptr;
+    const int ne = rowptr[b];   // the seeds are the block's first rows: their edges are [0, rowptr[b])
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int i = tid; i < b; i += nth) mask[i] = tag;
+    for (int e = tid; e < ne; e += nth) mask[col[e]] = tag;
+}
+
 // ------------------------------------------------------------------ weights, reduce, SGD
 // dW of every layer in one launch: grads[off_l + r*out + c] = Σ_z part_l[z][rpad(r)*n_pad + c]
 // (split order fixed: deterministic).
@@ -506,6 +750,27 @@ void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, 
                      const float* H_prev, Split dPre_prev, cudaStream_t s) {
     if (gcn) spmm_bwd<true>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
     else spmm_bwd<false>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
+}
+
+int bal_units_cap() { return kBalUnits; }
+
+void launch_agg_bal(const BalLaunch& b, cudaStream_t s) {
+    BalArgs a{b.n_ptr, b.ndst_ptr, b.dlim_ptr, b.rowptr, b.col, b.orow, b.rmask, b.tag_ptr, b.H, b.gmap,
+              b.dA, b.Hprev, b.in_pad, b.out, b.out_w, b.part, b.cnt};
+    const int mode = (b.bwd ? 2 : 0) + (b.gcn ? 1 : 0);
+    const int cpl = cpl_of(b.in_pad);
+    const int c = cpl <= 1 ? 1 : cpl <= 2 ? 2 : cpl <= 4 ? 4 : 8;
+#define GS_BAL(C, M) if (c == C && mode == M) { launch_pdl(k_agg_bal<C, M>, kWarpGrid, 256, 0, s, a); return; }
+    GS_BAL(1, 0) GS_BAL(1, 1) GS_BAL(1, 2) GS_BAL(1, 3)
+    GS_BAL(2, 0) GS_BAL(2, 1) GS_BAL(2, 2) GS_BAL(2, 3)
+    GS_BAL(4, 0) GS_BAL(4, 1) GS_BAL(4, 2) GS_BAL(4, 3)
+    GS_BAL(8, 0) GS_BAL(8, 1) GS_BAL(8, 2) GS_BAL(8, 3)
+#undef GS_BAL
+}
+
+void launch_rf_mark(const int32_t* nseed_ptr, const int32_t* rowptr, const int32_t* col, const uint32_t* tag_ptr,
+                    uint32_t* mask, cudaStream_t s) {
+    launch_pdl(k_rf_mark, 148 * 4, 256, 0, s, nseed_ptr, rowptr, col, tag_ptr, mask);
 }
 
 void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s) {

@@ -43,6 +43,9 @@ constexpr int kWarpGrid = 148 * 16;          // blocks of 256 threads for warp-p
 void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t epoch,
                       uint64_t* keys, cudaStream_t s);
 
+// Whether every CSR entry (v -> u) has its reverse (u -> v); synchronous (graph creation).
+bool check_symmetric(const int64_t* row_ptr, const int32_t* col, int64_t n, bool* symmetric);
+
 struct GridBarrier {
     unsigned count, gen;
     unsigned nts, pad;            // barriers so far; pad = nts at the last launch's start
@@ -129,6 +132,34 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
 void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,
                     const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
                     const int32_t* col, const int32_t* trowptr, Split A, cudaStream_t s);
+// Balanced (merge-path) aggregation over a ShaDow block (dense.cu k_agg_bal): the same
+// arithmetic as launch_agg_sage/_gcn (fwd) and launch_spmm_bwd (bwd), with rows split over
+// warps by a fixed cut of the merged row+edge sequence, partials combined in a fixed order.
+struct BalLaunch {
+    bool bwd, gcn;
+    const int32_t* n_ptr;      // rows traversed (fwd: output rows; bwd: n_src of the block)
+    const int32_t* ndst_ptr;   // n_dst of the block
+    const int32_t* dlim_ptr;   // bwd: dA rows < dlim carry gradient
+    const int32_t* rowptr;     // traversed CSR (fwd: block; bwd: transposed block)
+    const int32_t* col;        // fwd: local sources; bwd: destinations
+    const int32_t* orow;       // fwd GCN: transposed row pointer (d_out); bwd: block row pointer (d_in)
+    const uint32_t* rmask;     // optional receptive-field mask (== *tag_ptr: in)
+    const uint32_t* tag_ptr;
+    FeatRows H;                // fwd input rows
+    const int32_t* gmap;       // fwd: H row of local node (self and neighbours), nullable
+    const float* dA;           // bwd
+    const float* Hprev;        // bwd
+    int in_pad;
+    Split out;
+    int out_w;
+    float* part;               // [2 * bal_units_cap()][in_pad] floats
+    int32_t* cnt;              // [rows cap] zero-initialised
+};
+int bal_units_cap();   // partial slots needed: 2 * bal_units_cap() rows of in_pad floats
+void launch_agg_bal(const BalLaunch& b, cudaStream_t s);
+// mask[r] = *tag_ptr for the seeds r < *nseed_ptr and their in-neighbours in the block.
+void launch_rf_mark(const int32_t* nseed_ptr, const int32_t* rowptr, const int32_t* col, const uint32_t* tag_ptr,
+                    uint32_t* mask, cudaStream_t s);
 // Per layer: flat fp32 W (rows x out, at params/grads offset poff), its GEMM planes
 // W [K_pad x N_pad] (bf16 split), and the wgrad split-K partials.
 struct PackLayer {

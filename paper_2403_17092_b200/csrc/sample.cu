@@ -15,7 +15,43 @@ __global__ void k_perm_keys(const int32_t* train, int64_t n, uint64_t seed, uint
     }
 }
 
+// Symmetry of the CSR: every entry u of row v has v in row u (rows ascending: binary search).
+// A warp per row; *asym is set on the first missing reverse entry.
+__global__ void k_check_symmetric(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, int64_t n,
+                                  int* __restrict__ asym) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = w0; v < n; v += nw) {
+        const int64_t rb = row_ptr[v], re = row_ptr[v + 1];
+        for (int64_t p = rb + lane; p < re; p += 32) {
+            const int u = col[p];
+            int64_t lo = row_ptr[u], hi = row_ptr[u + 1];
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (col[mid] < v) lo = mid + 1; else hi = mid;
+            }
+            if (lo >= row_ptr[u + 1] || col[lo] != v) atomicOr(asym, 1);
+        }
+    }
+}
+
 }  // namespace
+
+bool check_symmetric(const int64_t* row_ptr, const int32_t* col, int64_t n, bool* symmetric) {
+    int* d = nullptr;
+    if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return false;
+    int h = 0;
+    bool ok = cudaMemset(d, 0, sizeof(int)) == cudaSuccess;
+    if (ok && n > 0) {
+        k_check_symmetric<<<148 * 8, 256>>>(row_ptr, col, n, d);
+        ok = cudaGetLastError() == cudaSuccess;
+    }
+    ok = ok && cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d);
+    *symmetric = h == 0;
+    return ok;
+}
 
 void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t epoch, uint64_t* keys, cudaStream_t s) {
     if (n <= 0) return;

@@ -408,8 +408,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
                     if (m[r] >= 0) {
                         const int o = out + __popc(bal & ((1u << lane) - 1u));
                         S.col[o] = m[r];
-                        S.erow[o] = i;
-                        atomicAdd(&S.tcount[m[r]], 1);
+                        if (S.tcount) {   // transposed block wanted (not when the graph is symmetric)
+                            S.erow[o] = i;
+                            atomicAdd(&S.tcount[m[r]], 1);
+                        }
                     }
                     out += __popc(bal);
                 }

@@ -73,6 +73,7 @@ def lib():
             "gnn_debug_get": ([P, I32, P, I64], I32), "gnn_last_sizes": ([P, P], I32),
             "gnn_profile_enable": ([P, I32], I32), "gnn_profile_read": ([P, I32, P, P], I32),
             "gnn_profile_reset": ([P], I32), "gnn_launches_per_step": ([P], I64),
+            "gnn_graph_symmetric": ([P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(_lib, name)
@@ -114,6 +115,10 @@ class Graph:
         _check(lib().gnn_graph_create(n, _ptr(row_ptr), _ptr(col), self.feat_dim, stride, _ptr(X), _ptr(y),
                                       num_classes, device, C.byref(h)))
         self.h = h
+
+    @property
+    def symmetric(self) -> bool:
+        return lib().gnn_graph_symmetric(self.h) == 1
 
     def close(self):
         if self.h:

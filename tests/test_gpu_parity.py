@@ -156,10 +156,15 @@ def test_epoch_permutation_bitexact():
 # ---------------------------------------------------------------- the rest of the model x sampler grid
 # (Table 3: GCN and SAGE under both samplers, and
 # the ShaDow depth setting L = 5 layers on L' = 2 hops)
-@pytest.mark.parametrize("name", ["tiny_gcn", "tiny_sage_shadow", "tiny_shadow_l5"])
-def test_grid_sampling_and_training_parity(name):
+@pytest.mark.parametrize("name,transpose", [("tiny_gcn", 0), ("tiny_sage_shadow", 0), ("tiny_shadow_l5", 0),
+                                            ("tiny_sage_shadow", 1), ("tiny_shadow_l5", 1)])
+def test_grid_sampling_and_training_parity(name, transpose, monkeypatch):
+    """transpose=1: the ShaDow backward over an explicitly built, sorted transposed block (the
+    path of non-symmetric graphs) instead of the symmetric block itself."""
     w, inp, graph = inputs_for(name)
+    monkeypatch.setenv("GS_SHADOW_TRANSPOSE", str(transpose))
     g, m = make_gpu(w, inp)
+    assert g.symmetric          # the generator's graphs are symmetric (Chung-Lu, both directions)
     perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
     for b in (0, 1, w.n_batches - 1):
         want, _ = oracle.sample_batch(w, graph, 0, b, perm)
@@ -177,3 +182,22 @@ def test_grid_sampling_and_training_parity(name):
         out = check_train_step(m, w, graph, params, 0, step, perm, loss)
         params = out["params"]
         assert rel(m.get_params(), params) <= TOL_FP32
+
+
+def test_symmetry_check():
+    """gnn_graph_symmetric: the device check against a host brute force on a symmetric graph and
+    on the same graph with one reverse entry removed."""
+    from paper_2403_17092_b200 import Graph
+    w, inp, graph = inputs_for("tiny")
+    rp, col = inp["row_ptr"], inp["col"]
+    g = Graph(rp, col, inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim)
+    assert g.symmetric
+    g.close()
+    # drop the first entry of row v (v -> u): row u still lists v, so the graph is not symmetric
+    v = int(np.nonzero(np.diff(rp) > 0)[0][0])
+    keep = np.ones(col.shape[0], dtype=bool)
+    keep[rp[v]] = False
+    rp2 = rp.copy()
+    rp2[v + 1:] -= 1
+    g2 = Graph(rp2, col[keep], inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim)
+    assert not g2.symmetric
