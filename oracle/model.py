@@ -166,6 +166,26 @@ def sgd(Ws, G, lr):
     return [W - lr * g for W, g in zip(Ws, G)]
 
 
+def adam(Ws, G, state, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """NEXT-4: Adam, the optimizer of the paper's training listings
+    (`torch.optim.Adam(...)`; standard defaults,
+    no weight decay, no amsgrad).  Kingma & Ba, Algorithm 1, as torch.optim.Adam states it:
+        t <- t + 1;  m <- b1 m + (1 - b1) g;  v <- b2 v + (1 - b2) g^2
+        W <- W - lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+    `state` = dict(t, m, v) (m, v lists like Ws, zero at t = 0); updated in place."""
+    if not state:
+        state.update(t=0, m=[np.zeros_like(W) for W in Ws], v=[np.zeros_like(W) for W in Ws])
+    state["t"] += 1
+    t = state["t"]
+    bc1, bc2 = 1.0 - beta1 ** t, 1.0 - beta2 ** t
+    out = []
+    for i, (W, g) in enumerate(zip(Ws, G)):
+        state["m"][i] = beta1 * state["m"][i] + (1.0 - beta1) * g
+        state["v"][i] = beta2 * state["v"][i] + (1.0 - beta2) * g * g
+        out.append(W - lr * (state["m"][i] / bc1) / (np.sqrt(state["v"][i] / bc2) + eps))
+    return out
+
+
 def allreduce(rank_grads):
     """O8: Σ_p G_p in rank order."""
     out = [np.zeros_like(g) for g in rank_grads[0]]

@@ -191,3 +191,33 @@ def test_ragged_last_step_inactive_ranks(tiny_inputs):
     out = oracle.train_step(w, g, g["params"], 0, 39, 4)    # g = 156..159: only 156 active
     assert out["b_total"] == 16
     assert all(np.all(r == 0) for r in out["rank_grads"][1:])
+
+
+# ---------------------------------------------------------------- NEXT-4: Adam
+def test_adam_matches_torch_optim_adam():
+    """The oracle's Adam against the library routine the paper's listings call
+    (torch.optim.Adam, float64 on CPU), five steps on random weights and gradients."""
+    rng = np.random.default_rng(5)
+    Ws = [rng.standard_normal((6, 4)), rng.standard_normal((8, 3))]
+    grads = [[rng.standard_normal(W.shape) * 10.0 ** rng.integers(-3, 2) for W in Ws] for _ in range(5)]
+    tp = [torch.tensor(W.copy(), dtype=torch.float64, requires_grad=True) for W in Ws]
+    opt = torch.optim.Adam(tp, lr=0.01, betas=(0.9, 0.999), eps=1e-8)
+    state, cur = {}, Ws
+    for G in grads:
+        cur = M.adam(cur, G, state, 0.01)
+        for p, g in zip(tp, G):
+            p.grad = torch.tensor(g, dtype=torch.float64)
+        opt.step()
+    for a, p in zip(cur, tp):
+        assert np.allclose(a, p.detach().numpy(), rtol=1e-12, atol=1e-14)
+
+
+def test_adam_first_step_closed_form():
+    """t = 1: m/(1-b1) = g and v/(1-b2) = g^2, so each weight moves by lr*g/(|g|+eps)
+    (= lr*sign(g) up to eps), and a zero gradient leaves the weight unchanged."""
+    g = np.array([[3.0, -0.5, 0.0, 1e-3]])
+    W = np.zeros_like(g)
+    state = {}
+    out = M.adam([W], [g], state, lr=0.1)[0]
+    assert np.allclose(out, -0.1 * g / (np.abs(g) + 1e-8), rtol=1e-12, atol=0)
+    assert out[0, 2] == 0.0 and state["t"] == 1
