@@ -114,10 +114,14 @@ typedef struct {
     int32_t fanouts[8];     /* input-layer-first, each 1..32                  */
     int32_t precision;      /* GNN_FP32 | GNN_BF16_GEMM                       */
     int32_t use_graph;      /* 1: replay the step as one CUDA graph           */
-    float lr;               /* SGD learning rate                              */
+    float lr;               /* learning rate                                  */
     uint64_t seed;          /* sampler seed (permutation + sampling draws)    */
     uint64_t init_seed;     /* weight init                                    */
+    int32_t optimizer;      /* GNN_SGD (0) | GNN_ADAM (the
+                               listings' torch.optim.Adam, lines 398, 444)     */
+    float beta1, beta2, eps;/* Adam (torch defaults 0.9, 0.999, 1e-8)         */
 } gnn_model_config;
+enum { GNN_SGD = 0, GNN_ADAM = 1 };
 
 gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model** out);
 gnn_status gnn_model_destroy(gnn_model* m);
@@ -150,6 +154,23 @@ gnn_status gnn_comm_get_unique_id(uint8_t out_host[128]);
 gnn_status gnn_plan_step(int64_t n_train, int32_t batch_size, int32_t world, int32_t rank, int64_t step,
                          int64_t* g_out, int32_t* n_out, int64_t* offset_out, int32_t* b_total_out);
 int64_t gnn_steps_per_epoch(int64_t n_train, int32_t batch_size, int32_t world);
+
+/* ---- NEXT-3: the paper's Dynamic Load Balancer (§4)
+ * applied to homogeneous trainers.  Workload of a mini-batch = "the total number of
+ * aggregations ... using the computational graph of the mini-batches" (line 285): the edges of
+ * every layer's block, Σ_l E(block_l), estimated in advance by running the sampler (line 284).
+ * gnn_estimate_workload: work_out_host[g] for every global batch g of `epoch`
+ * (n == ceil(n_train/B), else SHAPE); samples every batch (synchronous, a one-time cost).
+ * gnn_plan_balanced (host only): sorts the batches by workload (heaviest first, ties by index,
+ * line 287), groups consecutive `world` batches into one synchronous step (so the ranks of a
+ * step have similar work and sync-SGD stragglers shrink), steps ordered by their smallest batch
+ * index, the ragged group last; order_out_host[s*world + r] = batch of rank r at step s.
+ * gnn_set_schedule: step s, rank r trains batch order[s*world + r] (a permutation of the
+ * epoch's batches, else PARAM/SHAPE); b_total = seeds of that step's batches; n = 0 restores
+ * the default rule g = s*world + r.  Every rank must set the same schedule. */
+gnn_status gnn_estimate_workload(gnn_model* m, int64_t epoch, int64_t* work_out_host, int64_t n);
+gnn_status gnn_plan_balanced(const int64_t* work_host, int64_t n, int32_t world, int64_t* order_out_host);
+gnn_status gnn_set_schedule(gnn_model* m, const int64_t* order_host, int64_t n);
 gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_t id_host[128]);
 
 /* The epoch's seed order (§2.2; SPEC.md partition_seeds lines 107-115):

@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -164,8 +165,10 @@ struct gnn_model {
     std::vector<Layer> layers;
     float *params = nullptr, *grads = nullptr;
     int64_t pcount = 0;
+    OptState opt{};                      // Adam moments + step count (m == nullptr: SGD)
     bool overlap = true;                 // prefetch the next batch during training
 
+    std::vector<int64_t> schedule;       // NEXT-3: step s, rank r trains batch schedule[s*world + r] (empty: g = s*world + r)
     int32_t *perm = nullptr, *train_sorted = nullptr;
     uint64_t *keys = nullptr, *keys_alt = nullptr;
     void* cub_tmp = nullptr;
@@ -370,10 +373,10 @@ void enqueue_training(gnn_model* m, int set) {
         K(m, s, GNN_K_ALLREDUCE, [&] {
             ncclAllReduce(m->grads, m->grads, (size_t)m->pcount, ncclFloat, ncclSum, m->comm, s);
         });
-        K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, false, s); });
+        K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, false, m->opt, s); });
     } else {
         // ---- one rank: the reduce of the partials is fused into the update
-        K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, true, s); });
+        K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, true, m->opt, s); });
     }
 }
 
@@ -495,11 +498,30 @@ gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const i
     return GNN_OK;
 }
 
+// The batch this rank trains at `step`: the engine's rule (plan_step), or the workload-balanced
+// schedule set with gnn_set_schedule (reading R8 with the batch order of NEXT-3).
+void plan_model_step(const gnn_model* m, int64_t step, int64_t* g, int32_t* n, int64_t* offset, int32_t* b_total) {
+    if (m->schedule.empty()) {
+        plan_step(m->n_train, m->cfg.batch_size, m->world, m->rank, step, g, n, offset, b_total);
+        return;
+    }
+    const int64_t B = m->cfg.batch_size, nb = (int64_t)m->schedule.size();
+    auto seeds = [&](int64_t gg) { return (int32_t)std::min<int64_t>(B, m->n_train - gg * B); };
+    const int64_t i = step * m->world + m->rank;
+    *g = i < nb ? m->schedule[i] : nb + i;   // past the end: inactive (joins the exchange with zeros)
+    *n = i < nb ? seeds(*g) : 0;
+    *offset = i < nb ? *g * B : 0;
+    int64_t bt = 0;
+    for (int64_t r = 0; r < m->world; ++r)
+        if (step * m->world + r < nb) bt += seeds(m->schedule[step * m->world + r]);
+    *b_total = (int32_t)bt;
+}
+
 gnn_status issue_sample_step(gnn_model* m, int set, int64_t epoch, int64_t step) {
     TRY(ensure_perm(m, epoch));
     int64_t g, offset;
     int32_t n, b_total;
-    plan_step(m->n_train, m->cfg.batch_size, m->world, m->rank, step, &g, &n, &offset, &b_total);
+    plan_model_step(m, step, &g, &n, &offset, &b_total);
     return issue_sample(m, set, n > 0 ? m->perm + offset : m->perm, nullptr, n, b_total, epoch, g, m->full_train);
 }
 
@@ -548,7 +570,7 @@ gnn_status train_set(gnn_model* m, int set) {
 gnn_status step_from_perm(gnn_model* m, int64_t epoch, int64_t step) {
     int64_t g, offset;
     int32_t n, b_total;
-    plan_step(m->n_train, m->cfg.batch_size, m->world, m->rank, step, &g, &n, &offset, &b_total);
+    plan_model_step(m, step, &g, &n, &offset, &b_total);
     int cur = find_set(m, epoch, g, n, b_total);
     if (cur < 0) {
         cur = other_set(m);
@@ -711,6 +733,9 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     if (c.batch_size < 1 || c.batch_size > 1024) return fail(GNN_ERR_CONFIG, "batch_size must be 1..1024");
     if (c.num_layers > 1 && (c.hidden < 16 || c.hidden % 16)) return fail(GNN_ERR_CONFIG, "hidden must be a positive multiple of 16");
     if (c.precision != GNN_FP32 && c.precision != GNN_BF16_GEMM) return fail(GNN_ERR_CONFIG, "unknown precision");
+    if (c.optimizer != GNN_SGD && c.optimizer != GNN_ADAM) return fail(GNN_ERR_CONFIG, "unknown optimizer");
+    if (c.optimizer == GNN_ADAM && !(c.beta1 >= 0.f && c.beta1 < 1.f && c.beta2 >= 0.f && c.beta2 < 1.f && c.eps > 0.f))
+        return fail(GNN_ERR_CONFIG, "Adam needs 0 <= beta1, beta2 < 1 and eps > 0");
     if (!(c.lr >= 0.f)) return fail(GNN_ERR_PARAM, "lr must be >= 0");
     TRY(set_device(g->dev));
 
@@ -908,6 +933,17 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     }
     AL(m->params, m->pcount);
     AL(m->grads, m->pcount);
+    if (c.optimizer == GNN_ADAM) {
+        AL(m->opt.m, m->pcount);
+        AL(m->opt.v, m->pcount);
+        AL(m->opt.t, 1);
+        AL(m->opt.done, 1);
+        CK(cudaMemset(m->opt.m, 0, sizeof(float) * m->pcount));
+        CK(cudaMemset(m->opt.v, 0, sizeof(float) * m->pcount));
+        CK(cudaMemset(m->opt.t, 0, sizeof(int32_t)));
+        CK(cudaMemset(m->opt.done, 0, sizeof(unsigned)));
+        m->opt.beta1 = c.beta1; m->opt.beta2 = c.beta2; m->opt.eps = c.eps;
+    }
 #undef AL
     CK(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&m->sstream, cudaStreamNonBlocking));
@@ -921,7 +957,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         const float bound = std::sqrt(6.0f / (float)(ly.in + ly.out));
         launch_init_params(m->params + ly.poff, ly.pcnt, bound, c.init_seed, (uint32_t)li, m->stream);
     }
-    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, false, m->stream);
+    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, false, OptState{}, m->stream);
     CK(cudaMemsetAsync(m->grads, 0, sizeof(float) * m->pcount, m->stream));
     CK(cudaStreamSynchronize(m->stream));
     CK(cudaDeviceSynchronize());
@@ -1019,7 +1055,7 @@ gnn_status gnn_set_params(gnn_model* m, const float* in_host, int64_t n) {
     if (n != m->pcount) return fail(GNN_ERR_SHAPE, "n != param_count");
     TRY(set_device(m->g->dev));
     CK(cudaMemcpyAsync(m->params, in_host, sizeof(float) * n, cudaMemcpyHostToDevice, m->stream));
-    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, false, m->stream);
+    launch_sgd_pack(pack_desc(m), m->params, nullptr, 0.f, false, OptState{}, m->stream);
     CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }
@@ -1197,7 +1233,7 @@ gnn_status gnn_train_epoch(gnn_model* m, int64_t epoch, gnn_epoch_stats* out_hos
         out_host->seconds = ms * 1e-3;
         out_host->steps = steps;
         int64_t mine = 0;
-        for (int64_t s = 0; s < steps; ++s) mine += (s * m->world + m->rank) < nb;
+        for (int64_t s = 0; s < steps; ++s) mine += (s * m->world + m->rank) < nb;   // same count under a schedule
         out_host->minibatches = mine;
         out_host->mean_loss = steps ? tot / (double)steps : 0.0;
     }
@@ -1305,6 +1341,79 @@ gnn_status gnn_profile_reset(gnn_model* m) {
 }
 
 int64_t gnn_launches_per_step(const gnn_model* m) { return m ? m->launches_per_step : -1; }
+// ---------------------------------------------------------------- NEXT-3: workload-aware batch assignment
+gnn_status gnn_estimate_workload(gnn_model* m, int64_t epoch, int64_t* work_out_host, int64_t n) {
+    if (!m || !work_out_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    const int64_t nb = num_batches(m);
+    if (n != nb) return fail(GNN_ERR_SHAPE, "n must equal the number of batches " + std::to_string(nb));
+    TRY(set_device(m->g->dev));
+    TRY(sync_all(m));
+    TRY(ensure_perm(m, epoch));
+    const int64_t B = m->cfg.batch_size;
+    const bool prof = m->profiling;
+    m->profiling = false;
+    gnn_status st_ = GNN_OK;
+    for (int64_t g = 0; g < nb && st_ == GNN_OK; ++g) {
+        const int set = other_set(m);
+        const int32_t cnt = (int32_t)std::min<int64_t>(B, m->n_train - g * B);
+        st_ = issue_sample(m, set, m->perm + g * B, nullptr, cnt, cnt, epoch, g, true);
+        if (st_ != GNN_OK) break;
+        m->bs[set].valid = false;
+        StepState ss;
+        st_ = copy_state(m, set, &ss);
+        // aggregations of the computational graph: the edges every layer aggregates over
+        int64_t w = 0;
+        for (int li = 0; li < m->L; ++li) w += ss.n_edges[m->layers[li].blk];
+        work_out_host[g] = w;
+    }
+    m->profiling = prof;
+    return st_;
+}
+
+gnn_status gnn_plan_balanced(const int64_t* work_host, int64_t n, int32_t world, int64_t* order_out_host) {
+    if (n < 0 || world < 1 || (n > 0 && (!work_host || !order_out_host))) return fail(GNN_ERR_PARAM, "bad arguments");
+    std::vector<int64_t> idx(n);
+    for (int64_t i = 0; i < n; ++i) idx[i] = i;
+    // heaviest first (ties: lower batch index first); consecutive groups of `world` are the steps,
+    // so every step's batches have similar work and the lightest batches share the ragged last step
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return work_host[a] > work_host[b]; });
+    const int64_t steps = (n + world - 1) / world;
+    std::vector<int64_t> first(steps);
+    for (int64_t s = 0; s < steps; ++s) {
+        int64_t mn = INT64_MAX;
+        for (int64_t i = s * world; i < std::min<int64_t>(n, (s + 1) * world); ++i) mn = std::min(mn, idx[i]);
+        first[s] = mn;
+    }
+    // steps in the order of their smallest batch index (the epoch permutation's order)
+    std::vector<int64_t> sorder(steps);
+    for (int64_t s = 0; s < steps; ++s) sorder[s] = s;
+    std::sort(sorder.begin(), sorder.end(), [&](int64_t a, int64_t b) { return first[a] < first[b]; });
+    int64_t o = 0;
+    for (int64_t s : sorder) {
+        if (s == steps - 1 && n % world) continue;   // the ragged group stays last
+        for (int64_t i = s * world; i < (s + 1) * world; ++i) order_out_host[o++] = idx[i];
+    }
+    if (n % world)
+        for (int64_t i = (steps - 1) * world; i < n; ++i) order_out_host[o++] = idx[i];
+    return GNN_OK;
+}
+
+gnn_status gnn_set_schedule(gnn_model* m, const int64_t* order_host, int64_t n) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    if (n == 0) { m->schedule.clear(); return GNN_OK; }
+    const int64_t nb = num_batches(m);
+    if (!order_host || n != nb) return fail(GNN_ERR_SHAPE, "schedule must list every batch once");
+    std::vector<char> seen(nb, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        if (order_host[i] < 0 || order_host[i] >= nb || seen[order_host[i]]) return fail(GNN_ERR_PARAM, "schedule is not a permutation of the batches");
+        seen[order_host[i]] = 1;
+    }
+    TRY(sync_all(m));
+    m->schedule.assign(order_host, order_host + n);
+    for (auto& B : m->bs) B.valid = false;   // prefetched batches followed the previous rule
+    return GNN_OK;
+}
+
 int32_t gnn_graph_symmetric(const gnn_graph* g) { return g ? (g->symmetric ? 1 : 0) : -1; }
 
 }  // extern "C"

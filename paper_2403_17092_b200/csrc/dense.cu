@@ -602,16 +602,29 @@ __global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
     }
 }
 
-// SGD (W <- W - lr G, §2.2) fused with the repack of the GEMM weight planes
-// W [K_pad x N_pad] (coalesced in that order; padding entries stay the zeros written at
-// creation).  Each parameter is visited exactly once.  grads == nullptr: pack only.
+// SGD (W <- W - lr G, §2.2) or Adam (NEXT-4, the listings' torch.optim.Adam,
+// P:L398) fused with the repack of the GEMM weight planes W [K_pad x N_pad] (coalesced in that
+// order; padding entries stay the zeros written at creation).  Each parameter is visited exactly
+// once.  grads == nullptr: pack only.
 // reduce (single rank, no exchange in between): G is first reduced from the wgrad split-K
 // partials in the fixed split order (the arithmetic of k_wgrad_reduce_all) and stored.
-__global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restrict__ grads, float lr, int reduce) {
+// Adam: t = *o.t + 1 for every thread; bias corrections in fp64; the last block to finish
+// stores t (the next step's kernel starts after this one completes).
+__global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restrict__ grads, float lr, int reduce,
+                           OptState o) {
     pdl_trigger();
     pdl_wait();
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const bool adam = o.m != nullptr && grads != nullptr;
+    int t = 0;
+    float step = 0.f, inv_sqrt_bc2 = 0.f;
+    if (adam) {
+        t = *o.t + 1;
+        const double bc1 = 1.0 - pow((double)o.beta1, (double)t), bc2 = 1.0 - pow((double)o.beta2, (double)t);
+        step = (float)((double)lr / bc1);
+        inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+    }
     for (int l = 0; l < P.n; ++l) {
         const PackLayer& L = P.l[l];
         const int64_t total = (int64_t)L.k_pad * L.n_pad;
@@ -638,11 +651,26 @@ __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restr
                 } else {
                     gr = grads[idx];
                 }
-                w = w - lr * gr;
+                if (adam) {   // m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2; W -= step m / (sqrt(v)/sqrt(bc2) + eps)
+                    const float mm = o.beta1 * o.m[idx] + (1.f - o.beta1) * gr;
+                    const float vv = o.beta2 * o.v[idx] + (1.f - o.beta2) * gr * gr;
+                    o.m[idx] = mm;
+                    o.v[idx] = vv;
+                    w = w - step * mm / (sqrtf(vv) * inv_sqrt_bc2 + o.eps);
+                } else {
+                    w = w - lr * gr;
+                }
                 params[idx] = w;
             }
             store_split1(L.Wkn, f, w);
         }
+    }
+    if (adam) {
+        __shared__ bool last;
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(o.done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last && threadIdx.x == 0) { *o.t = t; *o.done = 0u; }
     }
 }
 
@@ -777,8 +805,9 @@ void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s) {
     launch_pdl(k_wgrad_reduce_all, 148 * 4, 256, 0, s, p, grads);
 }
 
-void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, cudaStream_t s) {
-    launch_pdl(k_sgd_pack, reduce ? 148 * 8 : 148 * 2, 256, 0, s, p, params, grads, lr, reduce ? 1 : 0);
+void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, const OptState& o,
+                     cudaStream_t s) {
+    launch_pdl(k_sgd_pack, reduce ? 148 * 8 : 148 * 2, 256, 0, s, p, params, grads, lr, reduce ? 1 : 0, o);
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,

@@ -173,9 +173,14 @@ struct PackLayer {
 struct PackAll { PackLayer l[kMaxHops]; int n; bool sage; };
 // grads[poff + r*out + c] = Σ_z part[z][rpad(r)*n_pad + c] for every layer, fixed z order.
 void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s);
-// W <- W - lr*G (grads may be nullptr: pack only) and the bf16 planes of W, all layers.
-// reduce: G = the fixed-order sum of the wgrad partials, written to grads first (one rank).
-void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, cudaStream_t s);
+// Optimizer state: m == nullptr -> SGD; else Adam with moments m, v (flat like params), the
+// device step count *t (steps applied so far) and a block counter (zero between launches).
+struct OptState { float* m; float* v; int32_t* t; unsigned* done; float beta1, beta2, eps; };
+// W <- W - lr*G (SGD) or the Adam update (grads may be nullptr: pack only) and the bf16 planes
+// of W, all layers.  reduce: G = the fixed-order sum of the wgrad partials, written to grads
+// first (one rank).
+void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, const OptState& o,
+                     cudaStream_t s);
 // Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total
 // written as split planes [rows x ldz] (+ zero tail rows).
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels,

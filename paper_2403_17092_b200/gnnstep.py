@@ -15,6 +15,7 @@ GNN_NEIGHBOR, GNN_SHADOW = 0, 1
 GNN_FP32, GNN_BF16_GEMM = 0, 1
 GNN_SRC_IDS, GNN_BLK_ROWPTR, GNN_BLK_COL, GNN_BLK_NBR = 0, 1, 2, 3
 GNN_DBG_LOGITS, GNN_DBG_GRADS, GNN_DBG_LOSS, GNN_DBG_ACT = 0, 1, 2, 16
+GNN_SGD, GNN_ADAM = 0, 1
 KERNEL_IDS = dict(sample=0, relabel=1, agg_l1=2, agg=3, gemm_fwd=4, gemm_dgrad=5, gemm_wgrad=6,
                   spmm_bwd=7, ce=8, sgd=9, transpose=10, induce=11, allreduce=12, scan=13, other=14)
 
@@ -32,7 +33,8 @@ class _Config(C.Structure):
     _fields_ = [("model", C.c_int32), ("sampler", C.c_int32), ("num_layers", C.c_int32),
                 ("hidden", C.c_int32), ("batch_size", C.c_int32), ("num_fanouts", C.c_int32),
                 ("fanouts", C.c_int32 * 8), ("precision", C.c_int32), ("use_graph", C.c_int32),
-                ("lr", C.c_float), ("seed", C.c_uint64), ("init_seed", C.c_uint64)]
+                ("lr", C.c_float), ("seed", C.c_uint64), ("init_seed", C.c_uint64),
+                ("optimizer", C.c_int32), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
 
 
 class _Sizes(C.Structure):
@@ -74,6 +76,8 @@ def lib():
             "gnn_profile_enable": ([P, I32], I32), "gnn_profile_read": ([P, I32, P, P], I32),
             "gnn_profile_reset": ([P], I32), "gnn_launches_per_step": ([P], I64),
             "gnn_graph_symmetric": ([P], I32),
+            "gnn_estimate_workload": ([P, I64, P, I64], I32), "gnn_plan_balanced": ([P, I64, I32, P], I32),
+            "gnn_set_schedule": ([P, P, I64], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(_lib, name)
@@ -137,7 +141,7 @@ class Model:
 
     def __init__(self, graph: Graph, model="sage", sampler="neighbor", num_layers=2, hidden=32,
                  batch_size=64, fanouts=(10, 5), precision="fp32", use_graph=True, lr=0.01, seed=1,
-                 init_seed=2):
+                 init_seed=2, optimizer="sgd", betas=(0.9, 0.999), eps=1e-8):
         cfg = _Config()
         cfg.model = GNN_SAGE_MEAN if model == "sage" else GNN_GCN
         cfg.sampler = GNN_NEIGHBOR if sampler == "neighbor" else GNN_SHADOW
@@ -148,6 +152,10 @@ class Model:
         cfg.precision = GNN_FP32 if precision == "fp32" else GNN_BF16_GEMM
         cfg.use_graph = 1 if use_graph else 0
         cfg.lr, cfg.seed, cfg.init_seed = lr, seed, init_seed
+        if optimizer not in ("sgd", "adam"):
+            raise ValueError("optimizer must be 'sgd' or 'adam'")
+        cfg.optimizer = GNN_SGD if optimizer == "sgd" else GNN_ADAM
+        cfg.beta1, cfg.beta2, cfg.eps = betas[0], betas[1], eps
         self.graph = graph
         self.model, self.sampler, self.num_layers = model, sampler, num_layers
         self.fanouts = tuple(fanouts)
@@ -314,6 +322,20 @@ class Model:
         _check(lib().gnn_profile_read(self.h, KERNEL_IDS[kernel], C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def estimate_workload(self, epoch: int) -> np.ndarray:
+        """gnn_estimate_workload: aggregations (Σ_l E(block_l)) of every batch of `epoch`."""
+        out = np.zeros(self.num_batches, dtype=np.int64)
+        _check(lib().gnn_estimate_workload(self.h, epoch, _ptr(out), out.shape[0]))
+        return out
+
+    def set_schedule(self, order):
+        """gnn_set_schedule: step s, rank r trains batch order[s*world + r]; None restores the default."""
+        if order is None:
+            _check(lib().gnn_set_schedule(self.h, None, 0))
+            return
+        o = np.ascontiguousarray(order, dtype=np.int64)
+        _check(lib().gnn_set_schedule(self.h, _ptr(o), o.shape[0]))
+
     @property
     def launches_per_step(self) -> int:
         return lib().gnn_launches_per_step(self.h)
@@ -340,6 +362,14 @@ def plan_step(n_train: int, batch_size: int, world: int, rank: int, step: int):
     _check(L.gnn_plan_step(n_train, batch_size, world, rank, step, C.byref(g), C.byref(n), C.byref(off),
                            C.byref(bt)))
     return g.value, n.value, off.value, bt.value
+
+
+def plan_balanced(work, world: int) -> np.ndarray:
+    """gnn_plan_balanced (host only): the workload-balanced batch order (NEXT-3)."""
+    w = np.ascontiguousarray(work, dtype=np.int64)
+    out = np.zeros(w.shape[0], dtype=np.int64)
+    _check(lib().gnn_plan_balanced(_ptr(w), w.shape[0], world, _ptr(out)))
+    return out
 
 
 def steps_per_epoch(n_train: int, batch_size: int, world: int) -> int:

@@ -30,12 +30,12 @@ def inputs_for(name):
     return _cache[name]
 
 
-def make_gpu(w, inp, use_graph=True, precision="fp32", batch_size=None, params=None):
+def make_gpu(w, inp, use_graph=True, precision="fp32", batch_size=None, params=None, optimizer="sgd"):
     from paper_2403_17092_b200 import Graph, Model
     g = Graph(inp["row_ptr"], inp["col"], inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim)
     m = Model(g, model=w.model, sampler=w.sampler, num_layers=w.num_layers, hidden=w.hidden,
               batch_size=batch_size or w.batch_size, fanouts=w.fanouts, precision=precision,
-              use_graph=use_graph, lr=w.lr, seed=w.sampler_seed, init_seed=w.init_seed)
+              use_graph=use_graph, lr=w.lr, seed=w.sampler_seed, init_seed=w.init_seed, optimizer=optimizer)
     m.set_train_nodes(inp["train"])
     m.set_params(inp["params"] if params is None else params)
     return g, m

@@ -201,3 +201,64 @@ def test_symmetry_check():
     rp2[v + 1:] -= 1
     g2 = Graph(rp2, col[keep], inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim)
     assert not g2.symmetric
+
+
+# ---------------------------------------------------------------- NEXT-4: Adam
+@pytest.mark.parametrize("name", ["tiny", "tiny_gcn"])
+def test_adam_training_parity(name):
+    """Adam on the device (fused with the split-K reduce and the weight repack) against the
+    oracle's Adam (oracle.model.adam, pinned to torch.optim.Adam) applied to the oracle's own
+    gradients: 20 steps and the ragged last batch; loss/logits/grads per step and the
+    parameters after every update within 1e-4."""
+    from oracle import model as OM
+    w, inp, graph = inputs_for(name)
+    g, m = make_gpu(w, inp, optimizer="adam")
+    params = inp["params"].astype(np.float64)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    state = {}
+    for step in list(range(20)) + [w.n_batches - 1]:
+        loss = m.train_minibatch(0, step)
+        out = check_train_step(m, w, graph, params, 0, step, perm, loss)
+        Ws = OM.unflatten(params, w.dims, w.model)
+        G = OM.unflatten(out["grad"], w.dims, w.model)
+        params = OM.flatten(OM.adam(Ws, G, state, w.lr))
+        assert rel(m.get_params(), params) <= TOL_FP32, step
+
+
+# ---------------------------------------------------------------- NEXT-3: workload-aware batch assignment
+@pytest.mark.parametrize("name", ["tiny", "tiny_sage_shadow"])
+def test_workload_estimate_equals_oracle(name):
+    """gnn_estimate_workload (the sampler run over the whole epoch) == the oracle's
+    aggregation count of every batch."""
+    from oracle import balance
+    w, inp, graph = inputs_for(name)
+    g, m = make_gpu(w, inp)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    got = m.estimate_workload(0)
+    batches = range(w.n_batches) if name == "tiny" else (0, 1, w.n_batches - 1)
+    for b in batches:
+        s, _ = oracle.sample_batch(w, graph, 0, b, perm)
+        assert got[b] == balance.workload(s, w.sampler, w.num_layers), b
+
+
+def test_scheduled_training_parity():
+    """With the balanced schedule (world = 1: step s trains batch order[s]) every step equals
+    the oracle step on that batch, including the ragged last batch wherever it lands."""
+    from oracle import balance
+    from paper_2403_17092_b200 import plan_balanced
+    w, inp, graph = inputs_for("tiny")
+    g, m = make_gpu(w, inp)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    work = m.estimate_workload(0)
+    order = plan_balanced(work, 1)
+    assert list(order) == balance.plan(work, 1)
+    m.set_schedule(order)
+    params = inp["params"].astype(np.float64)
+    ragged = int(np.nonzero(order == w.n_batches - 1)[0][0])
+    for step in list(range(6)) + [ragged]:
+        m.set_params(params)
+        loss = m.train_minibatch(0, step)
+        out = check_train_step(m, w, graph, params, 0, int(order[step]), perm, loss)
+        params = out["params"]
+        assert rel(m.get_params(), params) <= TOL_FP32
+    m.set_schedule(None)

@@ -221,3 +221,68 @@ def test_adam_first_step_closed_form():
     out = M.adam([W], [g], state, lr=0.1)[0]
     assert np.allclose(out, -0.1 * g / (np.abs(g) + 1e-8), rtol=1e-12, atol=0)
     assert out[0, 2] == 0.0 and state["t"] == 1
+
+
+# ---------------------------------------------------------------- NEXT-3: workload-aware assignment
+def _partitions(items, size):
+    """All ways to split `items` into groups of `size` (the last group may be smaller)."""
+    if len(items) <= size:
+        yield [items]
+        return
+    import itertools
+    first, rest = items[0], items[1:]
+    for comb in itertools.combinations(rest, size - 1):
+        group = [first, *comb]
+        left = [x for x in rest if x not in comb]
+        for p in _partitions(left, size):
+            yield [group] + p
+
+
+def test_balanced_plan_is_optimal_by_brute_force():
+    """Sorted consecutive grouping minimises Σ_steps max work (exchange argument); pinned by
+    enumerating every grouping of up to 8 batches into steps of P = 2 and 3 (when P divides n,
+    so that every step has P batches)."""
+    from oracle import balance
+    rng = np.random.default_rng(3)
+    for n, P in ((4, 2), (6, 2), (6, 3), (8, 2)):
+        for _ in range(5):
+            work = rng.integers(1, 100, size=n)
+            best = min(sum(max(work[i] for i in g) for g in part) for part in _partitions(list(range(n)), P))
+            order = balance.plan(work, P)
+            assert sorted(order) == list(range(n))
+            assert balance.makespan(order, work, P) == best
+
+
+def test_balanced_plan_never_worse_than_round_robin():
+    from oracle import balance
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        n, P = int(rng.integers(1, 60)), int(rng.integers(1, 9))
+        work = rng.pareto(1.5, size=n) * 100 + 1
+        work = work.astype(np.int64)
+        assert balance.makespan(balance.plan(work, P), work, P) <= balance.makespan(list(range(n)), work, P)
+
+
+def test_workload_closed_form_when_every_degree_exceeds_fanout():
+    """On a complete graph K_n every frontier node has degree n-1 >= k, so hop h samples exactly
+    k_h edges per destination: workload = Σ_h n_dst(h) * k_h (SPEC-style closed form)."""
+    from oracle import balance
+    n = 40
+    row_ptr = np.arange(0, n * (n - 1) + 1, n - 1, dtype=np.int64)
+    col = np.array([u for v in range(n) for u in range(n) if u != v], dtype=np.int32)
+    fan = [4, 3]                      # input-layer-first: seeds sample 3, then 4
+    seeds = np.array([0, 5, 7], dtype=np.int32)
+    hops = S.neighbor_sample(row_ptr, col, seeds, fan, 1, 0, 0)
+    want = hops[0]["n_dst"] * 3 + hops[1]["n_dst"] * 4
+    assert balance.workload(hops, "neighbor", 2) == want
+
+
+def test_library_planner_matches_oracle_plan():
+    """gnn_plan_balanced (host-only C++ in libgnnstep.so) == the oracle's plan."""
+    from oracle import balance
+    from paper_2403_17092_b200 import plan_balanced
+    rng = np.random.default_rng(6)
+    for _ in range(40):
+        n, P = int(rng.integers(0, 300)), int(rng.integers(1, 9))
+        work = rng.integers(0, 50, size=n).astype(np.int64)   # many ties
+        assert list(plan_balanced(work, P)) == balance.plan(work, P), (n, P)
