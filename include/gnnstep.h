@@ -94,6 +94,20 @@ gnn_status gnn_graph_create_sharded(int64_t num_nodes, const int64_t* row_ptr_ho
                                     gnn_graph** out);
 gnn_status gnn_shard_export(gnn_graph* g, uint8_t handle_out_host[64]);
 gnn_status gnn_shard_import(gnn_graph* g, const uint8_t* handles_host);
+/* NEXT-2: GPU feature cache (§3.3), re-aimed at the
+ * NVLink-sharded table: a local replica of hot REMOTE rows, so their layer-1 gathers read local
+ * HBM instead of a peer.  gnn_cache_rows (after gnn_shard_import): replicate rows ids[0:n) (host
+ * array, distinct, none owned by this process: PARAM; out of range: RANGE) read from their
+ * owners; n = 0 drops the cache.  Results are unchanged (a replica is an exact copy); models and
+ * captured CUDA graphs pick the cache up at their next step.  Synchronous; call it while no
+ * step of a model on this graph is in flight.  STATE if the graph is not sharded or not imported.
+ * gnn_cache_plan_by_degree (host only): the `capacity` remote rows of shard `shard` (of
+ * nshards, uniform blocks of ceil(N/nshards) rows) with the highest CSR degree (ties: lower
+ * id), ascending in ids_out_host; *n_out_host = their count (a static hot set: a node is
+ * sampled about in proportion to its degree). */
+gnn_status gnn_cache_rows(gnn_graph* g, const int32_t* ids_host, int64_t n);
+gnn_status gnn_cache_plan_by_degree(const int64_t* row_ptr_host, int64_t num_nodes, int32_t nshards, int32_t shard,
+                                    int64_t capacity, int32_t* ids_out_host, int64_t* n_out_host);
 
 /* ---------------------------------------------------------------- model
  * Layers l = 1..L are numbered input-first; dims = [F, hidden, ..., hidden, C].

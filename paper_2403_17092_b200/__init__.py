@@ -4,6 +4,7 @@ The product is the C-ABI library libgnnstep.so (include/gnnstep.h, sources in cs
 this package is its thin Python binding.  No CPU fallback exists.
 """
 from .gnnstep import (Graph, Model, GnnError, comm_get_unique_id, lib, KERNEL_IDS, plan_step,  # noqa: F401
-                      steps_per_epoch, ShardedGraph, shard_rows, plan_balanced)
+                      steps_per_epoch, ShardedGraph, shard_rows, plan_balanced,
+                      cache_plan_by_degree)
 
 __all__ = ["Graph", "Model", "GnnError", "comm_get_unique_id", "lib", "KERNEL_IDS"]

@@ -86,7 +86,15 @@ struct gnn_graph {
     const float** shard_ptrs = nullptr;
     std::vector<void*> ipc_opened;
     std::vector<void*> owned;
-    FeatRows rows() const { return FeatRows{X, nshards ? shard_ptrs : nullptr, rps}; }
+    // NEXT-2 feature cache of remote rows (sharded tables): device descriptor + its buffers
+    FeatCache* cache_desc = nullptr;
+    int32_t* cmap = nullptr;
+    float* cache_rows = nullptr;
+    int64_t cache_n = 0;
+    FeatRows rows() const {
+        return FeatRows{X, nshards ? shard_ptrs : nullptr, rps, nshards ? cache_desc : nullptr,
+                        rps ? (int)(row_begin / rps) : 0};
+    }
 };
 
 namespace {
@@ -635,6 +643,73 @@ gnn_status gnn_shard_export(gnn_graph* g, uint8_t handle_out_host[64]) {
     return GNN_OK;
 }
 
+gnn_status gnn_cache_rows(gnn_graph* g, const int32_t* ids_host, int64_t n) {
+    if (!g || (n > 0 && !ids_host) || n < 0) return fail(GNN_ERR_PARAM, "bad arguments");
+    if (g->nshards < 1) return fail(GNN_ERR_STATE, "graph is not sharded");
+    if (!g->shard_ptrs) return fail(GNN_ERR_STATE, "gnn_cache_rows needs gnn_shard_import first");
+    TRY(set_device(g->dev));
+    std::vector<char> seen(n ? g->N : 0, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t v = ids_host[i];
+        if (v < 0 || v >= g->N) return fail(GNN_ERR_RANGE, "cache row id out of range");
+        if (v >= g->row_begin && v < g->row_end) return fail(GNN_ERR_PARAM, "cache row " + std::to_string(v) + " is local");
+        if (seen[v]) return fail(GNN_ERR_PARAM, "duplicate cache row id");
+        seen[v] = 1;
+    }
+    CK(cudaDeviceSynchronize());   // no kernel may be reading the previous cache
+    if (!g->cache_desc) {
+        gnn_status st = dalloc(&g->cache_desc, 1, g->owned);
+        if (st != GNN_OK) return st;
+        CK(cudaMemset(g->cache_desc, 0, sizeof(FeatCache)));
+    }
+    FeatCache off{nullptr, nullptr};
+    CK(cudaMemcpy(g->cache_desc, &off, sizeof(FeatCache), cudaMemcpyHostToDevice));
+    if (g->cache_rows) { cudaFree(g->cache_rows); g->cache_rows = nullptr; }
+    g->cache_n = 0;
+    if (n == 0) return GNN_OK;
+    if (!g->cmap) {
+        CK(cudaMalloc(&g->cmap, sizeof(int32_t) * g->N));
+    }
+    CK(cudaMemset(g->cmap, 0xff, sizeof(int32_t) * g->N));
+    int32_t* ids_dev = nullptr;
+    CK(cudaMalloc(&ids_dev, sizeof(int32_t) * n));
+    CK(cudaMalloc(&g->cache_rows, sizeof(float) * n * g->stride));
+    CK(cudaMemcpy(ids_dev, ids_host, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    launch_cache_fill(g->rows(), ids_dev, n, g->stride, g->cache_rows, nullptr);
+    std::vector<int32_t> slots(g->N, -1);
+    for (int64_t i = 0; i < n; ++i) slots[ids_host[i]] = (int32_t)i;
+    CK(cudaMemcpy(g->cmap, slots.data(), sizeof(int32_t) * g->N, cudaMemcpyHostToDevice));
+    CK(cudaDeviceSynchronize());
+    cudaFree(ids_dev);
+    FeatCache on{g->cmap, g->cache_rows};
+    CK(cudaMemcpy(g->cache_desc, &on, sizeof(FeatCache), cudaMemcpyHostToDevice));
+    g->cache_n = n;
+    return GNN_OK;
+}
+
+gnn_status gnn_cache_plan_by_degree(const int64_t* row_ptr_host, int64_t num_nodes, int32_t nshards, int32_t shard,
+                                    int64_t capacity, int32_t* ids_out_host, int64_t* n_out_host) {
+    if (!row_ptr_host || !ids_out_host || !n_out_host || num_nodes < 0 || nshards < 1 || shard < 0 ||
+        shard >= nshards || capacity < 0)
+        return fail(GNN_ERR_PARAM, "bad arguments");
+    const int64_t rps = (num_nodes + nshards - 1) / nshards;
+    const int64_t b = std::min<int64_t>(num_nodes, (int64_t)shard * rps), e = std::min<int64_t>(num_nodes, b + rps);
+    std::vector<int32_t> cand;
+    cand.reserve(num_nodes - (e - b));
+    for (int64_t v = 0; v < num_nodes; ++v)
+        if (v < b || v >= e) cand.push_back((int32_t)v);
+    auto deg = [&](int32_t v) { return row_ptr_host[v + 1] - row_ptr_host[v]; };
+    const int64_t k = std::min<int64_t>(capacity, (int64_t)cand.size());
+    // hottest rows: highest degree first (a node is sampled about in proportion to its degree), ties by id
+    std::partial_sort(cand.begin(), cand.begin() + k, cand.end(), [&](int32_t a, int32_t c) {
+        return deg(a) != deg(c) ? deg(a) > deg(c) : a < c;
+    });
+    std::sort(cand.begin(), cand.begin() + k);
+    std::copy(cand.begin(), cand.begin() + k, ids_out_host);
+    *n_out_host = k;
+    return GNN_OK;
+}
+
 gnn_status gnn_shard_import(gnn_graph* g, const uint8_t* handles_host) {
     if (!g || !handles_host) return fail(GNN_ERR_PARAM, "NULL argument");
     if (g->nshards < 1) return fail(GNN_ERR_STATE, "graph is not sharded");
@@ -715,6 +790,8 @@ gnn_status gnn_graph_destroy(gnn_graph* g) {
     cudaSetDevice(g->dev);
     for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
     for (void* p : g->owned) cudaFree(p);
+    if (g->cmap) cudaFree(g->cmap);
+    if (g->cache_rows) cudaFree(g->cache_rows);
     delete g;
     return GNN_OK;
 }

@@ -107,17 +107,34 @@ __host__ __device__ __forceinline__ int64_t tix(const Split& o, int64_t r, int64
 
 // Rows of an aggregation input: a local buffer (shards == nullptr), or the feature table
 // row-sharded over peers (config 4): row r lives in shard r / rps at local row r % rps; the
-// shard pointers are CUDA-IPC mappings of the peers' HBM (NVLink peer loads).
+// shard pointers are CUDA-IPC mappings of the peers' HBM (NVLink peer loads).  NEXT-2: a
+// remote row with a local replica (cache->cmap[r] = slot >= 0) is read from cache->rows
+// instead (the GPU feature cache of PAPER.md §3.3, re-aimed at NVLink traffic).
+// The cache descriptor lives in device memory at a fixed address, so captured CUDA graphs
+// see a cache installed after capture.
+struct FeatCache { const int32_t* cmap; const float* rows; };
 struct FeatRows {
     const float* base;
     const float* const* shards;
     int64_t rps;
+    const FeatCache* cache;   // sharded tables only (nullable)
+    int own;                  // this process's shard
     __device__ __forceinline__ const float* row(int r, int ld) const {
         if (!shards) return base + (int64_t)r * ld;
         const int s = (int)(r / rps);
+        if (s == own) return base + (int64_t)(r - s * rps) * ld;
+        if (cache) {
+            const int32_t* cm = cache->cmap;
+            if (cm) {
+                const int c = __ldg(cm + r);
+                if (c >= 0) return cache->rows + (int64_t)c * ld;
+            }
+        }
         return shards[s] + (int64_t)(r - s * rps) * ld;
     }
 };
+// NEXT-2: copy rows ids[0:n) of the (sharded) table into cache rows [0, n) (peer loads).
+void launch_cache_fill(FeatRows src, const int32_t* ids, int64_t n, int ld, float* out, cudaStream_t s);
 
 // SAGE-mean aggregation into A = [H_self | mean] for rows i < *rows_ptr.  Neighbour row of
 // source c is gmap ? gmap[c] : c, self row smap ? smap[i] : i (layer 1 reads X by global id:

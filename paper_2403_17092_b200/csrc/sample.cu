@@ -36,7 +36,25 @@ __global__ void k_check_symmetric(const int64_t* __restrict__ row_ptr, const int
     }
 }
 
+// NEXT-2 cache fill: a warp per cached row, 16-byte chunks (the row read like the aggregation reads it).
+__global__ void k_cache_fill(FeatRows src, const int32_t* __restrict__ ids, int64_t n, int ld, float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < n; i += nw) {
+        const float4* p = reinterpret_cast<const float4*>(src.row(ids[i], ld));
+        float4* q = reinterpret_cast<float4*>(out + i * ld);
+        for (int c = lane; c < (ld >> 2); c += 32) q[c] = p[c];
+    }
+}
+
 }  // namespace
+
+void launch_cache_fill(FeatRows src, const int32_t* ids, int64_t n, int ld, float* out, cudaStream_t s) {
+    if (n <= 0) return;
+    src.cache = nullptr;   // read the owners' copies
+    k_cache_fill<<<148 * 8, 256, 0, s>>>(src, ids, n, ld, out);
+}
 
 bool check_symmetric(const int64_t* row_ptr, const int32_t* col, int64_t n, bool* symmetric) {
     int* d = nullptr;

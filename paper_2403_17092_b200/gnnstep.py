@@ -410,6 +410,17 @@ class ShardedGraph(Graph):
         _check(L.gnn_shard_export(self.h, buf))
         return bytes(buf)
 
+    def cache_rows(self, ids):
+        """gnn_cache_rows: replicate these remote rows locally (NEXT-2); empty/None drops the cache."""
+        L = lib()
+        L.gnn_cache_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.gnn_cache_rows.restype = C.c_int32
+        if ids is None or len(ids) == 0:
+            _check(L.gnn_cache_rows(self.h, None, 0))
+            return
+        a = np.ascontiguousarray(ids, dtype=np.int32)
+        _check(L.gnn_cache_rows(self.h, _ptr(a), a.shape[0]))
+
     def import_handles(self, handles):
         blob = b"".join(handles)
         buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
@@ -417,6 +428,20 @@ class ShardedGraph(Graph):
         L.gnn_shard_import.argtypes = [C.c_void_p, C.c_void_p]
         L.gnn_shard_import.restype = C.c_int32
         _check(L.gnn_shard_import(self.h, buf))
+
+
+def cache_plan_by_degree(row_ptr, nshards: int, shard: int, capacity: int) -> np.ndarray:
+    """gnn_cache_plan_by_degree (host only): the hottest remote rows of `shard` (NEXT-2)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    n = rp.shape[0] - 1
+    out = np.zeros(max(min(capacity, n), 1), dtype=np.int32)
+    cnt = C.c_int64()
+    L = lib()
+    L.gnn_cache_plan_by_degree.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int64, C.c_void_p,
+                                           C.c_void_p]
+    L.gnn_cache_plan_by_degree.restype = C.c_int32
+    _check(L.gnn_cache_plan_by_degree(_ptr(rp), n, nshards, shard, min(capacity, n), _ptr(out), C.byref(cnt)))
+    return out[:cnt.value].copy()
 
 
 def shard_rows(num_nodes: int, nshards: int, shard: int):

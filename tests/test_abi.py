@@ -56,3 +56,20 @@ def test_oracle_not_linked_into_product():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_cache_plan_by_degree_matches_definition():
+    """gnn_cache_plan_by_degree (host only, NEXT-2) == its definition written with numpy: the
+    `capacity` highest-degree rows outside this shard's block, ties by id, ascending."""
+    import numpy as np
+    from paper_2403_17092_b200 import cache_plan_by_degree
+    rng = np.random.default_rng(8)
+    for n, P, cap in ((50, 2, 10), (97, 4, 30), (10, 3, 100), (64, 8, 0)):
+        deg = rng.integers(0, 6, size=n)
+        rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+        for shard in range(P):
+            rps = -(-n // P)
+            b, e = min(n, shard * rps), min(n, shard * rps + rps)
+            remote = [v for v in range(n) if not (b <= v < e)]
+            want = sorted(sorted(remote, key=lambda v: (-deg[v], v))[:cap])
+            assert list(cache_plan_by_degree(rp, P, shard, cap)) == want

@@ -20,7 +20,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, q, cache=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -46,13 +46,27 @@ def _worker(rank, world, port, name, q):
         g.import_handles(handles)
         dist.barrier()
         perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
-        errs = []
+        errs, plain = [], []
         for gidx in (rank, rank + 2):
             seeds = OS.batch_seeds(perm, w.batch_size, gidx)
             m.set_params(inp["params"])
             loss = m.train_batch_host(seeds, len(seeds), 0, gidx)
             out = check_train_step(m, w, graph, inp["params"].astype(np.float64), 0, gidx, perm, loss)
             errs.append(out["errors"])
+            plain.append((loss, m.grads()))
+        if cache:
+            # NEXT-2: replicate the hottest quarter of the remote rows; the replica is an exact
+            # copy, so every step must be bit-identical to the uncached one
+            from paper_2403_17092_b200 import cache_plan_by_degree
+            ids = cache_plan_by_degree(inp["row_ptr"], world, rank, w.num_nodes // 4)
+            assert len(ids) and ((ids < b) | (ids >= e)).all()
+            g.cache_rows(ids)
+            for k, gidx in enumerate((rank, rank + 2)):
+                seeds = OS.batch_seeds(perm, w.batch_size, gidx)
+                m.set_params(inp["params"])
+                loss = m.train_batch_host(seeds, len(seeds), 0, gidx)
+                assert loss == plain[k][0] and np.array_equal(m.grads(), plain[k][1]), "cache changed the result"
+            g.cache_rows(None)
         dist.barrier()                 # peers keep their blocks mapped until everyone is done
         m.close()
         g.close()
@@ -63,12 +77,14 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["tiny", "reddit", "papers_small"])
-def test_sharded_feature_gather_matches_oracle(name):
+@pytest.mark.parametrize("name,cache", [("tiny", False), ("reddit", False), ("papers_small", False),
+                                        ("tiny", True), ("papers_small", True)])
+def test_sharded_feature_gather_matches_oracle(name, cache):
+    """cache=True adds the NEXT-2 feature cache of hot remote rows (bit-identical results)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q, cache)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=900) for _ in procs)
