@@ -38,6 +38,9 @@ def parse():
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--no-overlap", action="store_true", help="sample each step before training it")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--balance", action="store_true",
+                   help="N>1: workload-balanced batch->rank schedule (NEXT-3; estimated once before warm-up)")
+    p.add_argument("--optimizer", default="sgd", choices=["sgd", "adam"])
     return p.parse_args()
 
 
@@ -234,7 +237,8 @@ def main():
     g = Graph(inp["row_ptr"], inp["col"], inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim, device=local)
     m = Model(g, model=w.model, sampler=w.sampler, num_layers=w.num_layers, hidden=w.hidden,
               batch_size=w.batch_size, fanouts=w.fanouts, precision=args.precision,
-              use_graph=not args.no_graph, lr=w.lr, seed=w.sampler_seed, init_seed=w.init_seed)
+              use_graph=not args.no_graph, lr=w.lr, seed=w.sampler_seed, init_seed=w.init_seed,
+              optimizer=args.optimizer)
     m.set_train_nodes(inp["train"])
     m.set_params(inp["params"])
     m.set_overlap(not args.no_overlap)
@@ -247,6 +251,20 @@ def main():
     torch.cuda.set_stream(stream)
     m.set_stream(stream)
     steps_per_epoch = (w.n_batches + world - 1) // world
+    # batch of (step, rank): the engine's rule g = s*world + r, or the balanced schedule (NEXT-3:
+    # workloads estimated by a sampler pass over epoch 0, a one-time pre-processing cost)
+    order = list(range(w.n_batches))
+    if args.balance and world > 1:
+        from paper_2403_17092_b200 import plan_balanced
+        order = [int(x) for x in plan_balanced(m.estimate_workload(0), world)]
+        m.set_schedule(order)
+
+    def batch_of(s, p):
+        i = s * world + p
+        return order[i] if i < w.n_batches else None
+
+    def seeds_of(gb):
+        return min(w.batch_size, w.n_train - gb * w.batch_size)
 
     def step_at(i):
         return divmod(i, steps_per_epoch)    # (epoch, step)
@@ -297,9 +315,10 @@ def main():
     batches = []
     for i in range(base, base + args.steps):
         e, s = step_at(i % steps_per_epoch)
-        gidx = s * world + rank
-        sd = perm0[gidx * w.batch_size: (gidx + 1) * w.batch_size] if gidx < w.n_batches else perm0[:0]
-        bt = int(max(0, min(w.n_train - s * world * w.batch_size, world * w.batch_size)))
+        gb = batch_of(s, rank)
+        gidx = gb if gb is not None else s * world + rank
+        sd = perm0[gidx * w.batch_size: (gidx + 1) * w.batch_size] if gb is not None else perm0[:0]
+        bt = int(sum(seeds_of(batch_of(s, p)) for p in range(world) if batch_of(s, p) is not None))
         batches.append((np.ascontiguousarray(sd, dtype=np.int32), bt, gidx))
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -348,8 +367,8 @@ def main():
     sizes = []
     for i in range(args.warmup, args.warmup + args.steps):
         e, s = step_at(i)
-        if s * world + rank < w.n_batches:
-            sizes.append(m.sample_sizes(e, s * world + rank))
+        if batch_of(s, rank) is not None:
+            sizes.append(m.sample_sizes(e, batch_of(s, rank)))
     barrier()
     tot_ms = sum(v[0] for v in prof.values())
     hbm, bf16, bf16_sus, peak_kind = load_peaks()
@@ -406,7 +425,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if args.precision == "fp32" else "bf16-gemm/f32",
             "data": "synthetic (gnn_inputs: power-law Chung-Lu CSR, hashed features/labels)",
-            "config": config_dict(w, world),
+            "config": dict(config_dict(w, world), optimizer=args.optimizer,
+                           schedule="balanced (NEXT-3)" if (args.balance and world > 1) else "g = step*world + rank"),
             "epoch_time_s": w.n_batches / value,
             "e2e": {"value": e2e_value, "unit": "mini-batches/s", "h2d_bytes_per_step": h2d // len(batches),
                     "d2h_bytes_per_step": 4,
