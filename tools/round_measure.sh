@@ -23,3 +23,4 @@ ncu --nvtx --nvtx-include "steps/" --set full --import-source on --clock-control
 python tools/phase_times.py products > "$out/phases_products.txt" 2>&1
 python tools/phase_times.py products_shadow > "$out/phases_products_shadow.txt" 2>&1
 python tools/gather_ceiling.py > "$out/gather_ceiling.txt" 2>&1
+python bench.py --optimizer adam --no-cpu-baseline > "$out/bench_products_adam.json" 2> "$out/bench_products_adam.err"
