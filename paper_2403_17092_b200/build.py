@@ -38,15 +38,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """out/defines: an experiment variant (extra -D flags) built to another path."""
+    if out is None and not force and not _stale():
         return LIB
     nccl_inc, nccl_lib = _nccl_dirs()
-    objdir = os.path.join(HERE, "build")
+    target = out or LIB
+    objdir = os.path.join(HERE, "build") if out is None else out + ".objs"
     os.makedirs(objdir, exist_ok=True)
     common = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", nccl_inc, "-I", os.path.join(os.path.dirname(HERE), "include"),
-              "-Xptxas", "-v" if verbose else "-O3"]
+              "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines]]
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
@@ -59,14 +61,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=8) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = target + f".{os.getpid()}.tmp"
     r = subprocess.run(["nvcc", *ARCH, "-shared", "-o", tmp, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
                         "-Xlinker", "-rpath=" + nccl_lib, "-lcudart"], capture_output=True, text=True)
     if r.returncode:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--out PATH -DNAME=VAL ...]  (variants for A/B experiments)
+    a = sys.argv[1:]
+    o = a[a.index("--out") + 1] if "--out" in a else None
+    print(build(force="--force" in a, verbose="-v" in a, out=o, defines=[x[2:] for x in a if x.startswith("-D")]))

@@ -6,6 +6,10 @@
 
 #include "kernels.h"
 
+#ifndef GS_AGGU1
+#define GS_AGGU1 4   // neighbour rows in flight per warp for rows of <= 128 floats (k_agg_sage)
+#endif
+
 namespace gs {
 namespace {
 constexpr unsigned kFull = 0xffffffffu;
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ ro
             int q = 0;
             // kAggU neighbour rows in flight per warp (memory-level parallelism of the gather);
             // the adds stay in CSR order
-            constexpr int kAggU = CPL <= 2 ? 4 : 2;
+            constexpr int kAggU = CPL == 1 ? GS_AGGU1 : CPL <= 2 ? 4 : 2;
             for (; q + kAggU <= m; q += kAggU) {
                 float4 v[kAggU][CPL];
 #pragma unroll
@@ -582,10 +586,13 @@ __global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
     pdl_wait();
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    int64_t base = 0;   // the layers' entries form one index space: one pass of the grid in all
     for (int l = 0; l < P.n; ++l) {
         const PackLayer& L = P.l[l];
         const int64_t total = (int64_t)L.rows * L.out;
-        for (int64_t f = tid; f < total; f += nth) {
+        const int64_t g0 = base > tid ? tid + ((base - tid + nth - 1) / nth) * nth : tid;
+        base += total;
+        for (int64_t f = g0 - (base - total); f < total; f += nth) {
             const int r = (int)(f / L.out), c = (int)(f % L.out);
             const int rp = P.sage ? (r / L.in) * L.in_pad + (r % L.in) : r;
             const float* src = L.part + (int64_t)rp * L.n_pad + c;
@@ -625,10 +632,13 @@ __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restr
         step = (float)((double)lr / bc1);
         inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
     }
+    int64_t base = 0;   // the layers' entries form one index space: one pass of the grid in all
     for (int l = 0; l < P.n; ++l) {
         const PackLayer& L = P.l[l];
         const int64_t total = (int64_t)L.k_pad * L.n_pad;
-        for (int64_t f = tid; f < total; f += nth) {
+        const int64_t g0 = base > tid ? tid + ((base - tid + nth - 1) / nth) * nth : tid;
+        base += total;
+        for (int64_t f = g0 - (base - total); f < total; f += nth) {
             const int rp = (int)(f / L.n_pad), c = (int)(f % L.n_pad);
             int r = -1;
             if (P.sage) { const int half = rp / L.in_pad, j = rp % L.in_pad; if (j < L.in && half < 2) r = half * L.in + j; }

@@ -54,7 +54,8 @@ def lib():
     """Load the in-tree library (building it with nvcc if it is missing or stale)."""
     global _lib
     if _lib is None:
-        path = _build.build()
+        # GS_LIB: an A/B experiment variant built by build.py --out (never the default)
+        path = os.environ.get("GS_LIB") or _build.build()
         _lib = C.CDLL(path)
         P, I32, I64 = C.c_void_p, C.c_int32, C.c_int64
         sig = {
