@@ -159,7 +159,7 @@ struct GemmArgs {
     const int32_t* nodes;
     Split dz;               // dZ planes [rows x ldc]
     int classes;
-    int diag;               // profiling diagnostics only (env GS_GEMM_DIAG): 1 skip C stores, 2 skip MMAs, 4 skip loads
+    int diag;               // profiling diagnostics only (env GS_GEMM_DIAG): 1 skip C stores, 2 skip MMAs, 4 skip loads, 8 skip the CE epilogue, 16 skip the loss sum
 };
 
 struct TileInfo { int tm, tn, z, kb0, nkb; };
@@ -186,6 +186,58 @@ __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t, int M) {
         ti.nkb = min(nkb_all, ti.kb0 + per) - ti.kb0;
     }
     return ti;
+}
+
+// Softmax cross-entropy of one logits row held by this thread (zr: fp32 bits, columns >= C
+// ignored) (R15): l = max + log sum exp(z - max) - z_y;  dZ = (softmax - onehot) /
+// b_total as split planes; rows in [M, round64(M)) get zero dZ (the wgrad reduction pads to 64).
+template <int BN>
+__device__ __forceinline__ void ce_rows(const GemmArgs& args, uint32_t (&zr)[(BN + 31) / 32][32], int row, int M) {
+    constexpr int kZ = (BN + 31) / 32 * 32;
+    const int C = args.classes;
+    const float inv_bt = 1.0f / (float)max(args.st->b_total, 1);
+    if (row < M) {
+        const int y = args.labels[args.nodes[row]];
+        float mx = -INFINITY, zy = 0.f;
+#pragma unroll
+        for (int c = 0; c < kZ; ++c) {
+            const float z = __uint_as_float(zr[c >> 5][c & 31]);
+            if (c < C) mx = fmaxf(mx, z);
+            if (c == y) zy = z;
+        }
+        float s = 0.f;
+#pragma unroll
+        for (int c = 0; c < kZ; ++c) {   // e_c = exp(z_c - max) kept in place
+            const float e = c < C ? expf(__uint_as_float(zr[c >> 5][c & 31]) - mx) : 0.f;
+            zr[c >> 5][c & 31] = __float_as_uint(e);
+            s += e;
+        }
+        const float inv_s = 1.0f / s;
+#pragma unroll
+        for (int c = 0; c < BN; c += 8) {   // dZ = (e/s - onehot)/b_total, 16-byte stores
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int c0 = c + 2 * q, c1 = c0 + 1;
+                const float d0 = c0 < C ? (__uint_as_float(zr[c0 >> 5][c0 & 31]) * inv_s - (c0 == y ? 1.f : 0.f)) * inv_bt : 0.f;
+                const float d1 = c1 < C ? (__uint_as_float(zr[c1 >> 5][c1 & 31]) * inv_s - (c1 == y ? 1.f : 0.f)) * inv_bt : 0.f;
+                const __nv_bfloat162 hi = __floats2bfloat162_rn(d0, d1);
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(d0 - __low2float(hi), d1 - __high2float(hi));
+                hw[q] = *reinterpret_cast<const uint32_t*>(&hi);
+                lw[q] = *reinterpret_cast<const uint32_t*>(&lo);
+            }
+            *reinterpret_cast<uint4*>(args.dz.hi + tix(args.dz, row, c)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + tix(args.dz, row, c)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+        args.st->row_loss[row] = (mx + logf(s)) - zy;
+        __threadfence();
+    } else if (row < ((M + 63) & ~63)) {      // zero tail rows of the dZ planes
+#pragma unroll
+        for (int c = 0; c < BN; c += 8) {
+            *reinterpret_cast<uint4*>(args.dz.hi + tix(args.dz, row, c)) = make_uint4(0u, 0u, 0u, 0u);
+            if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + tix(args.dz, row, c)) = make_uint4(0u, 0u, 0u, 0u);
+        }
+    }
 }
 
 // MODE 0 = dgrad (A, B K-major), MODE 1 = wgrad (A, B MN-major, split z), MODE 2 = fwd (A K-major,
@@ -234,12 +286,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     const int M = *args.m_ptr;
     const int ntiles = MODE != 1 ? ((M + kBM - 1) / kBM) * args.n_tiles
                                  : ((args.m_static + kBM - 1) / kBM) * args.n_tiles * args.splits;
+    const int t_first = (int)blockIdx.x, t_step = (int)gridDim.x;
 
     if (warp == 0) {
         // ================= TMA producer
         if (lane == 0) {
             int it = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int t = t_first; t < ntiles; t += t_step) {
                 const TileInfo ti = tile_info<MODE>(args, t, M);
                 const int tile_m = ti.tm * kBM, tile_n = ti.tn * BN;
                 for (int kb = 0; kb < ti.nkb; ++kb, ++it) {
@@ -291,7 +344,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
             // reduction extent: operands are zero past it, so the k16 steps beyond it are skipped
             const int klen = MODE == 1 ? M : args.k_len;
             int it = 0, j = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int t = t_first; t < ntiles; t += t_step) {
                 const TileInfo ti = tile_info<MODE>(args, t, M);
                 if (ti.nkb == 0) continue;
                 const int acc = j & 1;
@@ -386,7 +439,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                     bulk_commit();
                 }
             }
-            if (MODE == 3 && has) {
+            if (MODE == 3 && has && !(args.diag & 8)) {
                 // softmax cross-entropy of this thread's row (R15):
                 // l = max + log sum exp(z - max) - z_y;  dZ = (softmax - onehot) / b_total
                 constexpr int kZ = (BN + 31) / 32 * 32;
@@ -395,51 +448,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                 for (int c0 = 0; c0 < kZ; c0 += 32)
                     tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::kAccCols + c0), zr[c0 / 32]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int row = row0 + lane;
-                const int C = args.classes;
-                const float inv_bt = 1.0f / (float)max(args.st->b_total, 1);
-                if (row < M) {
-                    const int y = args.labels[args.nodes[row]];
-                    float mx = -INFINITY, zy = 0.f;
-#pragma unroll
-                    for (int c = 0; c < kZ; ++c) {
-                        const float z = __uint_as_float(zr[c >> 5][c & 31]);
-                        if (c < C) mx = fmaxf(mx, z);
-                        if (c == y) zy = z;
-                    }
-                    float s = 0.f;
-#pragma unroll
-                    for (int c = 0; c < kZ; ++c) {   // e_c = exp(z_c - max) kept in place
-                        const float e = c < C ? expf(__uint_as_float(zr[c >> 5][c & 31]) - mx) : 0.f;
-                        zr[c >> 5][c & 31] = __float_as_uint(e);
-                        s += e;
-                    }
-                    const float inv_s = 1.0f / s;
-#pragma unroll
-                    for (int c = 0; c < BN; c += 8) {   // dZ = (e/s - onehot)/b_total, 16-byte stores
-                        uint32_t hw[4], lw[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int c0 = c + 2 * q, c1 = c0 + 1;
-                            const float d0 = c0 < C ? (__uint_as_float(zr[c0 >> 5][c0 & 31]) * inv_s - (c0 == y ? 1.f : 0.f)) * inv_bt : 0.f;
-                            const float d1 = c1 < C ? (__uint_as_float(zr[c1 >> 5][c1 & 31]) * inv_s - (c1 == y ? 1.f : 0.f)) * inv_bt : 0.f;
-                            const __nv_bfloat162 hi = __floats2bfloat162_rn(d0, d1);
-                            const __nv_bfloat162 lo = __floats2bfloat162_rn(d0 - __low2float(hi), d1 - __high2float(hi));
-                            hw[q] = *reinterpret_cast<const uint32_t*>(&hi);
-                            lw[q] = *reinterpret_cast<const uint32_t*>(&lo);
-                        }
-                        *reinterpret_cast<uint4*>(args.dz.hi + tix(args.dz, row, c)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                        if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + tix(args.dz, row, c)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-                    }
-                    args.st->row_loss[row] = (mx + logf(s)) - zy;
-                    __threadfence();
-                } else if (row < ((M + 63) & ~63)) {      // zero tail rows of the dZ planes
-#pragma unroll
-                    for (int c = 0; c < BN; c += 8) {
-                        *reinterpret_cast<uint4*>(args.dz.hi + tix(args.dz, row, c)) = make_uint4(0u, 0u, 0u, 0u);
-                        if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + tix(args.dz, row, c)) = make_uint4(0u, 0u, 0u, 0u);
-                    }
-                }
+                ce_rows<BN>(args, zr, row0 + lane, M);
             }
             if (has) {
                 tc_fence_before();
@@ -456,7 +465,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
     }
-    if (MODE == 3) {
+    if (MODE == 3 && !(args.diag & 16)) {
         // the last CTA to finish sums the row losses in row order (deterministic)
         if (threadIdx.x == 0) ce_last = atomicAdd(&args.st->ce_done, 1u) == gridDim.x - 1;
         __syncthreads();
@@ -640,6 +649,7 @@ cudaError_t launch_gemm_tc_ce(bool bf16x3, const TcGemmMaps& maps, const int32_t
     a.nodes = nodes;
     a.dz = dz;
     a.classes = classes;
+    a.diag = gemm_diag();
     const int grid = std::max(1, std::min(kSMs, a.m_tiles_cap));
     return bf16x3 ? dispatch_ce<3>(n_pad, grid, maps, a, s) : dispatch_ce<1>(n_pad, grid, maps, a, s);
 }
