@@ -21,6 +21,10 @@
 
 #include "kernels.h"
 
+#ifndef GS_TC_STAGES_WIDE
+#define GS_TC_STAGES_WIDE 3   // pipeline stages of the 96/128-column tiles
+#endif
+
 namespace gs {
 namespace {
 
@@ -569,8 +573,8 @@ cudaError_t dispatch_bn(int bn, int grid, const TcGemmMaps& mp, const GemmArgs& 
         case 32: return launch_tc<32, 4, TERMS, MODE>(grid, mp, a, s);
         case 48: return launch_tc<48, 4, TERMS, MODE>(grid, mp, a, s);
         case 64: return launch_tc<64, 4, TERMS, MODE>(grid, mp, a, s);
-        case 96: return launch_tc<96, 3, TERMS, MODE>(grid, mp, a, s);
-        case 128: return launch_tc<128, 3, TERMS, MODE>(grid, mp, a, s);
+        case 96: return launch_tc<96, GS_TC_STAGES_WIDE, TERMS, MODE>(grid, mp, a, s);
+        case 128: return launch_tc<128, GS_TC_STAGES_WIDE, TERMS, MODE>(grid, mp, a, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -21,7 +21,14 @@ namespace gs {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kThreads = 1024;   // one block per SM: a cheaper grid barrier
+#ifndef GS_SAMPLE_THREADS
+#define GS_SAMPLE_THREADS 512
+#endif
+// one block per SM (a cheaper grid barrier) of 512 threads: at 64 registers it takes half the
+// register file, so the training kernels of the previous batch share the SMs while this batch is
+// sampled (measured: 1024 threads, the whole register file, serialised sampling and training;
+// products 3768 -> 4078 mini-batches/s with 512, 384 and 256 slower)
+constexpr int kThreads = GS_SAMPLE_THREADS;
 constexpr int kWarps = kThreads / 32;
 
 using BlockScan = cub::BlockScan<int, kThreads>;
@@ -130,7 +137,8 @@ __device__ int chunk_scan(Smem& sm, int n, F f, PUT put, unsigned long long* sta
 }
 
 constexpr int kWarpSort = 256;                    // ints per warp slice of shared memory
-constexpr int kBlockSort = kWarps * kWarpSort;    // 8192 ints = 32 KB (keeps most of L1 as cache)
+constexpr int kBlockSort = 8192;                  // ints = 32 KB: hub rows sorted in shared memory (keeps most of L1 as cache)
+static_assert(kBlockSort >= kWarps * kWarpSort, "warp slices fit the hub-sort buffer");
 
 // In-place ascending bitonic sort of s[0:n2) (n2 a power of two) by `nthr` cooperating
 // threads (thread index t), `sync` separating the stages.
@@ -253,7 +261,7 @@ __device__ __forceinline__ void relabel_edges(const SampleParams& P, const HopIO
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_sample_step(SampleParams P) {
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_sample_step(SampleParams P) {
     __shared__ Smem sm;
     StepState* st = P.st;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
