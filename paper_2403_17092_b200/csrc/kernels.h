@@ -37,7 +37,10 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 }
 
 // ------------------------------------------------------------------ sampling side (sample.cu, sample_step.cu)
-constexpr int kWarpGrid = 148 * 16;          // blocks of 256 threads for warp-per-item kernels
+#ifndef GS_WARP_GRID_PER_SM
+#define GS_WARP_GRID_PER_SM 16
+#endif
+constexpr int kWarpGrid = 148 * GS_WARP_GRID_PER_SM;   // blocks of 256 threads for warp-per-item kernels
 
 // Epoch permutation keys (Philox tag 1): keys[i] = (w0<<32)|w1 of (train[i], 0, epoch).
 void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t epoch,

@@ -261,7 +261,10 @@ __device__ __forceinline__ void relabel_edges(const SampleParams& P, const HopIO
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_sample_step(SampleParams P) {
+#ifndef GS_SAMPLE_MINB
+#define GS_SAMPLE_MINB 4   // register cap 32 / thread (a 48-byte spill): 16K registers per SM
+#endif
+__global__ void __launch_bounds__(kThreads, GS_SAMPLE_MINB) k_sample_step(SampleParams P) {
     __shared__ Smem sm;
     StepState* st = P.st;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
