@@ -404,8 +404,11 @@ def main():
                   "ms_per_launch": dur * 1e3, "launches_per_step": nl / args.steps,
                   "peak_source": f"{peak_kind} MEASURED_PEAKS.json " + ("bf16_tflops" if r["bound"] == "tensor" else "hbm_gbs")})
         rooflines[kind] = r
-    dominant = max(rooflines, key=lambda k: prof[k][0])
+    # the dominant kernel: the largest time per launch (a class such as gemm_fwd averages launches
+    # of different layers, shapes and template instantiations; the layer-1 gather is one launch)
+    dominant = max(rooflines, key=lambda k: prof[k][0] / prof[k][1])
     roof = dict(rooflines[dominant])
+    roof["dominant_rule"] = "largest time per launch among the kernel classes with a roofline" 
     agg = rooflines.get("agg_l1")
 
     # ---- cpu baseline (oracle on a bounded sample), rank 0 at N=1 only
