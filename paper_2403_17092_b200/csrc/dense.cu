@@ -6,6 +6,9 @@
 
 #include "kernels.h"
 
+#ifndef GS_AGG_MINB
+#define GS_AGG_MINB 1   // k_agg_sage register cap: 65536 / (256 * GS_AGG_MINB)
+#endif
 #ifndef GS_AGGU1
 #define GS_AGGU1 4   // neighbour rows in flight per warp for rows of <= 128 floats (k_agg_sage)
 #endif
@@ -60,7 +63,7 @@ constexpr float4 kZero4 = {0.f, 0.f, 0.f, 0.f};
 // Neighbour indices are fetched 32 at a time by the warp and broadcast with shuffles; the
 // sum runs in CSR row order with plain fp32 adds, then a true division by the degree.
 template <int CPL>
-__global__ void __launch_bounds__(256) k_agg_sage(const int32_t* __restrict__ rows_ptr,
+__global__ void __launch_bounds__(256, GS_AGG_MINB) k_agg_sage(const int32_t* __restrict__ rows_ptr,
         FeatRows H, int in_pad, const int32_t* __restrict__ gmap,
         const int32_t* __restrict__ smap, const int32_t* __restrict__ rowptr,
         const int32_t* __restrict__ col, Split A, int fixed_k) {
