@@ -6,8 +6,13 @@
 
 #include "kernels.h"
 
-#ifndef GS_AGG_MINB
-#define GS_AGG_MINB 1   // k_agg_sage register cap: 65536 / (256 * GS_AGG_MINB)
+// k_agg_sage register cap (experiments only): GS_AGG_MINB = n -> __launch_bounds__(256, n).  The
+// default (no minimum-blocks hint) compiles to 48 registers and was measured fastest (A/B:
+// minBlocks 1 -> 70 registers, products gather 57 -> 76 us; 4 -> 61.5 us; 6 -> Reddit 100 -> 145 us)
+#ifdef GS_AGG_MINB
+#define GS_AGG_BOUNDS __launch_bounds__(256, GS_AGG_MINB)
+#else
+#define GS_AGG_BOUNDS __launch_bounds__(256)
 #endif
 #ifndef GS_AGGU1
 #define GS_AGGU1 4   // neighbour rows in flight per warp for rows of <= 128 floats (k_agg_sage)
@@ -63,7 +68,7 @@ constexpr float4 kZero4 = {0.f, 0.f, 0.f, 0.f};
 // Neighbour indices are fetched 32 at a time by the warp and broadcast with shuffles; the
 // sum runs in CSR row order with plain fp32 adds, then a true division by the degree.
 template <int CPL>
-__global__ void __launch_bounds__(256, GS_AGG_MINB) k_agg_sage(const int32_t* __restrict__ rows_ptr,
+__global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
         FeatRows H, int in_pad, const int32_t* __restrict__ gmap,
         const int32_t* __restrict__ smap, const int32_t* __restrict__ rowptr,
         const int32_t* __restrict__ col, Split A, int fixed_k) {
