@@ -378,7 +378,12 @@ struct BalArgs {
 };
 
 template <int CPL, int MODE>   // MODE: 0 FWD SAGE, 1 FWD GCN, 2 BWD SAGE, 3 BWD GCN
-__global__ void __launch_bounds__(256) k_agg_bal(BalArgs a) {
+#ifdef GS_BAL_MINB
+#define GS_BAL_BOUNDS __launch_bounds__(256, GS_BAL_MINB)
+#else
+#define GS_BAL_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void GS_BAL_BOUNDS k_agg_bal(BalArgs a) {
     constexpr bool BWD = MODE >= 2, GCN = (MODE & 1) != 0;
     pdl_trigger();
     pdl_wait();
