@@ -134,6 +134,8 @@ struct Layer {
     int64_t rows_alloc = 0;  // operand-plane rows (m_cap rounded to the 128-row GEMM tile)
     Split A{}, dPre{}, Wkn{};   // bf16 split planes (GEMM operands); W as [K_pad x N_pad]
     float *H = nullptr, *dA = nullptr, *wpart = nullptr;
+    uint32_t* hmask = nullptr;   // ReLU decisions of H (bit per element; layers with ReLU)
+    int mask_ld = 0;             // words per hmask row
     TcGemmMaps map_fwd{}, map_dgrad{}, map_wgrad{};
 };
 
@@ -295,7 +297,8 @@ void enqueue_training(gnn_model* m, int set) {
             b.col = B.tdst_s[blk] ? B.tdst_s[blk] : B.col[blk];
             b.orow = B.rowptr[blk];
             b.dA = ly.dA;
-            b.Hprev = m->layers[li - 1].H;
+            b.hmask = m->layers[li - 1].hmask;
+            b.mask_ld = m->layers[li - 1].mask_ld;
             b.out = m->layers[li - 1].dPre;
             b.out_w = ly.in_pad;
         }
@@ -338,7 +341,7 @@ void enqueue_training(gnn_model* m, int set) {
         // Pre = A W (+ReLU) -> H (fp32)
         K(m, s, GNN_K_GEMM_FWD, [&] {
             launch_gemm_tc(2, m->bf16x3, ly.map_fwd, rows, 0, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, ly.n_pad,
-                           ly.n_pad, li < L - 1, 1, 0, s);
+                           ly.n_pad, li < L - 1, 1, 0, s, ly.hmask, ly.mask_ld);
         });
         if (li == L - 1) {   // ---- loss (wide logits rows: separate kernel)
             K(m, s, GNN_K_CE, [&] { launch_ce(B.st, ly.H, ly.n_pad, g->C, g->y, B.nodes, ly.dPre, s); });
@@ -370,7 +373,7 @@ void enqueue_training(gnn_model* m, int set) {
         if (m->shadow) K(m, s, GNN_K_SPMM_BWD, [&] { bal(true, li, rows); });
         else K(m, s, GNN_K_SPMM_BWD, [&] {
             launch_spmm_bwd(!m->sage, blk, B.st, rows, ly.dA, ly.in_pad, B.rowptr[blk], B.trowptr[blk], B.tdst_s[blk],
-                            prev.H, prev.dPre, s);
+                            prev.hmask, prev.mask_ld, prev.dPre, s);
         });
     }
     cudaEventRecord(m->ev_join, ws);
@@ -984,6 +987,11 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         ly.dPre.rows = ly.rows_alloc;
         if ((s = split(ly.Wkn, (int64_t)ly.k_pad * ly.n_pad)) != GNN_OK) return cleanup(s);
         AL(ly.H, ly.m_cap * ly.n_pad);
+        if (li < m->L - 1) {   // the ReLU layers' sign masks (read by the backward aggregation)
+            ly.mask_ld = (ly.n_pad + 31) / 32;
+            AL(ly.hmask, ly.m_cap * ly.mask_ld);
+            CK(cudaMemset(ly.hmask, 0, sizeof(uint32_t) * ly.m_cap * ly.mask_ld));
+        }
         if (li > 0) AL(ly.dA, ly.m_cap * ly.k_pad);
         AL(ly.wpart, (int64_t)ly.splits * ly.k_pad * ly.n_pad);
         // TMA descriptors (128B swizzle) of this layer's three GEMMs

@@ -224,7 +224,7 @@ template <int CPL, bool GCN>
 __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __restrict__ st,
         const int32_t* __restrict__ dlim_ptr, const float* __restrict__ dA, int in_pad,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ trowptr,
-        const int32_t* __restrict__ tdst, const float* __restrict__ Hprev, Split dPre) {
+        const int32_t* __restrict__ tdst, const uint32_t* __restrict__ hmask, int mask_ld, Split dPre) {
     pdl_trigger();
     pdl_wait();
     const int nsrc = st->n_src[h];
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
     if (u < nsrc) {
         cb = trowptr[u];
         ce = trowptr[u + 1];
-        prefetch_rows_l2(Hprev + (int64_t)u * in_pad, u < dlim ? dA + (int64_t)u * lda : nullptr, in_pad, lane);
+        if (u < dlim) prefetch_rows_l2(dA + (int64_t)u * lda, nullptr, in_pad, lane);
     }
     if (lane < ce - cb) ci = tdst[cb + lane];
     for (; u < nr; u += W) {
@@ -253,10 +253,9 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
         const int un = u + W;
         int nb = 0, ne = 0;
         if (un < nsrc) { nb = trowptr[un]; ne = trowptr[un + 1]; }
-        // the next row's H_prev and dA-self rows go to L2 now (they are read at the end of
-        // that row: no registers held across its edge loop)
-        if (un < nsrc) prefetch_rows_l2(Hprev + (int64_t)un * in_pad, un < dlim ? dA + (int64_t)un * lda : nullptr,
-                                        in_pad, lane);
+        // the next row's dA-self row goes to L2 now (it is read at the end of that row: no
+        // registers held across its edge loop)
+        if (un < dlim) prefetch_rows_l2(dA + (int64_t)un * lda, nullptr, in_pad, lane);
         const float dout = (float)(ce - cb + (u < ndst ? 1 : 0));
         float4 acc[CPL];
 #pragma unroll
@@ -316,13 +315,14 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
             const float din = (float)(rowptr[u + 1] - rowptr[u] + 1);
             wself = 1.0f / sqrtf(din * dout);
         }
-        const float4* hp = reinterpret_cast<const float4*>(Hprev + (int64_t)u * in_pad);
+        const uint32_t* mp = hmask + (int64_t)u * mask_ld;
         const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
-        float4 hv[CPL], sv[CPL];
+        uint32_t hv[CPL];
+        float4 sv[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
-            hv[c] = ch < nch ? __ldg(hp + ch) : kZero4;
+            hv[c] = ch < nch ? __ldg(mp + (ch >> 3)) >> ((4 * ch) & 31) : 0u;
             sv[c] = (ch < nch && u < dlim) ? __ldg(sp + ch) : kZero4;
         }
 #pragma unroll
@@ -331,9 +331,9 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
             if (ch < nch) {
                 float4 a = acc[c];
                 if (u < dlim) a = GCN ? f4fma(wself, sv[c], a) : f4add(a, sv[c]);
-                // ReLU'(pre) = [H > 0]  (ReLU'(0) = 0)
-                a.x = hv[c].x > 0.f ? a.x : 0.f; a.y = hv[c].y > 0.f ? a.y : 0.f;
-                a.z = hv[c].z > 0.f ? a.z : 0.f; a.w = hv[c].w > 0.f ? a.w : 0.f;
+                // ReLU'(pre) = [H > 0]  (ReLU'(0) = 0): the forward GEMM's sign bits
+                a.x = (hv[c] & 1u) ? a.x : 0.f; a.y = (hv[c] & 2u) ? a.y : 0.f;
+                a.z = (hv[c] & 4u) ? a.z : 0.f; a.w = (hv[c] & 8u) ? a.w : 0.f;
                 store_split4(dPre, tix(dPre, u, 4 * ch), a);
             }
         }
@@ -369,7 +369,8 @@ struct BalArgs {
     FeatRows H;                // FWD input rows
     const int32_t* gmap;       // FWD: row id of local node c in H (layer 1: global ids)
     const float* dA;           // BWD
-    const float* Hprev;        // BWD: ReLU mask rows
+    const uint32_t* hmask;     // BWD: ReLU decisions of the previous layer (bit per element)
+    int mask_ld;
     int in_pad;
     Split out;                 // FWD: A (SAGE [self | mean], GCN Â H); BWD: dPre
     int out_w;                 // columns of `out` (zero tail rows)
@@ -378,12 +379,7 @@ struct BalArgs {
 };
 
 template <int CPL, int MODE>   // MODE: 0 FWD SAGE, 1 FWD GCN, 2 BWD SAGE, 3 BWD GCN
-#ifdef GS_BAL_MINB
-#define GS_BAL_BOUNDS __launch_bounds__(256, GS_BAL_MINB)
-#else
-#define GS_BAL_BOUNDS __launch_bounds__(256)
-#endif
-__global__ void GS_BAL_BOUNDS k_agg_bal(BalArgs a) {
+__device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
     constexpr bool BWD = MODE >= 2, GCN = (MODE & 1) != 0;
     pdl_trigger();
     pdl_wait();
@@ -436,7 +432,7 @@ __global__ void GS_BAL_BOUNDS k_agg_bal(BalArgs a) {
                 const float dout = (float)(re - rb + (r < ndst ? 1 : 0));
                 wself = 1.0f / sqrtf(din * dout);
             }
-            const float4* hp = reinterpret_cast<const float4*>(a.Hprev + (int64_t)r * a.in_pad);
+            const uint32_t* mp = a.hmask + (int64_t)r * a.mask_ld;
             const float4* sp = reinterpret_cast<const float4*>(a.dA + (int64_t)r * ldd);
             if (!any && !self_on) {   // no gradient reaches row r: dPre = 0 (no reads)
                 for (int ch = lane; ch < nch; ch += 32) store_split4(a.out, tix(a.out, r, 4 * ch), kZero4);
@@ -448,9 +444,9 @@ __global__ void GS_BAL_BOUNDS k_agg_bal(BalArgs a) {
                 if (ch < nch) {
                     float4 v = acc[c];
                     if (self_on) v = GCN ? f4fma(wself, __ldg(sp + ch), v) : f4add(v, __ldg(sp + ch));
-                    const float4 h = __ldg(hp + ch);
-                    v.x = h.x > 0.f ? v.x : 0.f; v.y = h.y > 0.f ? v.y : 0.f;
-                    v.z = h.z > 0.f ? v.z : 0.f; v.w = h.w > 0.f ? v.w : 0.f;
+                    const uint32_t h = __ldg(mp + (ch >> 3)) >> ((4 * ch) & 31);   // ReLU decisions
+                    v.x = (h & 1u) ? v.x : 0.f; v.y = (h & 2u) ? v.y : 0.f;
+                    v.z = (h & 4u) ? v.z : 0.f; v.w = (h & 8u) ? v.w : 0.f;
                     store_split4(a.out, tix(a.out, r, 4 * ch), v);
                 }
             }
@@ -575,6 +571,14 @@ __global__ void GS_BAL_BOUNDS k_agg_bal(BalArgs a) {
         }
     }
 }
+
+// Forward and backward instantiations differ in register demand: the backward ones are capped
+// at 3 blocks/SM (<= 85 registers; uncapped the GCN backward compiles to 101, 2 blocks/SM),
+// the forward ones keep the compiler's choice (a cap measured slower).
+template <int CPL, int MODE>
+__global__ void __launch_bounds__(256) k_agg_bal(BalArgs a) { agg_bal_body<CPL, MODE>(a); }
+template <int CPL, int MODE>
+__global__ void __launch_bounds__(256, 3) k_agg_bal_bwd(BalArgs a) { agg_bal_body<CPL, MODE>(a); }
 
 // mask[r] = tag for the rows the last layer reads: the seeds r < *nseed_ptr and their
 // in-neighbours in the block (ShaDow receptive field of the last layer, R19).
@@ -787,31 +791,35 @@ void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H
 template <bool GCN>
 static void spmm_bwd(int h, const StepState* st, const int32_t* dlim, const float* dA, int in_pad,
                      const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
-                     const float* H_prev, Split dPre_prev, cudaStream_t s) {
+                     const uint32_t* hmask, int mask_ld, Split dPre_prev, cudaStream_t s) {
     switch (cpl_of(in_pad)) {
-        case 1: launch_pdl(k_spmm_bwd<1, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
-        case 2: launch_pdl(k_spmm_bwd<2, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
-        case 3: launch_pdl(k_spmm_bwd<3, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
-        default: launch_pdl(k_spmm_bwd<4, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev); break;
+        case 1: launch_pdl(k_spmm_bwd<1, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, hmask, mask_ld, dPre_prev); break;
+        case 2: launch_pdl(k_spmm_bwd<2, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, hmask, mask_ld, dPre_prev); break;
+        case 3: launch_pdl(k_spmm_bwd<3, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, hmask, mask_ld, dPre_prev); break;
+        default: launch_pdl(k_spmm_bwd<4, GCN>, kWarpGrid, 256, 0, s, h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, hmask, mask_ld, dPre_prev); break;
     }
 }
 
 void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, const float* dA,
                      int in_pad, const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
-                     const float* H_prev, Split dPre_prev, cudaStream_t s) {
-    if (gcn) spmm_bwd<true>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
-    else spmm_bwd<false>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, H_prev, dPre_prev, s);
+                     const uint32_t* hmask, int mask_ld, Split dPre_prev, cudaStream_t s) {
+    if (gcn) spmm_bwd<true>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, hmask, mask_ld, dPre_prev, s);
+    else spmm_bwd<false>(h, st, dlim, dA, in_pad, blk_rowptr, trowptr, tdst, hmask, mask_ld, dPre_prev, s);
 }
 
 int bal_units_cap() { return kBalUnits; }
 
 void launch_agg_bal(const BalLaunch& b, cudaStream_t s) {
     BalArgs a{b.n_ptr, b.ndst_ptr, b.dlim_ptr, b.rowptr, b.col, b.orow, b.rmask, b.tag_ptr, b.H, b.gmap,
-              b.dA, b.Hprev, b.in_pad, b.out, b.out_w, b.part, b.cnt};
+              b.dA, b.hmask, b.mask_ld, b.in_pad, b.out, b.out_w, b.part, b.cnt};
     const int mode = (b.bwd ? 2 : 0) + (b.gcn ? 1 : 0);
     const int cpl = cpl_of(b.in_pad);
     const int c = cpl <= 1 ? 1 : cpl <= 2 ? 2 : cpl <= 4 ? 4 : 8;
-#define GS_BAL(C, M) if (c == C && mode == M) { launch_pdl(k_agg_bal<C, M>, kWarpGrid, 256, 0, s, a); return; }
+#define GS_BAL(C, M) if (c == C && mode == M) {                                                  \
+        if constexpr (M >= 2) launch_pdl(k_agg_bal_bwd<C, M>, kWarpGrid, 256, 0, s, a);            \
+        else launch_pdl(k_agg_bal<C, M>, kWarpGrid, 256, 0, s, a);                                 \
+        return;                                                                                   \
+    }
     GS_BAL(1, 0) GS_BAL(1, 1) GS_BAL(1, 2) GS_BAL(1, 3)
     GS_BAL(2, 0) GS_BAL(2, 1) GS_BAL(2, 2) GS_BAL(2, 3)
     GS_BAL(4, 0) GS_BAL(4, 1) GS_BAL(4, 2) GS_BAL(4, 3)

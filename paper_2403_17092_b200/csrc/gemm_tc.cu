@@ -163,6 +163,8 @@ struct GemmArgs {
     const int32_t* nodes;
     Split dz;               // dZ planes [rows x ldc]
     int classes;
+    uint32_t* mask;         // MODE 2 with relu: sign bits of the stored H (nullable)
+    int mask_ld;
     int diag;               // profiling diagnostics only (env GS_GEMM_DIAG): 1 skip C stores, 2 skip MMAs, 4 skip loads, 8 skip the CE epilogue, 16 skip the loss sum
 };
 
@@ -426,14 +428,20 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                 for (int hb = 0; hb < 2; ++hb) {
                     if (hb == 1 && !two) break;
                     uint8_t* myrow = ebuf + hb * kEpiBuf + lane * 128;
+                    uint32_t mb = 0u;   // ReLU decisions of these 32 columns (MODE 2)
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
                         float4 f;
                         f.x = __uint_as_float(v[hb][4 * c]); f.y = __uint_as_float(v[hb][4 * c + 1]);
                         f.z = __uint_as_float(v[hb][4 * c + 2]); f.w = __uint_as_float(v[hb][4 * c + 3]);
                         if (args.relu) { f.x = fmaxf(f.x, 0.f); f.y = fmaxf(f.y, 0.f); f.z = fmaxf(f.z, 0.f); f.w = fmaxf(f.w, 0.f); }
+                        if (MODE == 2)
+                            mb |= ((f.x > 0.f ? 1u : 0u) | (f.y > 0.f ? 2u : 0u) | (f.z > 0.f ? 4u : 0u) | (f.w > 0.f ? 8u : 0u))
+                                  << (4 * c);
                         *reinterpret_cast<float4*>(myrow + ((c ^ (lane & 7)) << 4)) = f;
                     }
+                    if (MODE == 2 && args.mask && row0 + lane < M)
+                        args.mask[(size_t)(row0 + lane) * args.mask_ld + ((tile_n + c0) >> 5) + hb] = mb;
                 }
                 fence_async_smem();
                 __syncwarp();
@@ -606,9 +614,11 @@ static int gemm_diag() {
 
 cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_static,
                            int m_cap, int n_pad, int k_pad, float* C, int ldc, int n_store, bool relu, int splits,
-                           int64_t split_stride, cudaStream_t s) {
+                           int64_t split_stride, cudaStream_t s, uint32_t* relu_mask, int mask_ld) {
     const int bn = tc_tile_n(n_pad);
     GemmArgs a{};
+    a.mask = relu ? relu_mask : nullptr;
+    a.mask_ld = mask_ld;
     a.m_ptr = m_ptr;
     a.m_static = m_static;
     a.m_tiles_cap = (m_cap + kBM - 1) / kBM;

@@ -168,7 +168,8 @@ struct BalLaunch {
     FeatRows H;                // fwd input rows
     const int32_t* gmap;       // fwd: H row of local node (self and neighbours), nullable
     const float* dA;           // bwd
-    const float* Hprev;        // bwd
+    const uint32_t* hmask;     // bwd: ReLU decisions of the previous layer (bit per element)
+    int mask_ld;               // bwd: words per mask row
     int in_pad;
     Split out;
     int out_w;
@@ -208,10 +209,11 @@ void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* lab
 // Backward aggregation over the transposed block (atomic-free, fixed order), u < n_src[h]:
 //   SAGE: dPre_prev[u] = ([u<dlim] dA[u,:in_pad] + Σ_{e in T(u), dst<dlim} dA[dst, in_pad:]/deg(dst)) * [H_prev[u]>0]
 //   GCN:  dPre_prev[u] = (Â^T dA)[u] * [H_prev[u] > 0]   (dA rows < dlim)
+// [H_prev > 0] is read from the previous layer's forward-GEMM sign mask (hmask, mask_ld words/row).
 // dPre_prev is written as split planes [n_src x in_pad] (+ zero tail rows).
 void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, const float* dA,
                      int in_pad, const int32_t* blk_rowptr, const int32_t* trowptr, const int32_t* tdst,
-                     const float* H_prev, Split dPre_prev, cudaStream_t s);
+                     const uint32_t* hmask, int mask_ld, Split dPre_prev, cudaStream_t s);
 void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint32_t layer,
                         cudaStream_t s);
 
@@ -235,9 +237,11 @@ int tc_tile_n(int n_pad);
 // mode 1 (wgrad): C_z[m_static x n_pad] = Σ_{m in split z} A[m, :]^T B[m, :], reduction length
 //   *m_ptr split into `splits` ranges of 64-row blocks; A, B MN-major, maps with box rows 64.
 // bf16x3: 3-term split product (fp32 parity); else 1 term (bf16 GEMM variant).
+// relu_mask (mode 2 with relu, optional): bit j of word [r * mask_ld + c / 32] = [H[r, c] > 0],
+// the ReLU decision the backward pass applies (it then reads 1 bit per element instead of H).
 cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_static,
                            int m_cap, int n_pad, int k_pad, float* C, int ldc, int n_store, bool relu, int splits,
-                           int64_t split_stride, cudaStream_t s);
+                           int64_t split_stride, cudaStream_t s, uint32_t* relu_mask = nullptr, int mask_ld = 0);
 
 // Last layer, fused: Z = A W (logits, stored like mode 2) and, in the epilogue, the softmax
 // cross-entropy of every row < *m_ptr (= batch_n): st->row_loss, dZ split planes [rows x n_pad]
