@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define GNN_ABI_VERSION 1
+#define GNN_ABI_VERSION 2
 
 typedef enum {
     GNN_OK = 0,

@@ -16,6 +16,7 @@ GNN_FP32, GNN_BF16_GEMM = 0, 1
 GNN_SRC_IDS, GNN_BLK_ROWPTR, GNN_BLK_COL, GNN_BLK_NBR = 0, 1, 2, 3
 GNN_DBG_LOGITS, GNN_DBG_GRADS, GNN_DBG_LOSS, GNN_DBG_ACT = 0, 1, 2, 16
 GNN_SGD, GNN_ADAM = 0, 1
+ABI_VERSION = 2   # include/gnnstep.h GNN_ABI_VERSION
 KERNEL_IDS = dict(sample=0, relabel=1, agg_l1=2, agg=3, gemm_fwd=4, gemm_dgrad=5, gemm_wgrad=6,
                   spmm_bwd=7, ce=8, sgd=9, transpose=10, induce=11, allreduce=12, scan=13, other=14)
 
@@ -84,6 +85,9 @@ def lib():
             f = getattr(_lib, name)
             f.argtypes = args
             f.restype = res
+        if _lib.gnn_abi_version() != ABI_VERSION:
+            v, _lib = _lib.gnn_abi_version(), None
+            raise RuntimeError(f"libgnnstep ABI {v} != binding ABI {ABI_VERSION} (rebuild)")
     return _lib
 
 

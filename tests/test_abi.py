@@ -30,7 +30,7 @@ def test_library_loads_and_exports_every_symbol():
     L = lib()
     for s in declared_symbols():
         assert hasattr(L, s), s
-    assert L.gnn_abi_version() == 1
+    assert L.gnn_abi_version() == 2   # 2: gnn_model_config gained optimizer, beta1, beta2, eps
     path = L._name
     out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
     for s in declared_symbols():
