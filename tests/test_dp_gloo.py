@@ -134,3 +134,33 @@ def test_dp_gradient_allreduce_equals_union_batch():
         assert s0 == s1 and np.array_equal(g0, g1)            # identical on every rank
         want = oracle.train_step(w, graph, inp["params"], 0, s0, 2)["grad"]
         assert np.allclose(g0, want, rtol=1e-12, atol=1e-15)
+
+
+def _balanced_plan(rank, world):
+    """NEXT-3 host logic on every rank: the same workload vector (in training it comes from the
+    sampler pass, identical on all ranks since keys use the global batch index) gives the same
+    plan everywhere; each rank reads its batch of every step from it."""
+    from paper_2403_17092_b200 import plan_balanced
+    rng = np.random.default_rng(11)
+    work = rng.pareto(1.2, size=157).astype(np.int64) * 100 + 1   # the tiny epoch's 157 batches, skewed
+    order = [int(x) for x in plan_balanced(work, world)]
+    S = (len(order) + world - 1) // world
+    mine = [order[s * world + rank] if s * world + rank < len(order) else None for s in range(S)]
+    allp = [None] * world
+    dist.all_gather_object(allp, (order, mine))
+    return allp
+
+
+def test_balanced_schedule_world2():
+    from oracle import balance
+    out = _run(_balanced_plan)
+    allp = out[0]
+    assert allp == out[1]
+    (order0, mine0), (order1, mine1) = allp
+    assert order0 == order1                                      # every rank holds the same plan
+    seen = [b for pair in zip(mine0, mine1) for b in pair if b is not None]
+    assert sorted(seen) == list(range(157))                      # every batch exactly once
+    rng = np.random.default_rng(11)
+    work = rng.pareto(1.2, size=157).astype(np.int64) * 100 + 1
+    assert order0 == balance.plan(work, 2)                       # the oracle's plan (R31)
+    assert balance.makespan(order0, work, 2) <= balance.makespan(list(range(157)), work, 2)
