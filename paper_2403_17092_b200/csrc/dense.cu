@@ -14,6 +14,9 @@
 #else
 #define GS_AGG_BOUNDS __launch_bounds__(256)
 #endif
+#ifndef GS_AGGU2
+#define GS_AGGU2 4   // the same for rows of 129..256 floats
+#endif
 #ifndef GS_AGGU1
 #define GS_AGGU1 4   // neighbour rows in flight per warp for rows of <= 128 floats (k_agg_sage)
 #endif
@@ -102,7 +105,7 @@ __global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
             int q = 0;
             // kAggU neighbour rows in flight per warp (memory-level parallelism of the gather);
             // the adds stay in CSR order
-            constexpr int kAggU = CPL == 1 ? GS_AGGU1 : CPL <= 2 ? 4 : 2;
+            constexpr int kAggU = CPL == 1 ? GS_AGGU1 : CPL <= 2 ? GS_AGGU2 : 2;
             for (; q + kAggU <= m; q += kAggU) {
                 float4 v[kAggU][CPL];
 #pragma unroll
