@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--balance", action="store_true",
                    help="N>1: workload-balanced batch->rank schedule (NEXT-3; estimated once before warm-up)")
     p.add_argument("--optimizer", default="sgd", choices=["sgd", "adam"])
+    p.add_argument("--epochs", type=int, default=5,
+                   help="whole epochs timed through gnn_train_epoch (after one warm-up epoch); 0 skips")
     return p.parse_args()
 
 
@@ -167,6 +169,23 @@ def oracle_threads():
         return 1
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def time_oracle_threads(w, graph, steps, threads):
+    """The oracle with its BLAS pool limited to `threads` (its C sampler is single-threaded)."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=threads):
+        return time_oracle(w, graph, steps)
+
+
 def time_oracle(w, graph, steps, warmup=0):
     import oracle
     from oracle import sampling as OS
@@ -198,7 +217,7 @@ def run_reference(args, w, inp, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_dict(w, world),
             "cpu_baseline": {"value": v, "unit": "mini-batches/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "host_cores": os.cpu_count(), "sample": sample},
             "e2e": {"value": v, "unit": "mini-batches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "epoch_time_s": w.n_batches / v}
     print(json.dumps(line), flush=True)
@@ -411,26 +430,51 @@ def main():
     roof["dominant_rule"] = "largest time per launch among the kernel classes with a roofline" 
     agg = rooflines.get("agg_l1")
 
+    # ---- whole epochs through gnn_train_epoch (permutation, every step, overlapped sampling):
+    # the paper's metric is epoch time (Table 3).  One warm-up epoch, then
+    # args.epochs timed epochs (device events inside the library, max over ranks).
+    epochs = None
+    if args.epochs > 0:
+        m.train_epoch(1000)
+        secs = []
+        for e in range(args.epochs):
+            st = m.train_epoch(1001 + e)
+            t = st["seconds"]
+            if world > 1:
+                tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            secs.append(t)
+        epochs = {"epochs": args.epochs, "median_s": statistics.median(secs), "min_s": min(secs),
+                  "all_s": secs, "batches_per_epoch": w.n_batches,
+                  "mini_batches_per_s_median": w.n_batches / statistics.median(secs),
+                  "api": "gnn_train_epoch (epoch permutation + every step; CUDA events in the library)"}
+
     # ---- cpu baseline (oracle on a bounded sample), rank 0 at N=1 only
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         graph = oracle_graph(w, inp)
         nb = 2
-        secs = time_oracle(w, graph, nb)
-        cpu = {"value": nb / secs, "unit": "mini-batches/s", "cores": oracle_threads(), "kind": "oracle",
+        secs_all = time_oracle(w, graph, nb)
+        secs_one = time_oracle_threads(w, graph, nb, 1)
+        cpu = {"value": nb / secs_all, "unit": "mini-batches/s", "cores": oracle_threads(), "kind": "oracle",
+               "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+               "single_thread": {"value": nb / secs_one, "cores": 1},
                "sample": f"{nb} mini-batches (g=0,1 of epoch 0) of the same workload, full oracle step "
-                         f"(C sampling + fp64 numpy/scipy forward/backward/SGD)"}
+                         f"(C sampling, single-threaded + fp64 numpy/scipy forward/backward/SGD on `cores` BLAS "
+                         f"threads; single_thread: BLAS limited to 1 thread)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "mini-batches/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if args.precision == "fp32" else "bf16-gemm/f32",
+            "dtype": "f32 (GEMMs: 3-term bf16 split, DESIGN.md R28)" if args.precision == "fp32" else "bf16-gemm/f32",
             "data": "synthetic (gnn_inputs: power-law Chung-Lu CSR, hashed features/labels)",
             "config": dict(config_dict(w, world), optimizer=args.optimizer,
                            schedule="balanced (NEXT-3)" if (args.balance and world > 1) else "g = step*world + rank"),
-            "epoch_time_s": w.n_batches / value,
+            "epoch_time_s": epochs["median_s"] if epochs else w.n_batches / value,
+            "epoch_time": epochs,
             "e2e": {"value": e2e_value, "unit": "mini-batches/s", "h2d_bytes_per_step": h2d // len(batches),
                     "d2h_bytes_per_step": 4,
                     "api": "gnn_train_batch_host (host seeds -> pinned staging -> device, step, loss -> host; synchronous; next batch prefetched)"},

@@ -106,6 +106,15 @@ gnn_status gnn_shard_import(gnn_graph* g, const uint8_t* handles_host);
  * id), ascending in ids_out_host; *n_out_host = their count (a static hot set: a node is
  * sampled about in proportion to its degree). */
 gnn_status gnn_cache_rows(gnn_graph* g, const int32_t* ids_host, int64_t n);
+/* Row-read counters of a sharded graph's layer-1 gathers (evidence that the cache is read, and
+ * the share of remote gathers it removes): counts_out_host[0..2] = row reads served by
+ * {this process's shard, a peer's shard (NVLink), the cache replica} since the last reset, one
+ * count per warp-level row read (an edge's neighbour row or a destination's self row).
+ * Synchronizes the device, then: enable = 1 resets the counters and turns counting on (one
+ * atomic per row read), 0 resets and turns it off, -1 only reads.  counts_out_host may be NULL.
+ * Captured steps see the switch (the descriptor lives at a fixed address).  STATE if the graph
+ * is not sharded. */
+gnn_status gnn_cache_stats(gnn_graph* g, int32_t enable, int64_t* counts_out_host);
 gnn_status gnn_cache_plan_by_degree(const int64_t* row_ptr_host, int64_t num_nodes, int32_t nshards, int32_t shard,
                                     int64_t capacity, int32_t* ids_out_host, int64_t* n_out_host);
 
@@ -146,7 +155,8 @@ gnn_status gnn_set_stream(gnn_model* m, void* stream);
  * ordered by events; §4.1 lines 256-263 overlap sampling with training).  Off:
  * every step samples then trains.  Results are identical either way. */
 gnn_status gnn_set_overlap(gnn_model* m, int32_t enable);
-/* The train split (copied).  ids in [0, N), duplicate-free.  n may be 0. */
+/* The train split (copied).  ids in [0, N), duplicate-free (RANGE / PARAM).  n may be 0.
+ * Drops any schedule set with gnn_set_schedule (it listed the previous split's batches). */
 gnn_status gnn_set_train_nodes(gnn_model* m, const int32_t* ids_host, int64_t n);
 int64_t gnn_param_count(const gnn_model* m);
 int64_t gnn_num_batches(const gnn_model* m);   /* ceil(n_train / batch_size) */
@@ -186,6 +196,16 @@ gnn_status gnn_estimate_workload(gnn_model* m, int64_t epoch, int64_t* work_out_
 gnn_status gnn_plan_balanced(const int64_t* work_host, int64_t n, int32_t world, int64_t* order_out_host);
 gnn_status gnn_set_schedule(gnn_model* m, const int64_t* order_host, int64_t n);
 gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_t id_host[128]);
+/* How a step exchanges its gradient (§2.2, synchronous SGD):
+ *   GNN_EXCH_AUTO (default): world 1 -> the fixed-order reduce of the weight-gradient partials
+ *     fused into the update kernel; world > 1 -> as GNN_EXCH_NCCL.
+ *   GNN_EXCH_NCCL: reduce kernel -> ncclAllReduce(sum, fp32) of the flat gradient -> update
+ *     kernel, all captured in the step's CUDA graph; on world 1 the library builds a one-rank
+ *     communicator (the multi-rank branch, verifiable on one GPU: results are bit-identical to
+ *     AUTO, since a one-rank all-reduce is a copy and both reduce in the same fixed order).
+ * Synchronizes; the next step recaptures.  PARAM for an unknown mode. */
+enum { GNN_EXCH_AUTO = 0, GNN_EXCH_NCCL = 1 };
+gnn_status gnn_set_exchange(gnn_model* m, int32_t mode);
 
 /* The epoch's seed order (§2.2; SPEC.md partition_seeds lines 107-115):
  * train ids sorted by (Philox key64(id, epoch), id) (R7); batch g is
@@ -223,11 +243,14 @@ gnn_status gnn_train_minibatch(gnn_model* m, int64_t epoch, int64_t step, float*
 /* End-to-end call: the seeds of this rank's batch come from HOST memory (copied into the
  * library's pinned staging, then to the device), the step runs (sampling keyed by
  * (epoch, g)), and this rank's loss is copied back; synchronous.  b_total = seeds in the
- * step over all ranks.  Optional prefetch: with next_g >= 0 the NEXT call's batch
- * (next_seeds_host[0:next_n), next_b_total, global index next_g, same epoch) is sampled on
- * the library's sampling stream while this batch trains; the next call with exactly those
- * (epoch, g, n_seeds, b_total) reuses it (its seeds_host is then not re-read).  next_g < 0:
- * no prefetch (next_* ignored).  The seed arrays are not retained after the call. */
+ * step over all ranks.  Seeds must be node ids in [0, N) (RANGE) without repeats (PARAM);
+ * they are checked on the host before they reach the device.  Optional prefetch: with
+ * next_g >= 0 the NEXT call's batch (next_seeds_host[0:next_n), next_b_total, global index
+ * next_g, same epoch) is checked and sampled on the library's sampling stream while this batch
+ * trains; the next call reuses it only if its (epoch, g, n_seeds, b_total) AND its seeds equal
+ * the prefetched ones (else it samples its own seeds).  A batch prefetched by
+ * gnn_train_minibatch (from the epoch permutation) is never reused here, nor the reverse.
+ * next_g < 0: no prefetch (next_* ignored).  The seed arrays are not retained after the call. */
 gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t n_seeds,
                                 int32_t b_total, int64_t epoch, int64_t g,
                                 const int32_t* next_seeds_host, int32_t next_n, int32_t next_b_total,

@@ -12,9 +12,11 @@
 // events order "sampled(B) -> train(B)" and "trained(A) -> sample into A".
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <climits>
+#include <cstddef>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -55,6 +57,12 @@ gnn_status fail(gnn_status s, const std::string& msg) {
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+// NVTX range around an ABI call (host side; Nsight tools attribute the enqueued kernels to it).
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+};
+
 template <class T>
 gnn_status dalloc(T** p, int64_t count, std::vector<void*>& owned) {
     *p = nullptr;
@@ -87,10 +95,13 @@ struct gnn_graph {
     std::vector<void*> ipc_opened;
     std::vector<void*> owned;
     // NEXT-2 feature cache of remote rows (sharded tables): device descriptor + its buffers
+    // (allocated with a sharded graph, so every captured step reads the current descriptor)
     FeatCache* cache_desc = nullptr;
     int32_t* cmap = nullptr;
     float* cache_rows = nullptr;
     int64_t cache_n = 0;
+    unsigned long long* cache_stats = nullptr;   // {local, peer, cache} row reads (gnn_cache_stats)
+    bool stats_on = false;
     FeatRows rows() const {
         return FeatRows{X, nshards ? shard_ptrs : nullptr, rps, nshards ? cache_desc : nullptr,
                         rps ? (int)(row_begin / rps) : 0};
@@ -119,6 +130,7 @@ struct BatchSet {
     bool trained_once = false;
     // the batch this set holds (valid until trained or overwritten)
     bool valid = false;
+    bool host_seeds = false;         // seeds came from a host array (e2e) rather than the epoch permutation
     int64_t epoch = -1, g = -1;
     int32_t n = -1, b_total = -1;
     cudaGraphExec_t gexec = nullptr, prof_gexec = nullptr;
@@ -187,6 +199,7 @@ struct gnn_model {
 
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
+    int exchange = GNN_EXCH_AUTO;        // gradient exchange (gnn_set_exchange)
 
     bool bf16x3 = true;                  // fp32 parity mode: 3-term bf16 split GEMMs
     int64_t launches_per_step = 0;
@@ -259,6 +272,13 @@ const int32_t* rows_ptr(gnn_model* m, int set, int li) {   // output rows of lay
     return &st->n_dst[m->layers[li].blk];
 }
 
+// The gradient exchange of a step (§2.2): NCCL all-reduce between the
+// reduce and the update (any world with GNN_EXCH_NCCL, world > 1 by default), else one rank's
+// reduce fused into the update.
+bool uses_nccl(const gnn_model* m) {
+    return m->exchange == GNN_EXCH_NCCL || (m->exchange == GNN_EXCH_AUTO && m->world > 1);
+}
+
 // ---------------------------------------------------------------- step bodies
 void enqueue_training(gnn_model* m, int set) {
     gnn_graph* g = m->g;
@@ -322,7 +342,7 @@ void enqueue_training(gnn_model* m, int set) {
             const int fixed_k = direct && !m->full_train ? m->bs[set].sp.hop[blk].k : 0;
             K(m, s, kid, [&] {
                 launch_agg_sage(rows, Hrows, ly.in_pad, direct ? nullptr : self_ids, self_ids, B.rowptr[blk],
-                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, s);
+                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, direct ? m->bs[set].sp.hop[blk].k : 0, s);
             });
         } else {
             K(m, s, kid, [&] {
@@ -378,7 +398,7 @@ void enqueue_training(gnn_model* m, int set) {
     }
     cudaEventRecord(m->ev_join, ws);
     cudaStreamWaitEvent(s, m->ev_join, 0);
-    if (m->world > 1) {
+    if (uses_nccl(m)) {
         // ---- split-K partials of every layer -> flat gradient (fixed order), exchange, update
         K(m, s, GNN_K_GEMM_WGRAD, [&] { launch_wgrad_reduce_all(pack_desc(m), m->grads, s); });
         K(m, s, GNN_K_ALLREDUCE, [&] {
@@ -434,6 +454,12 @@ void drop_graphs(gnn_model* m) {
 gnn_status check_ready(gnn_model* m) {
     if (m->g->nshards && !m->g->shard_ptrs)
         return fail(GNN_ERR_STATE, "row-sharded features: call gnn_shard_import before training");
+    if (uses_nccl(m) && !m->comm) {
+        if (m->world > 1) return fail(GNN_ERR_STATE, "world > 1 without a communicator (gnn_comm_init)");
+        ncclUniqueId id;   // GNN_EXCH_NCCL on one rank: a communicator of one
+        CKN(ncclGetUniqueId(&id));
+        CKN(ncclCommInitRank(&m->comm, 1, id, 0));
+    }
     return GNN_OK;
 }
 
@@ -502,6 +528,7 @@ gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const i
     CK(cudaGetLastError());
     CK(cudaEventRecord(B.sampled, m->sstream));
     B.valid = true;
+    B.host_seeds = seeds_dev == nullptr;
     B.epoch = epoch;
     B.g = g;
     B.n = n;
@@ -511,12 +538,13 @@ gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const i
 
 // The batch this rank trains at `step`: the engine's rule (plan_step), or the workload-balanced
 // schedule set with gnn_set_schedule (reading R8 with the batch order of NEXT-3).
-void plan_model_step(const gnn_model* m, int64_t step, int64_t* g, int32_t* n, int64_t* offset, int32_t* b_total) {
+gnn_status plan_model_step(const gnn_model* m, int64_t step, int64_t* g, int32_t* n, int64_t* offset, int32_t* b_total) {
     if (m->schedule.empty()) {
         plan_step(m->n_train, m->cfg.batch_size, m->world, m->rank, step, g, n, offset, b_total);
-        return;
+        return GNN_OK;
     }
     const int64_t B = m->cfg.batch_size, nb = (int64_t)m->schedule.size();
+    if (nb != num_batches(m)) return fail(GNN_ERR_STATE, "schedule does not cover the current batches (set it again)");
     auto seeds = [&](int64_t gg) { return (int32_t)std::min<int64_t>(B, m->n_train - gg * B); };
     const int64_t i = step * m->world + m->rank;
     *g = i < nb ? m->schedule[i] : nb + i;   // past the end: inactive (joins the exchange with zeros)
@@ -526,22 +554,42 @@ void plan_model_step(const gnn_model* m, int64_t step, int64_t* g, int32_t* n, i
     for (int64_t r = 0; r < m->world; ++r)
         if (step * m->world + r < nb) bt += seeds(m->schedule[step * m->world + r]);
     *b_total = (int32_t)bt;
+    return GNN_OK;
 }
 
 gnn_status issue_sample_step(gnn_model* m, int set, int64_t epoch, int64_t step) {
     TRY(ensure_perm(m, epoch));
     int64_t g, offset;
     int32_t n, b_total;
-    plan_model_step(m, step, &g, &n, &offset, &b_total);
+    TRY(plan_model_step(m, step, &g, &n, &offset, &b_total));
     return issue_sample(m, set, n > 0 ? m->perm + offset : m->perm, nullptr, n, b_total, epoch, g, m->full_train);
 }
 
-int find_set(gnn_model* m, int64_t epoch, int64_t g, int32_t n, int32_t b_total) {
+// The set holding this batch, if one was prefetched.  A set sampled from host seeds serves only a
+// host-seeded call with the same seeds (compared with the pinned staging copy), and a set sampled
+// from the epoch permutation only a permutation-driven step.
+int find_set(gnn_model* m, int64_t epoch, int64_t g, int32_t n, int32_t b_total, const int32_t* seeds_host = nullptr) {
     for (int k = 0; k < 2; ++k) {
         const BatchSet& B = m->bs[k];
-        if (B.valid && B.epoch == epoch && B.g == g && B.n == n && B.b_total == b_total) return k;
+        if (!B.valid || B.epoch != epoch || B.g != g || B.n != n || B.b_total != b_total) continue;
+        if (B.host_seeds != (seeds_host != nullptr)) continue;
+        if (seeds_host && n && std::memcmp(B.seeds_stage, seeds_host, sizeof(int32_t) * n) != 0) continue;
+        return k;
     }
     return -1;
+}
+
+// Host seeds must be node ids in [0, N) without repeats: the sampling kernel indexes the CSR and
+// the node map with them (an out-of-range id would write outside device memory).
+gnn_status check_seeds(const gnn_model* m, const int32_t* seeds, int32_t n) {
+    thread_local std::vector<int32_t> tmp;
+    tmp.assign(seeds, seeds + n);
+    std::sort(tmp.begin(), tmp.end());
+    for (int32_t i = 0; i < n; ++i) {
+        if (tmp[i] < 0 || tmp[i] >= m->g->N) return fail(GNN_ERR_RANGE, "seed id " + std::to_string(tmp[i]) + " out of [0, N)");
+        if (i && tmp[i] == tmp[i - 1]) return fail(GNN_ERR_PARAM, "duplicate seed id " + std::to_string(tmp[i]));
+    }
+    return GNN_OK;
 }
 
 int other_set(gnn_model* m) { return m->last < 0 ? 0 : 1 - m->last; }
@@ -581,7 +629,7 @@ gnn_status train_set(gnn_model* m, int set) {
 gnn_status step_from_perm(gnn_model* m, int64_t epoch, int64_t step) {
     int64_t g, offset;
     int32_t n, b_total;
-    plan_model_step(m, step, &g, &n, &offset, &b_total);
+    TRY(plan_model_step(m, step, &g, &n, &offset, &b_total));
     int cur = find_set(m, epoch, g, n, b_total);
     if (cur < 0) {
         cur = other_set(m);
@@ -623,6 +671,7 @@ static gnn_status graph_create(int64_t num_nodes, const int64_t* row_ptr_host, c
 gnn_status gnn_graph_create(int64_t num_nodes, const int64_t* row_ptr_host, const int32_t* col_idx_host,
                             int32_t feat_dim, int32_t feat_stride, const float* features_host,
                             const int32_t* labels_host, int32_t num_classes, int32_t device, gnn_graph** out) {
+    Range nvtx_("gnn_graph_create");
     return graph_create(num_nodes, row_ptr_host, col_idx_host, feat_dim, feat_stride, features_host, labels_host,
                         num_classes, device, 1, 0, out);
 }
@@ -660,12 +709,8 @@ gnn_status gnn_cache_rows(gnn_graph* g, const int32_t* ids_host, int64_t n) {
         seen[v] = 1;
     }
     CK(cudaDeviceSynchronize());   // no kernel may be reading the previous cache
-    if (!g->cache_desc) {
-        gnn_status st = dalloc(&g->cache_desc, 1, g->owned);
-        if (st != GNN_OK) return st;
-        CK(cudaMemset(g->cache_desc, 0, sizeof(FeatCache)));
-    }
-    FeatCache off{nullptr, nullptr};
+    unsigned long long* stats = g->stats_on ? g->cache_stats : nullptr;
+    FeatCache off{nullptr, nullptr, stats};
     CK(cudaMemcpy(g->cache_desc, &off, sizeof(FeatCache), cudaMemcpyHostToDevice));
     if (g->cache_rows) { cudaFree(g->cache_rows); g->cache_rows = nullptr; }
     g->cache_n = 0;
@@ -684,9 +729,29 @@ gnn_status gnn_cache_rows(gnn_graph* g, const int32_t* ids_host, int64_t n) {
     CK(cudaMemcpy(g->cmap, slots.data(), sizeof(int32_t) * g->N, cudaMemcpyHostToDevice));
     CK(cudaDeviceSynchronize());
     cudaFree(ids_dev);
-    FeatCache on{g->cmap, g->cache_rows};
+    FeatCache on{g->cmap, g->cache_rows, stats};
     CK(cudaMemcpy(g->cache_desc, &on, sizeof(FeatCache), cudaMemcpyHostToDevice));
     g->cache_n = n;
+    return GNN_OK;
+}
+
+gnn_status gnn_cache_stats(gnn_graph* g, int32_t enable, int64_t* counts_out_host) {
+    if (!g) return fail(GNN_ERR_PARAM, "NULL graph");
+    if (g->nshards < 1) return fail(GNN_ERR_STATE, "graph is not sharded");
+    TRY(set_device(g->dev));
+    CK(cudaDeviceSynchronize());   // the counts of every step enqueued so far
+    unsigned long long h[3] = {0, 0, 0};
+    CK(cudaMemcpy(h, g->cache_stats, sizeof(h), cudaMemcpyDeviceToHost));
+    if (counts_out_host)
+        for (int i = 0; i < 3; ++i) counts_out_host[i] = (int64_t)h[i];
+    if (enable >= 0) {
+        CK(cudaMemset(g->cache_stats, 0, 3 * sizeof(unsigned long long)));
+        g->stats_on = enable != 0;
+        // the descriptor lives at a fixed address: captured steps see the switch
+        unsigned long long* stats = g->stats_on ? g->cache_stats : nullptr;
+        CK(cudaMemcpy(reinterpret_cast<char*>(g->cache_desc) + offsetof(FeatCache, stats), &stats, sizeof(stats),
+                      cudaMemcpyHostToDevice));
+    }
     return GNN_OK;
 }
 
@@ -782,6 +847,13 @@ static gnn_status graph_create(int64_t num_nodes, const int64_t* row_ptr_host, c
         e = cudaMemset2D(g->X + feat_dim, sizeof(float) * feat_stride, 0, sizeof(float) * (feat_stride - feat_dim),
                          local_rows);
     if (e != cudaSuccess) return cleanup(fail(GNN_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e)));
+    if (g->nshards) {   // the NEXT-2 cache descriptor (empty) and its counters, at fixed addresses
+        if ((s = dalloc(&g->cache_desc, 1, g->owned)) != GNN_OK) return cleanup(s);
+        if ((s = dalloc(&g->cache_stats, 3, g->owned)) != GNN_OK) return cleanup(s);
+        e = cudaMemset(g->cache_desc, 0, sizeof(FeatCache));
+        if (e == cudaSuccess) e = cudaMemset(g->cache_stats, 0, 3 * sizeof(unsigned long long));
+        if (e != cudaSuccess) return cleanup(fail(GNN_ERR_CUDA, std::string("cache descriptor: ") + cudaGetErrorString(e)));
+    }
     if (!check_symmetric(g->row_ptr, g->col, num_nodes, &g->symmetric))
         return cleanup(fail(GNN_ERR_CUDA, "symmetry check failed"));
     *out = g;
@@ -800,6 +872,7 @@ gnn_status gnn_graph_destroy(gnn_graph* g) {
 }
 
 gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model** out) {
+    Range nvtx_("gnn_model_create");
     if (!g || !cfg || !out) return fail(GNN_ERR_PARAM, "NULL argument");
     *out = nullptr;
     const gnn_model_config& c = *cfg;
@@ -1119,6 +1192,7 @@ gnn_status gnn_set_train_nodes(gnn_model* m, const int32_t* ids_host, int64_t n)
     if (n) CK(cudaMemcpy(m->train_sorted, ids.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     m->n_train = n;
     m->perm_epoch = -1;
+    m->schedule.clear();   // a schedule lists the previous split's batches
     for (auto& B : m->bs) B.valid = false;
     return GNN_OK;
 }
@@ -1186,6 +1260,18 @@ gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_
     return GNN_OK;
 }
 
+gnn_status gnn_set_exchange(gnn_model* m, int32_t mode) {
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    if (mode != GNN_EXCH_AUTO && mode != GNN_EXCH_NCCL) return fail(GNN_ERR_PARAM, "unknown exchange mode");
+    TRY(set_device(m->g->dev));
+    TRY(sync_all(m));
+    if (mode != m->exchange) {
+        m->exchange = mode;
+        drop_graphs(m);   // the captured step holds the previous exchange
+    }
+    return GNN_OK;
+}
+
 gnn_status gnn_epoch_permutation(gnn_model* m, int64_t epoch, int32_t* out_host, int64_t n) {
     if (!m || (!out_host && m->n_train)) return fail(GNN_ERR_PARAM, "NULL argument");
     if (n < m->n_train) return fail(GNN_ERR_BUFFER, "need n_train = " + std::to_string(m->n_train));
@@ -1198,6 +1284,7 @@ gnn_status gnn_epoch_permutation(gnn_model* m, int64_t epoch, int32_t* out_host,
 }
 
 gnn_status gnn_sample(gnn_model* m, int64_t epoch, int64_t g, gnn_batch_sizes* sizes_host) {
+    Range nvtx_("gnn_sample");
     if (!m || !sizes_host) return fail(GNN_ERR_PARAM, "NULL argument");
     const int64_t nb = num_batches(m);
     if (g < 0 || g >= nb) return fail(GNN_ERR_RANGE, "batch index out of range");
@@ -1252,6 +1339,7 @@ gnn_status gnn_sample_fetch(gnn_model* m, int32_t hop, int32_t what, int32_t* ou
 }
 
 gnn_status gnn_train_minibatch(gnn_model* m, int64_t epoch, int64_t step, float* loss_out_host) {
+    Range nvtx_("gnn_train_minibatch");
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
     if (step < 0 || epoch < 0) return fail(GNN_ERR_PARAM, "negative epoch/step");
     TRY(set_device(m->g->dev));
@@ -1267,6 +1355,7 @@ gnn_status gnn_train_minibatch(gnn_model* m, int64_t epoch, int64_t step, float*
 gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t n_seeds, int32_t b_total,
                                 int64_t epoch, int64_t g, const int32_t* next_seeds_host, int32_t next_n,
                                 int32_t next_b_total, int64_t next_g, float* loss_out_host) {
+    Range nvtx_("gnn_train_batch_host");
     if (!m || (n_seeds > 0 && !seeds_host) || !loss_out_host) return fail(GNN_ERR_PARAM, "NULL argument");
     if (n_seeds < 0 || n_seeds > m->cfg.batch_size) return fail(GNN_ERR_SHAPE, "n_seeds must be 0..batch_size");
     if (b_total < n_seeds) return fail(GNN_ERR_PARAM, "b_total < n_seeds");
@@ -1275,20 +1364,24 @@ gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t
         return fail(GNN_ERR_PARAM, "bad next batch");
     TRY(set_device(m->g->dev));
     TRY(check_ready(m));
-    int cur = find_set(m, epoch, g, n_seeds, b_total);
+    int cur = find_set(m, epoch, g, n_seeds, b_total, seeds_host ? seeds_host : m->bs[0].seeds_stage);
     if (cur < 0) {
+        TRY(check_seeds(m, seeds_host, n_seeds));
         cur = other_set(m);
         TRY(issue_sample(m, cur, nullptr, seeds_host, n_seeds, b_total, epoch, g, m->full_train));
     }
     TRY(train_set(m, cur));
     CK(cudaMemcpyAsync(loss_out_host, &m->bs[cur].st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
-    if (prefetch && m->overlap && !m->profiling)   // after the training launch (see step_from_perm)
+    if (prefetch && m->overlap && !m->profiling) {   // after the training launch (see step_from_perm)
+        TRY(check_seeds(m, next_seeds_host, next_n));   // host work that overlaps the step on the device
         TRY(issue_sample(m, 1 - cur, nullptr, next_seeds_host, next_n, next_b_total, epoch, next_g, m->full_train));
+    }
     CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }
 
 gnn_status gnn_train_epoch(gnn_model* m, int64_t epoch, gnn_epoch_stats* out_host) {
+    Range nvtx_("gnn_train_epoch");
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
     TRY(set_device(m->g->dev));
     const int64_t nb = num_batches(m);
@@ -1428,6 +1521,7 @@ gnn_status gnn_profile_reset(gnn_model* m) {
 int64_t gnn_launches_per_step(const gnn_model* m) { return m ? m->launches_per_step : -1; }
 // ---------------------------------------------------------------- NEXT-3: workload-aware batch assignment
 gnn_status gnn_estimate_workload(gnn_model* m, int64_t epoch, int64_t* work_out_host, int64_t n) {
+    Range nvtx_("gnn_estimate_workload");
     if (!m || !work_out_host) return fail(GNN_ERR_PARAM, "NULL argument");
     const int64_t nb = num_batches(m);
     if (n != nb) return fail(GNN_ERR_SHAPE, "n must equal the number of batches " + std::to_string(nb));

@@ -3,8 +3,11 @@
 // packing for the tensor-core GEMMs (gemm_tc.cu), SGD.  All extents come from the device
 // StepState (graph-replayable).  GEMM operands are written as bf16 split planes.
 #include <cub/block/block_reduce.cuh>
+#include <cstdlib>
+#include <map>
 
 #include "kernels.h"
+#include "tma.cuh"
 
 // k_agg_sage register cap (experiments only): GS_AGG_MINB = n -> __launch_bounds__(256, n).  The
 // default (no minimum-blocks hint) compiles to 48 registers and was measured fastest (A/B:
@@ -156,6 +159,114 @@ __global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
                 store_split4(A, tix(A, i, 4 * (nch + ch)), f4scale(acc[c], inv));
             }
         }
+    }
+}
+
+// ------------------------------------------------------------------ layer-1 gather, staged by TMA
+// The fused feature gather + mean of layer 1 (S4 + S5: X rows read by global id), with every row
+// moved by the bulk-copy engine (cp.async.bulk global -> shared, one instruction per row, no
+// registers held while it is in flight) instead of per-lane vector loads.  Each warp owns NB
+// row buffers of `slots` = 1 + k_max row slots (self row + the sampled neighbours of one
+// destination row) and an mbarrier per buffer.  For its t-th destination row the warp's lanes
+// issue the row copies in parallel (lane 0: self row, lane j: neighbour j-1) after lane 0 armed
+// the buffer's barrier with the row bytes; while rows t+1 .. t+NB-1 are in flight the warp waits
+// for row t's barrier, sums the neighbour rows from shared memory in CSR order (plain fp32 adds,
+// then times the correctly rounded 1/deg: the same arithmetic as k_agg_sage), writes [self | mean]
+// as split planes, and re-arms the buffer with row t+NB.
+// Memory-level parallelism: NB x (1 + k) rows per warp in flight (products: 2 x 16 rows of 400 B
+// = 12.8 KB per warp, ~200 KB per SM) against ~4 rows per warp for register loads.
+constexpr int kL1Warps = 4;   // warps per block
+template <int NB>
+__global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __restrict__ rows_ptr,
+        const float* __restrict__ X, int in_pad, const int32_t* __restrict__ smap,
+        const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col, Split A, int fixed_k, int slots) {
+    extern __shared__ __align__(128) unsigned char l1_smem[];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    uint64_t* bar = reinterpret_cast<uint64_t*>(l1_smem) + warp * NB;
+    const uint32_t row_bytes = (uint32_t)in_pad * 4u;
+    float* ring = reinterpret_cast<float*>(l1_smem + 128 + (size_t)warp * NB * slots * row_bytes);
+    if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_async_smem();
+    }
+    __syncwarp();
+    pdl_trigger();
+    pdl_wait();
+    const int n = *rows_ptr;
+    const int nch = in_pad >> 2;
+    const int64_t W = total_warps();
+    const int64_t gw = global_warp();
+    // zero tail rows [n, round64(n)) of the operand planes
+    for (int64_t i = n + gw; i < round64(n); i += W)
+        for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, tix(A, i, 4 * ch), kZero4);
+    const uint64_t pol = policy_evict_normal();
+    int cnt[NB];
+    // arm buffer b with destination row i: self row -> slot 0, neighbour j -> slot 1 + j
+    auto issue = [&](int b, int64_t i) {
+        int beg, c;
+        int nb = 0;
+        if (fixed_k) {   // fixed-stride rows: the count and the ids load in parallel
+            beg = (int)i * fixed_k;
+            if (lane < fixed_k) nb = col[beg + lane];
+            c = rowptr[i];
+        } else {
+            beg = rowptr[i];
+            c = rowptr[i + 1] - beg;
+            if (lane < c) nb = col[beg + lane];
+        }
+        const int self = smap[i];
+        float* buf = ring + (size_t)b * slots * in_pad;
+        if (lane == 0) mbar_expect_tx(&bar[b], (uint32_t)(c + 1) * row_bytes);
+        __syncwarp();
+        const int src = __shfl_up_sync(0xffffffffu, nb, 1);   // lane j (>= 1) takes neighbour j-1
+        if (lane <= c) {
+            const int r = lane == 0 ? self : src;
+            bulk_g2s(buf + (size_t)lane * in_pad, X + (int64_t)r * in_pad, row_bytes, &bar[b], pol);
+        }
+        return c;
+    };
+#pragma unroll
+    for (int b = 0; b < NB; ++b) cnt[b] = gw + b * W < n ? issue(b, gw + b * W) : 0;
+    uint32_t phase = 0;   // parity bit of every buffer's current use (buffers are used round-robin)
+    int b = 0;
+    for (int64_t i = gw; i < n; i += W) {
+        mbar_wait(&bar[b], phase);
+        const float* buf = ring + (size_t)b * slots * in_pad;
+        int c = cnt[0];
+#pragma unroll
+        for (int q = 1; q < NB; ++q) if (b == q) c = cnt[q];
+        float4 sv = kZero4, acc = kZero4;
+        if (lane < nch) {
+            sv = reinterpret_cast<const float4*>(buf)[lane];
+            for (int j = 1; j <= c; ++j) acc = f4add(acc, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane]);
+        }
+        // rows of more than 128 floats: lanes take further chunks
+        float4 sv2 = kZero4, acc2 = kZero4;
+        const bool wide = nch > 32;
+        if (wide && lane + 32 < nch) {
+            sv2 = reinterpret_cast<const float4*>(buf)[lane + 32];
+            for (int j = 1; j <= c; ++j) acc2 = f4add(acc2, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane + 32]);
+        }
+        // the buffer is read: re-arm it with this warp's row i + NB*W (async-proxy writes after
+        // generic-proxy reads of the same shared memory need the proxy fence)
+        fence_async_smem();
+        __syncwarp();
+        const int64_t inext = i + (int64_t)NB * W;
+        const int cn = inext < n ? issue(b, inext) : 0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) if (b == q) cnt[q] = cn;
+        const float inv = c ? 1.0f / (float)c : 0.f;   // one division per row (R23)
+        if (lane < nch) {
+            store_split4(A, tix(A, i, 4 * lane), sv);
+            store_split4(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv));
+        }
+        if (wide && lane + 32 < nch) {
+            store_split4(A, tix(A, i, 4 * (lane + 32)), sv2);
+            store_split4(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv));
+        }
+        if (++b == NB) { b = 0; phase ^= 1u; }
     }
 }
 
@@ -778,9 +889,42 @@ int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
         default: launch_pdl(KERNEL<8>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;           \
     }
 
+template <int NB>
+static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, const int32_t* smap,
+                           const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k, int slots,
+                           cudaStream_t s) {
+    const size_t smem = 128 + (size_t)kL1Warps * NB * slots * in_pad * 4;
+    if (smem > 200 * 1024) return false;
+    static std::map<size_t, int> grids;   // smem bytes -> co-resident blocks x SMs (occupancy-derived)
+    int& grid = grids[smem];
+    if (!grid) {
+        cudaFuncSetAttribute(k_agg_l1_bulk<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_l1_bulk<NB>, kL1Warps * 32, smem);
+        if (per_sm < 1) return false;
+        grid = per_sm * sms;
+    }
+    launch_pdl(k_agg_l1_bulk<NB>, grid, kL1Warps * 32, smem, s, rows_ptr, X, in_pad, smap, blk_rowptr, col, A,
+               fixed_k, slots);
+    return true;
+}
+
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
-                     cudaStream_t s) {
+                     int k_max, cudaStream_t s) {
+    // layer 1 of the neighbour sampler on a local table: rows staged by the bulk-copy engine
+    // (GS_L1_BULK=0: register loads, for A/B; GS_L1_NB: buffers per warp)
+    static const int bulk = [] { const char* e = std::getenv("GS_L1_BULK"); return e ? std::atoi(e) : 1; }();
+    static const int nb = [] { const char* e = std::getenv("GS_L1_NB"); return e ? std::atoi(e) : 2; }();
+    if (bulk && !H.shards && !gmap && smap && k_max > 0 && k_max <= 31 && in_pad * 4 <= 1024) {
+        const bool ok = nb == 3 ? launch_l1_bulk<3>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
+                                                     1 + k_max, s)
+                                : launch_l1_bulk<2>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
+                                                     1 + k_max, s);
+        if (ok) return;
+    }
     GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A, fixed_k);
 }
 

@@ -115,24 +115,29 @@ __host__ __device__ __forceinline__ int64_t tix(const Split& o, int64_t r, int64
 // instead (the GPU feature cache of PAPER.md §3.3, re-aimed at NVLink traffic).
 // The cache descriptor lives in device memory at a fixed address, so captured CUDA graphs
 // see a cache installed after capture.
-struct FeatCache { const int32_t* cmap; const float* rows; };
+// stats (nullable, gnn_cache_stats): row reads by source {local shard, peer, cache replica},
+// counted once per warp-level row read (lane 0), so tests and the bench can see the cache work.
+struct FeatCache { const int32_t* cmap; const float* rows; unsigned long long* stats; };
 struct FeatRows {
     const float* base;
     const float* const* shards;
     int64_t rps;
-    const FeatCache* cache;   // sharded tables only (nullable)
+    const FeatCache* cache;   // sharded tables only (allocated with the graph: never null then)
     int own;                  // this process's shard
+    __device__ __forceinline__ void count(int which) const {
+        unsigned long long* st = cache->stats;
+        if (st && (threadIdx.x & 31) == 0) atomicAdd(st + which, 1ull);
+    }
     __device__ __forceinline__ const float* row(int r, int ld) const {
         if (!shards) return base + (int64_t)r * ld;
         const int s = (int)(r / rps);
-        if (s == own) return base + (int64_t)(r - s * rps) * ld;
-        if (cache) {
-            const int32_t* cm = cache->cmap;
-            if (cm) {
-                const int c = __ldg(cm + r);
-                if (c >= 0) return cache->rows + (int64_t)c * ld;
-            }
+        if (s == own) { count(0); return base + (int64_t)(r - s * rps) * ld; }
+        const int32_t* cm = cache->cmap;
+        if (cm) {
+            const int c = __ldg(cm + r);
+            if (c >= 0) { count(2); return cache->rows + (int64_t)c * ld; }
         }
+        count(1);
         return shards[s] + (int64_t)(r - s * rps) * ld;
     }
 };
@@ -143,10 +148,11 @@ void launch_cache_fill(FeatRows src, const int32_t* ids, int64_t n, int ld, floa
 // source c is gmap ? gmap[c] : c, self row smap ? smap[i] : i (layer 1 reads X by global id:
 // the fused feature gather).
 // fixed_k > 0: the block is fixed-stride (row i's sources at col[i*fixed_k], count in
-// blk_rowptr[i]; the training-only last hop of the sampling kernel).
+// blk_rowptr[i]; the training-only last hop of the sampling kernel).  k_max: the block's fanout
+// (rows have at most k_max sources); layer 1 on a local table then stages rows by bulk copy.
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
-                     cudaStream_t s);
+                     int k_max, cudaStream_t s);
 // GCN aggregation A = Â H (self loop included) for rows i < *rows_ptr of a block with
 // *ndst_ptr destinations; d_out from the transposed row pointer.  col must be local ids.
 void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,

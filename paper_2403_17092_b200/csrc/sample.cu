@@ -42,7 +42,8 @@ __global__ void k_cache_fill(FeatRows src, const int32_t* __restrict__ ids, int6
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = w0; i < n; i += nw) {
-        const float4* p = reinterpret_cast<const float4*>(src.row(ids[i], ld));
+        const int64_t r = ids[i], sh = r / src.rps;   // the owner's copy (never the cache itself)
+        const float4* p = reinterpret_cast<const float4*>(src.shards[sh] + (r - sh * src.rps) * ld);
         float4* q = reinterpret_cast<float4*>(out + i * ld);
         for (int c = lane; c < (ld >> 2); c += 32) q[c] = p[c];
     }
@@ -52,7 +53,6 @@ __global__ void k_cache_fill(FeatRows src, const int32_t* __restrict__ ids, int6
 
 void launch_cache_fill(FeatRows src, const int32_t* ids, int64_t n, int ld, float* out, cudaStream_t s) {
     if (n <= 0) return;
-    src.cache = nullptr;   // read the owners' copies
     k_cache_fill<<<148 * 8, 256, 0, s>>>(src, ids, n, ld, out);
 }
 

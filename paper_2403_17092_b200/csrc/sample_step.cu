@@ -15,6 +15,8 @@
 #include <cub/block/block_scan.cuh>
 #include <climits>
 
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace gs {
@@ -554,8 +556,23 @@ int sample_step_grid() {
 // scan sites per step: 2 per hop + 1 induce + 1 per transposed block
 int sample_step_sites(int hops) { return 2 * hops + 1 + (hops + 1); }
 
+// The phases are separated by a software grid barrier and the scans spin on predecessors' words,
+// so every block must be resident at once: the launch is cooperative (the driver guarantees
+// co-residency, and refuses a grid larger than occupancy x SMs; sample_step_grid() is exactly one
+// block per SM).  GS_SAMPLE_COOP=0 launches it as a plain grid (A/B only).
 void launch_sample_step(const SampleParams& p, cudaStream_t s) {
-    k_sample_step<<<sample_step_grid(), kThreads, kSortSmem, s>>>(p);
+    static const bool coop = [] { const char* e = std::getenv("GS_SAMPLE_COOP"); return !(e && e[0] == '0'); }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sample_step_grid());
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSortSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = coop ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k_sample_step, p);
 }
 
 }  // namespace gs

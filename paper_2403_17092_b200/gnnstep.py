@@ -16,6 +16,7 @@ GNN_FP32, GNN_BF16_GEMM = 0, 1
 GNN_SRC_IDS, GNN_BLK_ROWPTR, GNN_BLK_COL, GNN_BLK_NBR = 0, 1, 2, 3
 GNN_DBG_LOGITS, GNN_DBG_GRADS, GNN_DBG_LOSS, GNN_DBG_ACT = 0, 1, 2, 16
 GNN_SGD, GNN_ADAM = 0, 1
+GNN_EXCH_AUTO, GNN_EXCH_NCCL = 0, 1
 ABI_VERSION = 2   # include/gnnstep.h GNN_ABI_VERSION
 KERNEL_IDS = dict(sample=0, relabel=1, agg_l1=2, agg=3, gemm_fwd=4, gemm_dgrad=5, gemm_wgrad=6,
                   spmm_bwd=7, ce=8, sgd=9, transpose=10, induce=11, allreduce=12, scan=13, other=14)
@@ -79,7 +80,8 @@ def lib():
             "gnn_profile_reset": ([P], I32), "gnn_launches_per_step": ([P], I64),
             "gnn_graph_symmetric": ([P], I32),
             "gnn_estimate_workload": ([P, I64, P, I64], I32), "gnn_plan_balanced": ([P, I64, I32, P], I32),
-            "gnn_set_schedule": ([P, P, I64], I32),
+            "gnn_set_schedule": ([P, P, I64], I32), "gnn_set_exchange": ([P, I32], I32),
+            "gnn_cache_stats": ([P, I32, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(_lib, name)
@@ -206,6 +208,11 @@ class Model:
     def set_params(self, p):
         p = np.ascontiguousarray(p, dtype=np.float32)
         _check(lib().gnn_set_params(self.h, _ptr(p), p.shape[0]))
+
+    def set_exchange(self, mode: str):
+        """gnn_set_exchange: "auto" (world 1: reduce fused into the update) or "nccl" (reduce ->
+        ncclAllReduce -> update, on any world; world 1 uses a one-rank communicator)."""
+        _check(lib().gnn_set_exchange(self.h, {"auto": GNN_EXCH_AUTO, "nccl": GNN_EXCH_NCCL}[mode]))
 
     def comm_init(self, rank: int, world: int, uid: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
@@ -425,6 +432,13 @@ class ShardedGraph(Graph):
             return
         a = np.ascontiguousarray(ids, dtype=np.int32)
         _check(L.gnn_cache_rows(self.h, _ptr(a), a.shape[0]))
+
+    def cache_stats(self, enable=-1):
+        """gnn_cache_stats: row reads {local, peer, cache} since the last reset (synchronizes);
+        enable 1 = reset + count, 0 = reset + stop, -1 = read only."""
+        out = np.zeros(3, dtype=np.int64)
+        _check(lib().gnn_cache_stats(self.h, enable, _ptr(out)))
+        return dict(local=int(out[0]), peer=int(out[1]), cache=int(out[2]))
 
     def import_handles(self, handles):
         blob = b"".join(handles)

@@ -47,7 +47,7 @@ def test_fullsize_training_parity(name):
     for step in range(CASES[name]["steps"]):
         loss = m.train_minibatch(0, step)
         out = check_train_step(m, w, graph, params, 0, step, perm, loss)
-        print(name, step, out["errors"], "kink flips", out["kink_flips"])
+        print(name, step, out["errors"], "elementwise", out["elem"], "kink flips", out["kink_flips"])
         params = out["params"]
         assert rel(m.get_params(), params) <= TOL_FP32
     # ragged last batch through the end-to-end host call, from the initial params
@@ -57,3 +57,40 @@ def test_fullsize_training_parity(name):
     loss = m.train_batch_host(seeds, len(seeds), 0, last)
     out = check_train_step(m, w, graph, inp["params"], 0, last, perm, loss)
     print(name, "ragged", out["errors"], "kink flips", out["kink_flips"])
+
+
+@pytest.mark.parametrize("name", ["products", "reddit"])
+def test_fullsize_bf16_gemm_parity(name):
+    """The bf16-GEMM variant at full size (BASELINE.json north_star: within 2e-2): steps 0-1 and
+    the ragged last batch, loss / logits / every layer's dW."""
+    w, inp, graph = inputs_for(name)
+    g, m = make_gpu(w, inp, precision="bf16")
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    params = inp["params"].astype(np.float64)
+    for step in range(2):
+        loss = m.train_minibatch(0, step)
+        out = check_train_step(m, w, graph, params, 0, step, perm, loss, precision="bf16")
+        print(name, "bf16", step, out["errors"], "kink flips", out["kink_flips"])
+        params = out["params"]
+        assert rel(m.get_params(), params) <= 2e-2
+    last = w.n_batches - 1
+    seeds = OS.batch_seeds(perm, w.batch_size, last)
+    m.set_params(inp["params"])
+    loss = m.train_batch_host(seeds, len(seeds), 0, last)
+    out = check_train_step(m, w, graph, inp["params"], 0, last, perm, loss, precision="bf16")
+    print(name, "bf16 ragged", out["errors"], "kink flips", out["kink_flips"])
+
+
+@pytest.mark.parametrize("name", ["products"])
+def test_fullsize_exchange_nccl_equals_fused(name):
+    """The multi-rank branch (reduce -> one-rank ncclAllReduce -> update) in the bench's launch
+    configuration: bit-identical to the fused path over 3 steps."""
+    w, inp, graph = inputs_for(name)
+    runs = []
+    for exch in ("auto", "nccl"):
+        g, m = make_gpu(w, inp, exchange=exch)
+        losses = [m.train_minibatch(0, s) for s in range(3)]
+        runs.append((np.array(losses), m.grads(), m.get_params()))
+        m.close(); g.close()
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)

@@ -47,6 +47,7 @@ def _worker(rank, world, port, name, q, cache=False):
         dist.barrier()
         perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
         errs, plain = [], []
+        g.cache_stats(1)
         for gidx in (rank, rank + 2):
             seeds = OS.batch_seeds(perm, w.batch_size, gidx)
             m.set_params(inp["params"])
@@ -54,18 +55,28 @@ def _worker(rank, world, port, name, q, cache=False):
             out = check_train_step(m, w, graph, inp["params"].astype(np.float64), 0, gidx, perm, loss)
             errs.append(out["errors"])
             plain.append((loss, m.grads()))
+        st0 = g.cache_stats(0)
+        assert st0["cache"] == 0 and st0["peer"] > 0 and st0["local"] > 0, st0
         if cache:
             # NEXT-2: replicate the hottest quarter of the remote rows; the replica is an exact
-            # copy, so every step must be bit-identical to the uncached one
+            # copy, so every step must be bit-identical to the uncached one.  The training step
+            # was captured above, BEFORE the cache existed: the captured graph must still read it
+            # (ADVICE r1), which the row-read counters show (cache hits > 0, fewer peer reads).
             from paper_2403_17092_b200 import cache_plan_by_degree
             ids = cache_plan_by_degree(inp["row_ptr"], world, rank, w.num_nodes // 4)
             assert len(ids) and ((ids < b) | (ids >= e)).all()
             g.cache_rows(ids)
+            g.cache_stats(1)
             for k, gidx in enumerate((rank, rank + 2)):
                 seeds = OS.batch_seeds(perm, w.batch_size, gidx)
                 m.set_params(inp["params"])
                 loss = m.train_batch_host(seeds, len(seeds), 0, gidx)
                 assert loss == plain[k][0] and np.array_equal(m.grads(), plain[k][1]), "cache changed the result"
+            st1 = g.cache_stats(0)
+            assert st1["cache"] > 0, st1
+            assert st1["local"] == st0["local"] and st1["peer"] + st1["cache"] == st0["peer"], (st0, st1)
+            errs.append(dict(remote_gathers_removed=st1["cache"] / st0["peer"]))
+            print(name, rank, "row reads without cache", st0, "with cache", st1)
             g.cache_rows(None)
         dist.barrier()                 # peers keep their blocks mapped until everyone is done
         m.close()
@@ -94,4 +105,7 @@ def test_sharded_feature_gather_matches_oracle(name, cache):
         if isinstance(v, Exception):
             raise v
         for e in v:
+            if "remote_gathers_removed" in e:
+                assert e["remote_gathers_removed"] > 0.05, (r, e)   # hottest quarter of the remote rows
+                continue
             assert max(e.values()) <= 1e-4, (r, e)

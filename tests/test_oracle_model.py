@@ -72,6 +72,42 @@ def test_gcn_symmetric_square_block_is_kipf_welling():
     assert np.allclose(got, want, rtol=1e-14, atol=1e-15)
 
 
+def _read_gcn_golden():
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "gcn_bipartite_block.txt")
+    cases, cur = {}, None
+    for ln in open(path):
+        f = ln.split()
+        if not f or f[0].startswith("#"):
+            continue
+        if f[0] in ("block", "star"):
+            cur = cases.setdefault(f[0], dict(n_dst=int(f[1]), n_src=int(f[2]), want={}))
+        elif f[0] in ("rowptr", "col"):
+            cur[f[0]] = [int(x) for x in f[1:]]
+        else:
+            cur["want"][(int(f[1]), int(f[2]))] = float(f[3])
+    return cases
+
+
+@pytest.mark.parametrize("case", ["block", "star"])
+def test_gcn_bipartite_block_golden(case):
+    """Â of reading R12 on a bipartite block (and SPEC's star), against weights derived by hand in
+    tests/golden/gcn_bipartite_block.txt.  A "+1 on every source out-degree" or a "self weight
+    1/(deg_in+1)" misreading fails here (both change a hand-derived entry)."""
+    c = _read_gcn_golden()[case]
+    rp, col = c["rowptr"], c["col"]
+    blk = _block(c["n_dst"], c["n_src"], [col[rp[v]:rp[v + 1]] for v in range(c["n_dst"])])
+    got = M.normalized_adjacency(blk, "gcn").toarray()
+    want = np.zeros_like(got)
+    for (v, u), x in c["want"].items():
+        want[v, u] = x
+    assert len(c["want"]) == got.size or case == "star"
+    assert np.allclose(got, want, rtol=1e-15, atol=1e-16)
+    if case == "star":   # the documented deviation from SPEC.md normalize_block (line 186)
+        spec = np.array([[1 / 4, 1 / math.sqrt(8), 1 / math.sqrt(8), 1 / math.sqrt(8)]])
+        assert not np.allclose(got, spec)
+
+
 # ---------------------------------------------------------------- O6
 def test_ce_invariants_and_torch():
     C = 8

@@ -197,3 +197,26 @@ def test_shadow_induced_equals_membership_filter(gseed):
         r = np.repeat(np.arange(hp["n_dst"]), np.diff(hp["blk_rowptr"]))
         for e in range(hp["n_edges"]):
             assert (hp["blk_nbr"][e], src[r[e]]) in ind_global
+
+
+def test_epoch_perm_golden():
+    """O1 against the hand-derived orders of tests/golden/epoch_perm_example.txt (key64 = w0:w1 of
+    Philox tag 1 at the stated counters, sorted ascending).  A swapped word order, a wrong counter
+    layout (tag / epoch field) or a descending sort fails here."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "epoch_perm_example.txt")
+    words, perms = {}, {}
+    for ln in open(path):
+        f = ln.split()
+        if not f or f[0].startswith("#"):
+            continue
+        if f[0] == "words":
+            words[(int(f[1]), int(f[2]), int(f[3]))] = (int(f[4], 16), int(f[5], 16))
+        else:
+            perms[(int(f[1]), int(f[2]))] = [int(x) for x in f[4:]]
+    for (seed, epoch, v), (w0, w1) in words.items():
+        out = S.philox4x32([v, 0, (1 << 28) | ((epoch & 0xFFFFF) << 8), 0], [seed & 0xFFFFFFFF, seed >> 32])
+        assert (int(out[0]), int(out[1])) == (w0, w1)
+    for (seed, epoch), order in perms.items():
+        got = S.epoch_perm(np.arange(6, dtype=np.int32), seed, epoch)
+        assert list(got) == order, (epoch, got)
