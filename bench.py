@@ -200,8 +200,23 @@ def time_oracle(w, graph, steps, warmup=0):
 
 
 def oracle_graph(w, inp):
+    if "X_dev" in inp:   # configs[4]: feature rows recomputed by formula (the oracle's formula mode)
+        from gnn_inputs import feature_rows, make_labels
+        return dict(row_ptr=inp["row_ptr"], col=inp["col"], train=inp["train"], params=inp["params"],
+                    X=lambda ids: feature_rows(ids, w.feat_dim, w.graph_seed),
+                    y=make_labels(w.num_nodes, w.num_classes, w.graph_seed))
     return dict(row_ptr=inp["row_ptr"], col=inp["col"], X=inp["X"][:, :w.feat_dim], y=inp["y"],
                 train=inp["train"], params=inp["params"])
+
+
+def load_inputs(w, world, rank, local, host_csr):
+    """Host-built inputs (numpy generator), or for configs[4] (papers100M-shaped: 57 GB of features,
+    1.6B CSR entries) the device generator: this rank's feature rows (row-sharded when world > 1)."""
+    if w.name == "papers100m":
+        from gnn_inputs.device import build_inputs_device
+        return build_inputs_device(w, nshards=world, shard=rank, host_csr=host_csr, device=local)
+    from gnn_inputs import build_inputs
+    return build_inputs(w)
 
 
 def run_reference(args, w, inp, rank, world):
@@ -224,7 +239,12 @@ def run_reference(args, w, inp, rank, world):
 
 
 def config_dict(w, world):
-    return {"workload": f"{w.name} (BASELINE.json configs[1])" if w.name == "products" else w.name,
+    idx = {"tiny": 0, "products": 1, "products_shadow": 2, "reddit": 3, "papers100m": 4}.get(w.name)
+    extra = {}
+    if w.name == "papers100m":
+        extra["feature_table"] = (f"row-sharded over {world} ranks, remote rows by NVLink peer loads" if world > 1
+                                  else "whole table on the GPU (57 GB), device-generated")
+    return {**extra, "workload": f"{w.name} (BASELINE.json configs[{idx}])" if idx is not None else w.name,
             "nodes": w.num_nodes, "nnz_target": w.nnz, "feat_dim": w.feat_dim, "classes": w.num_classes,
             "model": "GraphSAGE-mean" if w.model == "sage" else "GCN", "sampler": w.sampler,
             "fanouts": list(w.fanouts), "layers": w.num_layers, "hidden": w.hidden,
@@ -238,13 +258,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    from gnn_inputs import WORKLOADS, build_inputs
+    from gnn_inputs import WORKLOADS
     w = WORKLOADS[args.config]
-    inp = build_inputs(w)
-
     if args.impl == "reference":
-        run_reference(args, w, inp, rank, world)
+        if rank == 0:
+            run_reference(args, w, load_inputs(w, 1, 0, local, True), rank, world)
         return
+    inp = load_inputs(w, world, rank, local, host_csr=(world == 1 and not args.no_cpu_baseline))
 
     import torch
     import torch.distributed as dist
@@ -253,7 +273,16 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2403_17092_b200 import Graph, Model, comm_get_unique_id
 
-    g = Graph(inp["row_ptr"], inp["col"], inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim, device=local)
+    if "X_dev" in inp:   # configs[4]: borrowed device buffers; row-sharded over the ranks when world > 1
+        from paper_2403_17092_b200 import DeviceGraph
+        g = DeviceGraph(w.num_nodes, inp["row_ptr_dev"], inp["col_dev"], inp["X_dev"], inp["y_dev"], w.num_classes,
+                        w.feat_dim, w.feat_stride, nshards=world, shard=rank, device=local)
+        if world > 1:   # NVLink peer gathers: every rank maps the others' feature blocks (CUDA IPC)
+            handles = [None] * world
+            dist.all_gather_object(handles, g.export_handle())
+            g.import_handles(handles)
+    else:
+        g = Graph(inp["row_ptr"], inp["col"], inp["X"], inp["y"], w.num_classes, feat_dim=w.feat_dim, device=local)
     m = Model(g, model=w.model, sampler=w.sampler, num_layers=w.num_layers, hidden=w.hidden,
               batch_size=w.batch_size, fanouts=w.fanouts, precision=args.precision,
               use_graph=not args.no_graph, lr=w.lr, seed=w.sampler_seed, init_seed=w.init_seed,
@@ -356,6 +385,7 @@ def main():
         h2d += 4 * n
     e1.record(stream)
     barrier()
+    reuse = m.prefetch_reuse()
     ms_e2e = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms_e2e], device="cuda")
@@ -477,7 +507,8 @@ def main():
             "epoch_time": epochs,
             "e2e": {"value": e2e_value, "unit": "mini-batches/s", "h2d_bytes_per_step": h2d // len(batches),
                     "d2h_bytes_per_step": 4,
-                    "api": "gnn_train_batch_host (host seeds -> pinned staging -> device, step, loss -> host; synchronous; next batch prefetched)"},
+                    "api": "gnn_train_batch_host (host seeds -> pinned staging -> device, step, loss -> host; synchronous; next batch prefetched)",
+                    "prefetch_reuse_since_create": {"hits": reuse[0], "misses": reuse[1]}},
             "gpu_launches": int(m.launches_per_step * args.steps),
             "launches_per_step": m.launches_per_step,
             "roofline": roof,

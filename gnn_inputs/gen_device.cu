@@ -269,3 +269,14 @@ int gen_labels(int64_t n, int C, uint64_t seed, int32_t* y) {
 void gen_free(void* p) { cudaFree(p); }
 
 }  // extern "C"
+
+extern "C" {
+void* gen_alloc(int64_t bytes) {
+    void* p = nullptr;
+    return cudaMalloc(&p, (size_t)bytes) == cudaSuccess ? p : nullptr;
+}
+int gen_d2h(void* dst_host, const void* src_dev, int64_t bytes) {
+    return cudaMemcpy(dst_host, src_dev, (size_t)bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -1;
+}
+int gen_set_device(int dev) { return cudaSetDevice(dev) == cudaSuccess ? 0 : -1; }
+}

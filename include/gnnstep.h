@@ -92,6 +92,19 @@ gnn_status gnn_graph_create_sharded(int64_t num_nodes, const int64_t* row_ptr_ho
                                     int32_t nshards, int32_t shard, const float* shard_features_host,
                                     const int32_t* labels_host, int32_t num_classes, int32_t device,
                                     gnn_graph** out);
+/* The same graph from DEVICE memory of `device`, borrowed (not copied): for tables too large to
+ * stage through host memory (configs[4]: 111M x 128 fp32 features = 57 GB, 1.6B CSR entries).
+ * The library references row_ptr_dev, col_idx_dev, features_dev (this process's feature block:
+ * all N rows if nshards == 1, else block `shard` as in gnn_graph_create_sharded) and labels_dev;
+ * they must stay valid and unchanged until gnn_graph_destroy, which does not free them.
+ * Columns >= feat_dim of the feature rows must be 0.  The CSR and labels are validated on the
+ * device (SHAPE / RANGE as gnn_graph_create).  With nshards > 1, features_dev must be the start
+ * of its own cudaMalloc allocation (it is exported by CUDA IPC): else PARAM.  PARAM if a pointer
+ * is not device memory of `device`. */
+gnn_status gnn_graph_create_device(int64_t num_nodes, const int64_t* row_ptr_dev, const int32_t* col_idx_dev,
+                                   int32_t feat_dim, int32_t feat_stride, int32_t nshards, int32_t shard,
+                                   const float* features_dev, const int32_t* labels_dev, int32_t num_classes,
+                                   int32_t device, gnn_graph** out);
 gnn_status gnn_shard_export(gnn_graph* g, uint8_t handle_out_host[64]);
 gnn_status gnn_shard_import(gnn_graph* g, const uint8_t* handles_host);
 /* NEXT-2: GPU feature cache (§3.3), re-aimed at the
@@ -199,13 +212,30 @@ gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_
 /* How a step exchanges its gradient (§2.2, synchronous SGD):
  *   GNN_EXCH_AUTO (default): world 1 -> the fixed-order reduce of the weight-gradient partials
  *     fused into the update kernel; world > 1 -> as GNN_EXCH_NCCL.
- *   GNN_EXCH_NCCL: reduce kernel -> ncclAllReduce(sum, fp32) of the flat gradient -> update
- *     kernel, all captured in the step's CUDA graph; on world 1 the library builds a one-rank
+ *   GNN_EXCH_NCCL: per layer, as soon as its weight gradient is ready: reduce kernel ->
+ *     ncclAllReduce(sum, fp32) of that layer's bucket, on a side stream overlapping the backward of
+ *     the layers below; then the update kernel; all captured in the step's CUDA graph; on world 1
+ *     the library builds a one-rank
  *     communicator (the multi-rank branch, verifiable on one GPU: results are bit-identical to
  *     AUTO, since a one-rank all-reduce is a copy and both reduce in the same fixed order).
  * Synchronizes; the next step recaptures.  PARAM for an unknown mode. */
-enum { GNN_EXCH_AUTO = 0, GNN_EXCH_NCCL = 1 };
+enum { GNN_EXCH_AUTO = 0, GNN_EXCH_NCCL = 1, GNN_EXCH_PEER = 2 };
 gnn_status gnn_set_exchange(gnn_model* m, int32_t mode);
+/* GNN_EXCH_PEER: a deterministic one-shot all-reduce over peer memory, fused with the update and
+ * independent of NCCL.  Each rank owns an inbox [2 (step parity)][world][param_count] fp32 and a
+ * flag array [world] u64 in one device allocation; gnn_exchange_export(rank, world) allocates it,
+ * sets this model's rank/world (the batch -> rank rule of gnn_plan_step) and writes its CUDA IPC
+ * handle (64 bytes); after the caller exchanged the handles (e.g. torch.distributed
+ * all_gather), gnn_exchange_import(handles = world x 64 bytes, in rank order) maps every peer's
+ * region.  Then gnn_set_exchange(GNN_EXCH_PEER): in every step, as soon as layer l's weight
+ * gradient is reduced, rank r stores it into slot r of every rank's inbox (NVLink stores), while
+ * the backward of the layers below runs; the last bucket publishes the step's sequence number in
+ * every rank's flag array; the update kernel waits for all flags, sums the slots in rank order
+ * (identical bits on every rank, summation order independent of arrival) and applies SGD/Adam.
+ * Every rank must run the same sequence of steps (an absent rank stalls the others).  PARAM for
+ * bad arguments or a world different from an NCCL communicator's; STATE out of order. */
+gnn_status gnn_exchange_export(gnn_model* m, int32_t rank, int32_t world, uint8_t handle_out_host[64]);
+gnn_status gnn_exchange_import(gnn_model* m, const uint8_t* handles_host);
 
 /* The epoch's seed order (§2.2; SPEC.md partition_seeds lines 107-115):
  * train ids sorted by (Philox key64(id, epoch), id) (R7); batch g is
@@ -266,7 +296,11 @@ gnn_status gnn_synchronize(gnn_model* m);
  * all-reduce, before SGD), GNN_DBG_LOSS (1 value: this rank's loss), GNN_DBG_ACT + l
  * (layer l's output H^(l) of the last step, 0-based l, rows x out, fp32; its sign pattern
  * is the ReLU decision the backward pass used).  BUFFER if n is too small. */
-enum { GNN_DBG_LOGITS = 0, GNN_DBG_GRADS = 1, GNN_DBG_LOSS = 2, GNN_DBG_PHASES = 8, GNN_DBG_ACT = 16 };
+enum { GNN_DBG_LOGITS = 0, GNN_DBG_GRADS = 1, GNN_DBG_LOSS = 2, GNN_DBG_PHASES = 8, GNN_DBG_REUSE = 9,
+       GNN_DBG_ACT = 16 };
+/* GNN_DBG_REUSE: 2 values, the training calls (train_minibatch / train_batch_host / train_epoch
+ * steps) whose batch was found already sampled (prefetched while the previous step trained) and
+ * those that had to sample it first, since the model was created. */
 /* GNN_DBG_PHASES: microseconds of each phase (between grid barriers, the last one until the
  * last block ends) of the last sampling-kernel run; BUFFER if n < phases (<= 32). */
 gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n);

@@ -4,6 +4,7 @@ Dense half of the step in float64 numpy (DESIGN.md oracle steps O4-O9), written 
 the plain definitions, in the paper's notation:
 
   O4 gather        X_in = H^0[src ids of the layer-1 block]            (§2.2 l.160)
+                   (H^0 an array, or a function of the row ids: the formula-recompute mode)
   O5 forward       GCN   H^(l) = σ(Â H^(l-1) W^(l))                     (Eq. 1, l.131-137)
                    SAGE  H^(l) = σ(H^(l-1) W_1 + Â H^(l-1) W_2)         (Eq. 2, l.139-142)
                    σ = ReLU for l < L, identity at l = L                (R14)
@@ -153,7 +154,10 @@ def layer_blocks(sample, sampler, num_layers):
 
 def minibatch_grad(Ws, model, blocks, input_ids, X, labels, b, b_total, mask_override=None):
     """One rank's O4-O7: returns (rank loss, list of dW, cache)."""
-    X_in = np.asarray(X, dtype=np.float64)[np.asarray(input_ids, dtype=np.int64)]
+    ids = np.asarray(input_ids, dtype=np.int64)
+    # formula-recompute mode (configs[4]: the 57 GB table is never materialised on the host): X is
+    # a function returning the feature rows of the given ids (gnn_inputs.feature_rows)
+    X_in = np.asarray(X(ids), dtype=np.float64) if callable(X) else np.asarray(X, dtype=np.float64)[ids]
     cache = forward(Ws, model, blocks, X_in)
     Z = cache["H"][-1][:b]
     loss, dZ = cross_entropy(Z, labels, b_total)

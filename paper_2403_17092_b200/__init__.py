@@ -5,6 +5,6 @@ this package is its thin Python binding.  No CPU fallback exists.
 """
 from .gnnstep import (Graph, Model, GnnError, comm_get_unique_id, lib, KERNEL_IDS, plan_step,  # noqa: F401
                       steps_per_epoch, ShardedGraph, shard_rows, plan_balanced,
-                      cache_plan_by_degree)
+                      cache_plan_by_degree, DeviceGraph)
 
 __all__ = ["Graph", "Model", "GnnError", "comm_get_unique_id", "lib", "KERNEL_IDS"]

@@ -200,10 +200,17 @@ struct gnn_model {
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
     int exchange = GNN_EXCH_AUTO;        // gradient exchange (gnn_set_exchange)
+    // GNN_EXCH_PEER: this rank's region {inbox [2][world][pcount] fp32, flags [world] u64}, the
+    // peers' regions (CUDA IPC), device arrays of their addresses, sequence number and counters
+    void* xregion = nullptr;
+    std::vector<void*> xopened;
+    PeerX px{};
+    bool peer_ready = false;
 
     bool bf16x3 = true;                  // fp32 parity mode: 3-term bf16 split GEMMs
     int64_t launches_per_step = 0;
 
+    int64_t reuse_hits = 0, reuse_misses = 0;   // steps that found / did not find their batch prefetched
     bool profiling = false;
     std::vector<ProfPair> pending;
     std::vector<cudaEvent_t> free_events;
@@ -371,6 +378,7 @@ void enqueue_training(gnn_model* m, int set) {
     // them before the update): they run on a forked stream as soon as their dPre is ready,
     // concurrently with the dgrad -> backward-aggregation chain, and join before the update.
     cudaStream_t ws = m->wstream;
+    const bool nccl = uses_nccl(m), peer = m->exchange == GNN_EXCH_PEER;
     for (int li = L - 1; li >= 0; --li) {
         Layer& ly = m->layers[li];
         const int32_t* rows = rows_ptr(m, set, li);
@@ -382,6 +390,18 @@ void enqueue_training(gnn_model* m, int set) {
             launch_gemm_tc(1, m->bf16x3, ly.map_wgrad, rows, ly.k_pad, ly.k_pad, ly.n_pad, 0, ly.wpart, ly.n_pad,
                            ly.n_pad, false, ly.splits, stride, ws);
         });
+        // the exchange of layer li's gradient starts now, while the backward of the layers below
+        // runs on the training stream (per-layer buckets, §4.1: overlap)
+        if (nccl) {
+            K(m, ws, GNN_K_ALLREDUCE, [&] {
+                launch_wgrad_reduce(pack_desc(m), li, li + 1, m->grads, PeerX{}, ws);
+                ncclAllReduce(m->grads + ly.poff, m->grads + ly.poff, (size_t)ly.pcnt, ncclFloat, ncclSum, m->comm, ws);
+            });
+        } else if (peer) {
+            PeerX x = m->px;
+            x.signal = li == 0;   // the last bucket publishes the step
+            K(m, ws, GNN_K_ALLREDUCE, [&] { launch_wgrad_reduce(pack_desc(m), li, li + 1, nullptr, x, ws); });
+        }
         if (li == 0) break;
         // dA = dPre W^T (fp32)
         K(m, s, GNN_K_GEMM_DGRAD, [&] {
@@ -398,13 +418,14 @@ void enqueue_training(gnn_model* m, int set) {
     }
     cudaEventRecord(m->ev_join, ws);
     cudaStreamWaitEvent(s, m->ev_join, 0);
-    if (uses_nccl(m)) {
-        // ---- split-K partials of every layer -> flat gradient (fixed order), exchange, update
-        K(m, s, GNN_K_GEMM_WGRAD, [&] { launch_wgrad_reduce_all(pack_desc(m), m->grads, s); });
-        K(m, s, GNN_K_ALLREDUCE, [&] {
-            ncclAllReduce(m->grads, m->grads, (size_t)m->pcount, ncclFloat, ncclSum, m->comm, s);
-        });
+    if (nccl) {
+        // ---- every layer's bucket is all-reduced: update
         K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, false, m->opt, s); });
+    } else if (peer) {
+        // ---- wait for every rank's gradient, sum the inbox in rank order, update
+        K(m, s, GNN_K_SGD, [&] {
+            launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, false, m->opt, s, m->px);
+        });
     } else {
         // ---- one rank: the reduce of the partials is fused into the update
         K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, true, m->opt, s); });
@@ -595,7 +616,9 @@ gnn_status check_seeds(const gnn_model* m, const int32_t* seeds, int32_t n) {
 int other_set(gnn_model* m) { return m->last < 0 ? 0 : 1 - m->last; }
 
 // Train the batch held by `set` on the model's stream.
-gnn_status train_set(gnn_model* m, int set) {
+// loss_dst (nullable, host or device): the batch's loss is copied there on the training stream
+// before the set is released for resampling (its StepState is reset by the next sampling).
+gnn_status train_set(gnn_model* m, int set, float* loss_dst = nullptr) {
     BatchSet& B = m->bs[set];
     CK(cudaStreamWaitEvent(m->stream, B.sampled, 0));
     if (m->cfg.use_graph && !m->profiling) {
@@ -617,6 +640,7 @@ gnn_status train_set(gnn_model* m, int set) {
         enqueue_training(m, set);
         CK(cudaGetLastError());
     }
+    if (loss_dst) CK(cudaMemcpyAsync(loss_dst, &B.st->loss, sizeof(float), cudaMemcpyDefault, m->stream));
     CK(cudaEventRecord(B.trained, m->stream));
     B.trained_once = true;
     B.valid = false;
@@ -626,18 +650,19 @@ gnn_status train_set(gnn_model* m, int set) {
 
 // One step of the epoch loop: use the prefetched sample if it is this step's batch, prefetch
 // the next step's batch into the other set, train.
-gnn_status step_from_perm(gnn_model* m, int64_t epoch, int64_t step) {
+gnn_status step_from_perm(gnn_model* m, int64_t epoch, int64_t step, float* loss_dst = nullptr) {
     int64_t g, offset;
     int32_t n, b_total;
     TRY(plan_model_step(m, step, &g, &n, &offset, &b_total));
     int cur = find_set(m, epoch, g, n, b_total);
+    ++(cur < 0 ? m->reuse_misses : m->reuse_hits);
     if (cur < 0) {
         cur = other_set(m);
         TRY(issue_sample_step(m, cur, epoch, step));
     }
     // training is enqueued first, the next step's sampling after it: the GPU then never waits
     // for the host between steps (the sampling runs while the host comes back for the next call)
-    TRY(train_set(m, cur));
+    TRY(train_set(m, cur, loss_dst));
     if (m->overlap && !m->profiling && step + 1 < steps_per_epoch(m)) TRY(issue_sample_step(m, 1 - cur, epoch, step + 1));
     return GNN_OK;
 }
@@ -851,6 +876,81 @@ static gnn_status graph_create(int64_t num_nodes, const int64_t* row_ptr_host, c
         if ((s = dalloc(&g->cache_desc, 1, g->owned)) != GNN_OK) return cleanup(s);
         if ((s = dalloc(&g->cache_stats, 3, g->owned)) != GNN_OK) return cleanup(s);
         e = cudaMemset(g->cache_desc, 0, sizeof(FeatCache));
+        if (e == cudaSuccess) e = cudaMemset(g->cache_stats, 0, 3 * sizeof(unsigned long long));
+        if (e != cudaSuccess) return cleanup(fail(GNN_ERR_CUDA, std::string("cache descriptor: ") + cudaGetErrorString(e)));
+    }
+    if (!check_symmetric(g->row_ptr, g->col, num_nodes, &g->symmetric))
+        return cleanup(fail(GNN_ERR_CUDA, "symmetry check failed"));
+    *out = g;
+    return GNN_OK;
+}
+
+// Start address of the allocation holding p (driver entry point; the library links only cudart).
+static bool alloc_base(const void* p, const void** base) {
+    typedef int (*Fn)(unsigned long long*, size_t*, unsigned long long);
+    static Fn fn = [] {
+        void* q = nullptr;
+        cudaDriverEntryPointQueryResult r;
+        cudaGetDriverEntryPoint("cuMemGetAddressRange", &q, cudaEnableDefault, &r);
+        return r == cudaDriverEntryPointSuccess ? (Fn)q : (Fn) nullptr;
+    }();
+    unsigned long long b = 0;
+    size_t sz = 0;
+    if (!fn || fn(&b, &sz, (unsigned long long)(uintptr_t)p) != 0) return false;
+    *base = (const void*)(uintptr_t)b;
+    return true;
+}
+
+gnn_status gnn_graph_create_device(int64_t num_nodes, const int64_t* row_ptr_dev, const int32_t* col_idx_dev,
+                                   int32_t feat_dim, int32_t feat_stride, int32_t nshards, int32_t shard,
+                                   const float* features_dev, const int32_t* labels_dev, int32_t num_classes,
+                                   int32_t device, gnn_graph** out) {
+    Range nvtx_("gnn_graph_create_device");
+    if (!out) return fail(GNN_ERR_PARAM, "out is NULL");
+    *out = nullptr;
+    if (num_nodes <= 0 || num_nodes >= INT32_MAX) return fail(GNN_ERR_PARAM, "num_nodes out of (0, 2^31-1)");
+    if (!row_ptr_dev || !col_idx_dev || !features_dev || !labels_dev) return fail(GNN_ERR_PARAM, "NULL input array");
+    if (feat_dim <= 0 || feat_stride < feat_dim || feat_stride % 4) return fail(GNN_ERR_PARAM, "feat_stride must be >= feat_dim and a multiple of 4");
+    if (num_classes <= 0) return fail(GNN_ERR_PARAM, "num_classes must be > 0");
+    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(GNN_ERR_PARAM, "bad shard index");
+    TRY(set_device(device));
+    for (const void* p : {(const void*)row_ptr_dev, (const void*)col_idx_dev, (const void*)features_dev, (const void*)labels_dev}) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess || a.type != cudaMemoryTypeDevice || a.device != device) {
+            cudaGetLastError();
+            return fail(GNN_ERR_PARAM, "input arrays must be device memory of the graph's device");
+        }
+    }
+    if (nshards > 1) {   // the shard is exported by CUDA IPC, which maps whole allocations
+        const void* b = nullptr;
+        if (!alloc_base(features_dev, &b) || b != (const void*)features_dev)
+            return fail(GNN_ERR_PARAM, "a sharded features_dev must be the start of its cudaMalloc allocation");
+    }
+    const int bad = validate_graph(row_ptr_dev, col_idx_dev, num_nodes, labels_dev, num_classes);
+    if (bad < 0) return fail(GNN_ERR_CUDA, "graph validation kernel failed");
+    if (bad & 1) return fail(GNN_ERR_SHAPE, "row_ptr[0] != 0 or row_ptr not non-decreasing");
+    if (bad & 2) return fail(GNN_ERR_RANGE, "col_idx out of range");
+    if (bad & 4) return fail(GNN_ERR_SHAPE, "a row is not ascending/duplicate-free");
+    if (bad & 8) return fail(GNN_ERR_RANGE, "label out of range");
+    int64_t nnz = 0;
+    CK(cudaMemcpy(&nnz, row_ptr_dev + num_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    auto* g = new gnn_graph();
+    g->dev = device; g->N = num_nodes; g->nnz = nnz; g->F = feat_dim; g->stride = feat_stride; g->C = num_classes;
+    g->rps = (num_nodes + nshards - 1) / nshards;
+    g->row_begin = std::min<int64_t>(num_nodes, (int64_t)shard * g->rps);
+    g->row_end = std::min<int64_t>(num_nodes, g->row_begin + g->rps);
+    g->nshards = nshards > 1 ? nshards : 0;
+    // borrowed: referenced, never freed by the library
+    g->row_ptr = const_cast<int64_t*>(row_ptr_dev);
+    g->col = const_cast<int32_t*>(col_idx_dev);
+    g->X = const_cast<float*>(features_dev);
+    g->y = const_cast<int32_t*>(labels_dev);
+    auto cleanup = [&](gnn_status st) { for (void* p : g->owned) cudaFree(p); delete g; return st; };
+    if (g->nshards) {
+        gnn_status st;
+        if ((st = dalloc(&g->cache_desc, 1, g->owned)) != GNN_OK) return cleanup(st);
+        if ((st = dalloc(&g->cache_stats, 3, g->owned)) != GNN_OK) return cleanup(st);
+        cudaError_t e = cudaMemset(g->cache_desc, 0, sizeof(FeatCache));
         if (e == cudaSuccess) e = cudaMemset(g->cache_stats, 0, 3 * sizeof(unsigned long long));
         if (e != cudaSuccess) return cleanup(fail(GNN_ERR_CUDA, std::string("cache descriptor: ") + cudaGetErrorString(e)));
     }
@@ -1138,6 +1238,8 @@ gnn_status gnn_model_destroy(gnn_model* m) {
         if (B.trained) cudaEventDestroy(B.trained);
     }
     if (m->comm) ncclCommDestroy(m->comm);
+    for (void* p : m->xopened) cudaIpcCloseMemHandle(p);
+    if (m->xregion) cudaFree(m->xregion);
     for (void* p : m->owned) cudaFree(p);
     for (void* p : m->owned_host) cudaFreeHost(p);
     for (void* p : {(void*)m->train_sorted, (void*)m->perm, (void*)m->keys, (void*)m->keys_alt, m->cub_tmp})
@@ -1262,13 +1364,84 @@ gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_
 
 gnn_status gnn_set_exchange(gnn_model* m, int32_t mode) {
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
-    if (mode != GNN_EXCH_AUTO && mode != GNN_EXCH_NCCL) return fail(GNN_ERR_PARAM, "unknown exchange mode");
+    if (mode != GNN_EXCH_AUTO && mode != GNN_EXCH_NCCL && mode != GNN_EXCH_PEER)
+        return fail(GNN_ERR_PARAM, "unknown exchange mode");
+    if (mode == GNN_EXCH_PEER && !m->peer_ready)
+        return fail(GNN_ERR_STATE, "GNN_EXCH_PEER needs gnn_exchange_export + gnn_exchange_import first");
     TRY(set_device(m->g->dev));
     TRY(sync_all(m));
     if (mode != m->exchange) {
         m->exchange = mode;
         drop_graphs(m);   // the captured step holds the previous exchange
     }
+    return GNN_OK;
+}
+
+gnn_status gnn_exchange_export(gnn_model* m, int32_t rank, int32_t world, uint8_t handle_out_host[64]) {
+    if (!m || !handle_out_host || world < 1 || rank < 0 || rank >= world) return fail(GNN_ERR_PARAM, "bad arguments");
+    if (m->comm && m->world != world) return fail(GNN_ERR_PARAM, "world differs from the NCCL communicator's");
+    TRY(set_device(m->g->dev));
+    TRY(sync_all(m));
+    if (m->xregion) return fail(GNN_ERR_STATE, "exchange region already exported");
+    const size_t inbox = sizeof(float) * 2 * (size_t)world * m->pcount;
+    const size_t bytes = inbox + sizeof(unsigned long long) * world;
+    CK(cudaMalloc(&m->xregion, bytes));   // its own allocation: exported whole by CUDA IPC
+    CK(cudaMemset(m->xregion, 0, bytes));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, m->xregion));
+    std::memcpy(handle_out_host, &h, 64);
+    m->rank = rank;
+    m->world = world;
+    drop_graphs(m);
+    for (auto& B : m->bs) B.valid = false;
+    return GNN_OK;
+}
+
+gnn_status gnn_exchange_import(gnn_model* m, const uint8_t* handles_host) {
+    if (!m || !handles_host) return fail(GNN_ERR_PARAM, "NULL argument");
+    if (!m->xregion) return fail(GNN_ERR_STATE, "gnn_exchange_export first");
+    if (m->peer_ready) return fail(GNN_ERR_STATE, "exchange already imported");
+    TRY(set_device(m->g->dev));
+    const int W = m->world;
+    const size_t inbox = sizeof(float) * 2 * (size_t)W * m->pcount;
+    std::vector<float*> ib(W);
+    std::vector<unsigned long long*> fl(W);
+    for (int q = 0; q < W; ++q) {
+        void* p = m->xregion;
+        if (q != m->rank) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, handles_host + 64 * q, 64);
+            CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            m->xopened.push_back(p);
+        }
+        ib[q] = static_cast<float*>(p);
+        fl[q] = reinterpret_cast<unsigned long long*>(static_cast<char*>(p) + inbox);
+    }
+    float** d_ib = nullptr;
+    unsigned long long** d_fl = nullptr;
+    unsigned long long* seq = nullptr;
+    unsigned* done = nullptr;
+    TRY(dalloc(&d_ib, W, m->owned));
+    TRY(dalloc(&d_fl, W, m->owned));
+    TRY(dalloc(&seq, 1, m->owned));
+    TRY(dalloc(&done, 2, m->owned));
+    CK(cudaMemcpy(d_ib, ib.data(), sizeof(float*) * W, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_fl, fl.data(), sizeof(void*) * W, cudaMemcpyHostToDevice));
+    const unsigned long long one = 1;
+    CK(cudaMemcpy(seq, &one, sizeof(one), cudaMemcpyHostToDevice));
+    CK(cudaMemset(done, 0, 2 * sizeof(unsigned)));
+    PeerX& x = m->px;
+    x.inbox = d_ib;
+    x.flags = d_fl;
+    x.my_inbox = ib[m->rank];
+    x.my_flags = fl[m->rank];
+    x.seq = seq;
+    x.world = W;
+    x.rank = m->rank;
+    x.pcount = m->pcount;
+    x.done = done;
+    x.done2 = done + 1;
+    m->peer_ready = true;
     return GNN_OK;
 }
 
@@ -1365,6 +1538,7 @@ gnn_status gnn_train_batch_host(gnn_model* m, const int32_t* seeds_host, int32_t
     TRY(set_device(m->g->dev));
     TRY(check_ready(m));
     int cur = find_set(m, epoch, g, n_seeds, b_total, seeds_host ? seeds_host : m->bs[0].seeds_stage);
+    ++(cur < 0 ? m->reuse_misses : m->reuse_hits);
     if (cur < 0) {
         TRY(check_seeds(m, seeds_host, n_seeds));
         cur = other_set(m);
@@ -1390,21 +1564,21 @@ gnn_status gnn_train_epoch(gnn_model* m, int64_t epoch, gnn_epoch_stats* out_hos
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    float* pinned = nullptr;
-    CK(cudaMallocHost(&pinned, sizeof(float) * std::max<int64_t>(steps, 1)));
+    // per-step losses land in a device array (copied back once, after the timed epoch)
+    float* dloss = nullptr;
+    CK(cudaMalloc(&dloss, sizeof(float) * std::max<int64_t>(steps, 1)));
+    std::vector<float> losses(std::max<int64_t>(steps, 1));
     TRY(sync_all(m));
     CK(cudaEventRecord(e0, m->stream));
-    for (int64_t s = 0; s < steps; ++s) {
-        TRY(step_from_perm(m, epoch, s));
-        CK(cudaMemcpyAsync(pinned + s, &m->bs[m->last].st->loss, sizeof(float), cudaMemcpyDeviceToHost, m->stream));
-    }
+    for (int64_t s = 0; s < steps; ++s) TRY(step_from_perm(m, epoch, s, dloss + s));
     CK(cudaEventRecord(e1, m->stream));
     CK(cudaEventSynchronize(e1));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     double tot = 0;
-    for (int64_t s = 0; s < steps; ++s) tot += pinned[s];
-    cudaFreeHost(pinned);
+    CK(cudaMemcpy(losses.data(), dloss, sizeof(float) * steps, cudaMemcpyDeviceToHost));
+    cudaFree(dloss);
+    for (int64_t s = 0; s < steps; ++s) tot += losses[s];
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (out_host) {
@@ -1447,6 +1621,12 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
         if (need)
             CK(cudaMemcpy2D(out_host, sizeof(float) * ly.out, ly.H, sizeof(float) * ly.n_pad, sizeof(float) * ly.out,
                             st.batch_n, cudaMemcpyDeviceToHost));
+        return GNN_OK;
+    }
+    if (what == GNN_DBG_REUSE) {   // steps whose batch was / was not found prefetched (since creation)
+        if (n < 2) return fail(GNN_ERR_BUFFER, "need 2");
+        out_host[0] = (float)m->reuse_hits;
+        out_host[1] = (float)m->reuse_misses;
         return GNN_OK;
     }
     if (what == GNN_DBG_PHASES) {   // sampling-kernel phase durations of the last sampling run (us)

@@ -53,6 +53,22 @@ __device__ __forceinline__ void store_split4(const Split& o, int64_t idx, float4
         *reinterpret_cast<uint2*>(o.lo + idx) = make_uint2(pack2(l0, l1), pack2(l2, l3));
     }
 }
+// store_split4 with an L2 eviction policy on the stores (createpolicy)
+__device__ __forceinline__ void st_v2_hint(void* p, uint32_t a, uint32_t b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void store_split4_pol(const Split& o, int64_t idx, float4 v, uint64_t pol) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(v.x), h1 = __float2bfloat16_rn(v.y);
+    const __nv_bfloat16 h2 = __float2bfloat16_rn(v.z), h3 = __float2bfloat16_rn(v.w);
+    st_v2_hint(o.hi + idx, pack2(h0, h1), pack2(h2, h3), pol);
+    if (o.lo) {
+        const __nv_bfloat16 l0 = __float2bfloat16_rn(v.x - __bfloat162float(h0));
+        const __nv_bfloat16 l1 = __float2bfloat16_rn(v.y - __bfloat162float(h1));
+        const __nv_bfloat16 l2 = __float2bfloat16_rn(v.z - __bfloat162float(h2));
+        const __nv_bfloat16 l3 = __float2bfloat16_rn(v.w - __bfloat162float(h3));
+        st_v2_hint(o.lo + idx, pack2(l0, l1), pack2(l2, l3), pol);
+    }
+}
 __device__ __forceinline__ void store_split1(const Split& o, int64_t idx, float v) {
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
     o.hi[idx] = h;
@@ -179,7 +195,8 @@ constexpr int kL1Warps = 4;   // warps per block
 template <int NB>
 __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __restrict__ rows_ptr,
         const float* __restrict__ X, int in_pad, const int32_t* __restrict__ smap,
-        const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col, Split A, int fixed_k, int slots) {
+        const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col, Split A, int fixed_k, int slots,
+        int xpol, int apol) {
     extern __shared__ __align__(128) unsigned char l1_smem[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     uint64_t* bar = reinterpret_cast<uint64_t*>(l1_smem) + warp * NB;
@@ -201,37 +218,52 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
     // zero tail rows [n, round64(n)) of the operand planes
     for (int64_t i = n + gw; i < round64(n); i += W)
         for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, tix(A, i, 4 * ch), kZero4);
-    const uint64_t pol = policy_evict_normal();
-    int cnt[NB];
-    // arm buffer b with destination row i: self row -> slot 0, neighbour j -> slot 1 + j
-    auto issue = [&](int b, int64_t i) {
-        int beg, c;
-        int nb = 0;
+    // L2 policies (A/B switches GS_L1_XPOL / GS_L1_APOL): feature rows 0 normal, 1 evict_last,
+    // 2 evict_first; operand-plane stores 0 plain, 1 evict_first, 2 evict_last
+    const uint64_t pol = xpol == 1 ? policy_evict_last() : xpol == 2 ? policy_evict_first() : policy_evict_normal();
+    const uint64_t spol = apol == 2 ? policy_evict_last() : policy_evict_first();
+    // A destination row's indices: this lane's row to copy (lane 0: the self row, lane j: the
+    // neighbour j-1) and the row's degree.  Fetched one row ahead of their use, so the index loads
+    // overlap the wait for the rows in flight instead of stalling the copy issue.
+    struct Idx { int nb, self, c; };
+    auto fetch = [&](int64_t i) {
+        Idx x{0, 0, 0};
+        if (i >= n) return x;
         if (fixed_k) {   // fixed-stride rows: the count and the ids load in parallel
-            beg = (int)i * fixed_k;
-            if (lane < fixed_k) nb = col[beg + lane];
-            c = rowptr[i];
+            if (lane < fixed_k) x.nb = col[(int)i * fixed_k + lane];
+            x.c = rowptr[i];
         } else {
-            beg = rowptr[i];
-            c = rowptr[i + 1] - beg;
-            if (lane < c) nb = col[beg + lane];
+            const int beg = rowptr[i];
+            x.c = rowptr[i + 1] - beg;
+            if (lane < x.c) x.nb = col[beg + lane];
         }
-        const int self = smap[i];
+        x.self = smap[i];
+        return x;
+    };
+    // arm buffer b with a row: self row -> slot 0, neighbour j -> slot 1 + j
+    auto issue = [&](int b, const Idx& x) {
         float* buf = ring + (size_t)b * slots * in_pad;
-        if (lane == 0) mbar_expect_tx(&bar[b], (uint32_t)(c + 1) * row_bytes);
+        if (lane == 0) mbar_expect_tx(&bar[b], (uint32_t)(x.c + 1) * row_bytes);
         __syncwarp();
-        const int src = __shfl_up_sync(0xffffffffu, nb, 1);   // lane j (>= 1) takes neighbour j-1
-        if (lane <= c) {
-            const int r = lane == 0 ? self : src;
+        const int src = __shfl_up_sync(0xffffffffu, x.nb, 1);   // lane j (>= 1) takes neighbour j-1
+        if (lane <= x.c) {
+            const int r = lane == 0 ? x.self : src;
             bulk_g2s(buf + (size_t)lane * in_pad, X + (int64_t)r * in_pad, row_bytes, &bar[b], pol);
         }
-        return c;
     };
+    int cnt[NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) cnt[b] = gw + b * W < n ? issue(b, gw + b * W) : 0;
+    for (int b = 0; b < NB; ++b) {
+        const int64_t i = gw + b * W;
+        const Idx x = fetch(i);
+        cnt[b] = x.c;
+        if (i < n) issue(b, x);
+    }
+    Idx pend = fetch(gw + (int64_t)NB * W);   // the row that re-arms the first freed buffer
     uint32_t phase = 0;   // parity bit of every buffer's current use (buffers are used round-robin)
     int b = 0;
     for (int64_t i = gw; i < n; i += W) {
+        const Idx nxt = fetch(i + (int64_t)(NB + 1) * W);   // loads in flight during this row
         mbar_wait(&bar[b], phase);
         const float* buf = ring + (size_t)b * slots * in_pad;
         int c = cnt[0];
@@ -253,18 +285,30 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
         // generic-proxy reads of the same shared memory need the proxy fence)
         fence_async_smem();
         __syncwarp();
-        const int64_t inext = i + (int64_t)NB * W;
-        const int cn = inext < n ? issue(b, inext) : 0;
+        const bool more = i + (int64_t)NB * W < n;
+        if (more) issue(b, pend);
 #pragma unroll
-        for (int q = 0; q < NB; ++q) if (b == q) cnt[q] = cn;
+        for (int q = 0; q < NB; ++q) if (b == q) cnt[q] = more ? pend.c : 0;
+        pend = nxt;
         const float inv = c ? 1.0f / (float)c : 0.f;   // one division per row (R23)
-        if (lane < nch) {
-            store_split4(A, tix(A, i, 4 * lane), sv);
-            store_split4(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv));
-        }
-        if (wide && lane + 32 < nch) {
-            store_split4(A, tix(A, i, 4 * (lane + 32)), sv2);
-            store_split4(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv));
+        if (apol) {
+            if (lane < nch) {
+                store_split4_pol(A, tix(A, i, 4 * lane), sv, spol);
+                store_split4_pol(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv), spol);
+            }
+            if (wide && lane + 32 < nch) {
+                store_split4_pol(A, tix(A, i, 4 * (lane + 32)), sv2, spol);
+                store_split4_pol(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv), spol);
+            }
+        } else {
+            if (lane < nch) {
+                store_split4(A, tix(A, i, 4 * lane), sv);
+                store_split4(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv));
+            }
+            if (wide && lane + 32 < nch) {
+                store_split4(A, tix(A, i, 4 * (lane + 32)), sv2);
+                store_split4(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv));
+            }
         }
         if (++b == NB) { b = 0; phase ^= 1u; }
     }
@@ -710,15 +754,27 @@ __global__ void __launch_bounds__(256) k_rf_mark(const int32_t* __restrict__ nse
 }
 
 // ------------------------------------------------------------------ weights, reduce, SGD
-// dW of every layer in one launch: grads[off_l + r*out + c] = Σ_z part_l[z][rpad(r)*n_pad + c]
-// (split order fixed: deterministic).
-__global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
+// dW of layers [l0, l1) in one launch: G[off_l + r*out + c] = Σ_z part_l[z][rpad(r)*n_pad + c]
+// (split order fixed: deterministic), stored to `grads` (when non-null) and, for the peer exchange
+// (x.world > 0), to slot `rank` of every rank's inbox (NVLink stores to CUDA-IPC mappings).  With
+// x.signal the last block then publishes the step's sequence number in every rank's flag array.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__global__ void k_wgrad_reduce(PackAll P, int l0, int l1, float* __restrict__ grads, PeerX x) {
     pdl_trigger();
     pdl_wait();
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const unsigned long long seq = x.world ? *x.seq : 0ull;
+    const int64_t slot = x.world ? ((int64_t)(seq & 1ull) * x.world + x.rank) * x.pcount : 0;
     int64_t base = 0;   // the layers' entries form one index space: one pass of the grid in all
-    for (int l = 0; l < P.n; ++l) {
+    for (int l = l0; l < l1; ++l) {
         const PackLayer& L = P.l[l];
         const int64_t total = (int64_t)L.rows * L.out;
         const int64_t g0 = base > tid ? tid + ((base - tid + nth - 1) / nth) * nth : tid;
@@ -735,8 +791,21 @@ __global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) if (z0 + j < L.splits) s += v[j];
             }
-            grads[L.poff + f] = s;
+            if (grads) grads[L.poff + f] = s;
+            for (int q = 0; q < x.world; ++q) x.inbox[q][slot + L.poff + f] = s;
         }
+    }
+    if (!x.world) return;
+    __threadfence_system();   // this thread's peer stores before anything it does next
+    if (!x.signal) return;
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(x.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence_system();
+        for (int q = 0; q < x.world; ++q) st_release_sys(x.flags[q] + x.rank, seq);
+        *x.done = 0u;
     }
 }
 
@@ -748,12 +817,33 @@ __global__ void k_wgrad_reduce_all(PackAll P, float* __restrict__ grads) {
 // partials in the fixed split order (the arithmetic of k_wgrad_reduce_all) and stored.
 // Adam: t = *o.t + 1 for every thread; bias corrections in fp64; the last block to finish
 // stores t (the next step's kernel starts after this one completes).
+// Peer exchange (x.world > 0): every block first waits until each rank r has published this step's
+// sequence number in this rank's flag array, then G = Σ_{r = 0..world-1} inbox[r] (rank order: the
+// same bits on every rank); the last block advances the sequence number.
 __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restrict__ grads, float lr, int reduce,
-                           OptState o) {
+                           OptState o, PeerX x) {
     pdl_trigger();
     pdl_wait();
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long seq = 0;
+    const float* inbox = nullptr;
+    if (x.world && grads) {
+        seq = *x.seq;
+        if (threadIdx.x < x.world) {
+            // a rank that never arrives (crashed peer, mismatched step sequence) aborts the kernel
+            // after 30 s instead of hanging the device
+            unsigned long long t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (ld_acquire_sys(x.my_flags + threadIdx.x) < seq) {
+                __nanosleep(256);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 30000000000ull) __trap();
+            }
+        }
+        __syncthreads();
+        inbox = x.my_inbox + (int64_t)(seq & 1ull) * x.world * x.pcount;
+    }
     const bool adam = o.m != nullptr && grads != nullptr;
     int t = 0;
     float step = 0.f, inv_sqrt_bc2 = 0.f;
@@ -789,6 +879,10 @@ __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restr
                         for (int j = 0; j < 8; ++j) if (z0 + j < L.splits) gr += v[j];
                     }
                     grads[idx] = gr;
+                } else if (inbox) {   // the peers' gradients, summed in rank order
+                    gr = 0.f;
+                    for (int q = 0; q < x.world; ++q) gr += __ldcv(inbox + (int64_t)q * x.pcount + idx);
+                    grads[idx] = gr;
                 } else {
                     gr = grads[idx];
                 }
@@ -806,12 +900,17 @@ __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restr
             store_split1(L.Wkn, f, w);
         }
     }
-    if (adam) {
+    if (adam || inbox) {
         __shared__ bool last;
         __syncthreads();
-        if (threadIdx.x == 0) last = atomicAdd(o.done, 1u) == gridDim.x - 1;
+        unsigned* done = adam ? o.done : x.done2;
+        if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
         __syncthreads();
-        if (last && threadIdx.x == 0) { *o.t = t; *o.done = 0u; }
+        if (last && threadIdx.x == 0) {
+            if (adam) *o.t = t;
+            if (inbox) *x.seq = seq + 1;
+            *done = 0u;
+        }
     }
 }
 
@@ -893,8 +992,12 @@ template <int NB>
 static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, const int32_t* smap,
                            const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k, int slots,
                            cudaStream_t s) {
-    const size_t smem = 128 + (size_t)kL1Warps * NB * slots * in_pad * 4;
+    size_t smem = 128 + (size_t)kL1Warps * NB * slots * in_pad * 4;
     if (smem > 200 * 1024) return false;
+    // GS_L1_BPS = b: pad the request just past the (b+1)-blocks threshold, so that at most b blocks
+    // share an SM and the rest of its shared memory stays free for a co-resident sampling block
+    static const int bps = [] { const char* e = std::getenv("GS_L1_BPS"); return e ? std::atoi(e) : 3; }();
+    if (bps > 0) smem = std::max(smem, (size_t)(233472 / (bps + 1) - 1024 + 16));
     static std::map<size_t, int> grids;   // smem bytes -> co-resident blocks x SMs (occupancy-derived)
     int& grid = grids[smem];
     if (!grid) {
@@ -906,8 +1009,15 @@ static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, 
         if (per_sm < 1) return false;
         grid = per_sm * sms;
     }
-    launch_pdl(k_agg_l1_bulk<NB>, grid, kL1Warps * 32, smem, s, rows_ptr, X, in_pad, smap, blk_rowptr, col, A,
-               fixed_k, slots);
+    static const int xpol = [] { const char* e = std::getenv("GS_L1_XPOL"); return e ? std::atoi(e) : 0; }();
+    static const int apol = [] { const char* e = std::getenv("GS_L1_APOL"); return e ? std::atoi(e) : 0; }();
+    static const int pdl = [] { const char* e = std::getenv("GS_L1_PDL"); return e ? std::atoi(e) : 1; }();
+    if (pdl)
+        launch_pdl(k_agg_l1_bulk<NB>, grid, kL1Warps * 32, smem, s, rows_ptr, X, in_pad, smap, blk_rowptr, col, A,
+                   fixed_k, slots, xpol, apol);
+    else
+        k_agg_l1_bulk<NB><<<grid, kL1Warps * 32, smem, s>>>(rows_ptr, X, in_pad, smap, blk_rowptr, col, A, fixed_k,
+                                                           slots, xpol, apol);
     return true;
 }
 
@@ -924,6 +1034,16 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
                                 : launch_l1_bulk<2>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
                                                      1 + k_max, s);
         if (ok) return;
+    }
+    // A/B diagnostic only: GS_AGG_DUMMY_SMEM = bytes of (unused) dynamic shared memory for the
+    // register-load layer-1 gather (does a shared-memory footprint alone change the step?)
+    static const int dummy = [] { const char* e = std::getenv("GS_AGG_DUMMY_SMEM"); return e ? std::atoi(e) : 0; }();
+    if (dummy && k_max > 0 && !gmap && cpl_of(in_pad) == 1) {
+        static bool set = false;
+        if (!set) { cudaFuncSetAttribute(k_agg_sage<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, dummy); set = true; }
+        launch_pdl(k_agg_sage<1>, kWarpGrid, 256, (size_t)dummy, s, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A,
+                   fixed_k);
+        return;
     }
     GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A, fixed_k);
 }
@@ -979,13 +1099,13 @@ void launch_rf_mark(const int32_t* nseed_ptr, const int32_t* rowptr, const int32
     launch_pdl(k_rf_mark, 148 * 4, 256, 0, s, nseed_ptr, rowptr, col, tag_ptr, mask);
 }
 
-void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s) {
-    launch_pdl(k_wgrad_reduce_all, 148 * 4, 256, 0, s, p, grads);
+void launch_wgrad_reduce(const PackAll& p, int l0, int l1, float* grads, const PeerX& x, cudaStream_t s) {
+    launch_pdl(k_wgrad_reduce, 148 * 4, 256, 0, s, p, l0, l1, grads, x);
 }
 
 void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, const OptState& o,
-                     cudaStream_t s) {
-    launch_pdl(k_sgd_pack, reduce ? 148 * 8 : 148 * 2, 256, 0, s, p, params, grads, lr, reduce ? 1 : 0, o);
+                     cudaStream_t s, const PeerX& x) {
+    launch_pdl(k_sgd_pack, reduce ? 148 * 8 : 148 * 2, 256, 0, s, p, params, grads, lr, reduce ? 1 : 0, o, x);
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,

@@ -46,6 +46,9 @@ constexpr int kWarpGrid = 148 * GS_WARP_GRID_PER_SM;   // blocks of 256 threads 
 void launch_perm_keys(const int32_t* train, int64_t n, uint64_t seed, int64_t epoch,
                       uint64_t* keys, cudaStream_t s);
 
+// Device-side validation of a CSR + labels (synchronous): 0 if valid, else the bit set of
+// k_validate (1 row_ptr, 2 column range, 4 row order, 8 label range), -1 on a CUDA error.
+int validate_graph(const int64_t* row_ptr, const int32_t* col, int64_t n, const int32_t* y, int C);
 // Whether every CSR entry (v -> u) has its reverse (u -> v); synchronous (graph creation).
 bool check_symmetric(const int64_t* row_ptr, const int32_t* col, int64_t n, bool* symmetric);
 
@@ -198,16 +201,34 @@ struct PackLayer {
     int64_t split_stride;
 };
 struct PackAll { PackLayer l[kMaxHops]; int n; bool sage; };
-// grads[poff + r*out + c] = Σ_z part[z][rpad(r)*n_pad + c] for every layer, fixed z order.
-void launch_wgrad_reduce_all(const PackAll& p, float* grads, cudaStream_t s);
+// Deterministic one-shot all-reduce over peer memory (GNN_EXCH_PEER): rank r stores its gradient
+// into slot r of every rank's inbox [2 (step parity)][world][pcount] (CUDA-IPC mappings, NVLink
+// stores), publishes the step's sequence number in every rank's flag array, and every rank sums
+// the world slots of its own inbox in rank order inside the update.  world == 0: not used.
+struct PeerX {
+    float* const* inbox;              // [world] inbox bases of every rank (device array of peer pointers)
+    unsigned long long* const* flags; // [world] flag arrays of every rank ([world] u64 each)
+    const float* my_inbox;            // this rank's inbox
+    const unsigned long long* my_flags;
+    unsigned long long* seq;          // this rank's step sequence number (starts at 1)
+    int world, rank, signal;
+    int64_t pcount;
+    unsigned* done;                   // block counters (zero between launches)
+    unsigned* done2;
+};
+// G[poff + r*out + c] = Σ_z part[z][rpad(r)*n_pad + c] for layers [l0, l1), fixed z order, into
+// grads (nullable) and, with x.world, into every rank's inbox (x.signal: then publish the step).
+void launch_wgrad_reduce(const PackAll& p, int l0, int l1, float* grads, const PeerX& x, cudaStream_t s);
 // Optimizer state: m == nullptr -> SGD; else Adam with moments m, v (flat like params), the
 // device step count *t (steps applied so far) and a block counter (zero between launches).
 struct OptState { float* m; float* v; int32_t* t; unsigned* done; float beta1, beta2, eps; };
 // W <- W - lr*G (SGD) or the Adam update (grads may be nullptr: pack only) and the bf16 planes
 // of W, all layers.  reduce: G = the fixed-order sum of the wgrad partials, written to grads
 // first (one rank).
+// x.world > 0 (peer exchange): G = the rank-order sum of this rank's inbox, after waiting for
+// every rank's flag (written to grads, then the update).
 void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, const OptState& o,
-                     cudaStream_t s);
+                     cudaStream_t s, const PeerX& x = PeerX{});
 // Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total
 // written as split planes [rows x ldz] (+ zero tail rows).
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels,

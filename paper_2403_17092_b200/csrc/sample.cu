@@ -36,6 +36,31 @@ __global__ void k_check_symmetric(const int64_t* __restrict__ row_ptr, const int
     }
 }
 
+// Validation of a graph given in device memory (gnn_graph_create_device): bad[0] |= 1 row_ptr not
+// non-decreasing or row_ptr[0] != 0, 2 a column id out of [0, n), 4 a row not strictly
+// ascending (duplicate or unsorted), 8 a label out of [0, C).
+__global__ void k_validate(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, int64_t n,
+                           const int32_t* __restrict__ y, int C, int* __restrict__ bad) {
+    int f = 0;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    if (tid == 0 && row_ptr[0] != 0) f |= 1;
+    for (int64_t v = tid; v < n; v += nth) {
+        const int64_t rb = row_ptr[v], re = row_ptr[v + 1];
+        if (re < rb) { f |= 1; continue; }
+        if (y[v] < 0 || y[v] >= C) f |= 8;
+    }
+    const int64_t nnz = row_ptr[n];
+    for (int64_t v = tid; v < n; v += nth) {   // rows: each entry vs its predecessor in the row
+        const int64_t rb = row_ptr[v], re = row_ptr[v + 1];
+        for (int64_t p = rb; p < re && p < nnz; ++p) {
+            const int c = col[p];
+            if (c < 0 || c >= n) f |= 2;
+            if (p > rb && c <= col[p - 1]) f |= 4;
+        }
+    }
+    if (f) atomicOr(bad, f);
+}
+
 // NEXT-2 cache fill: a warp per cached row, 16-byte chunks (the row read like the aggregation reads it).
 __global__ void k_cache_fill(FeatRows src, const int32_t* __restrict__ ids, int64_t n, int ld, float* __restrict__ out) {
     const int lane = threadIdx.x & 31;
@@ -54,6 +79,20 @@ __global__ void k_cache_fill(FeatRows src, const int32_t* __restrict__ ids, int6
 void launch_cache_fill(FeatRows src, const int32_t* ids, int64_t n, int ld, float* out, cudaStream_t s) {
     if (n <= 0) return;
     k_cache_fill<<<148 * 8, 256, 0, s>>>(src, ids, n, ld, out);
+}
+
+int validate_graph(const int64_t* row_ptr, const int32_t* col, int64_t n, const int32_t* y, int C) {
+    int* d = nullptr;
+    if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return -1;
+    int h = 0;
+    bool ok = cudaMemset(d, 0, sizeof(int)) == cudaSuccess;
+    if (ok) {
+        k_validate<<<148 * 16, 256>>>(row_ptr, col, n, y, C, d);
+        ok = cudaGetLastError() == cudaSuccess;
+    }
+    ok = ok && cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d);
+    return ok ? h : -1;
 }
 
 bool check_symmetric(const int64_t* row_ptr, const int32_t* col, int64_t n, bool* symmetric) {

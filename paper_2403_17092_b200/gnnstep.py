@@ -16,7 +16,7 @@ GNN_FP32, GNN_BF16_GEMM = 0, 1
 GNN_SRC_IDS, GNN_BLK_ROWPTR, GNN_BLK_COL, GNN_BLK_NBR = 0, 1, 2, 3
 GNN_DBG_LOGITS, GNN_DBG_GRADS, GNN_DBG_LOSS, GNN_DBG_ACT = 0, 1, 2, 16
 GNN_SGD, GNN_ADAM = 0, 1
-GNN_EXCH_AUTO, GNN_EXCH_NCCL = 0, 1
+GNN_EXCH_AUTO, GNN_EXCH_NCCL, GNN_EXCH_PEER = 0, 1, 2
 ABI_VERSION = 2   # include/gnnstep.h GNN_ABI_VERSION
 KERNEL_IDS = dict(sample=0, relabel=1, agg_l1=2, agg=3, gemm_fwd=4, gemm_dgrad=5, gemm_wgrad=6,
                   spmm_bwd=7, ce=8, sgd=9, transpose=10, induce=11, allreduce=12, scan=13, other=14)
@@ -81,7 +81,8 @@ def lib():
             "gnn_graph_symmetric": ([P], I32),
             "gnn_estimate_workload": ([P, I64, P, I64], I32), "gnn_plan_balanced": ([P, I64, I32, P], I32),
             "gnn_set_schedule": ([P, P, I64], I32), "gnn_set_exchange": ([P, I32], I32),
-            "gnn_cache_stats": ([P, I32, P], I32),
+            "gnn_cache_stats": ([P, I32, P], I32), "gnn_exchange_export": ([P, I32, I32, P], I32),
+            "gnn_exchange_import": ([P, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(_lib, name)
@@ -210,9 +211,24 @@ class Model:
         _check(lib().gnn_set_params(self.h, _ptr(p), p.shape[0]))
 
     def set_exchange(self, mode: str):
-        """gnn_set_exchange: "auto" (world 1: reduce fused into the update) or "nccl" (reduce ->
-        ncclAllReduce -> update, on any world; world 1 uses a one-rank communicator)."""
-        _check(lib().gnn_set_exchange(self.h, {"auto": GNN_EXCH_AUTO, "nccl": GNN_EXCH_NCCL}[mode]))
+        """gnn_set_exchange: "auto" (world 1: reduce fused into the update), "nccl" (per-layer
+        reduce -> ncclAllReduce buckets -> update, on any world; world 1 uses a one-rank
+        communicator) or "peer" (one-shot all-reduce over CUDA-IPC peer memory, after
+        exchange_export / exchange_import)."""
+        _check(lib().gnn_set_exchange(self.h, {"auto": GNN_EXCH_AUTO, "nccl": GNN_EXCH_NCCL,
+                                               "peer": GNN_EXCH_PEER}[mode]))
+
+    def exchange_export(self, rank: int, world: int) -> bytes:
+        """gnn_exchange_export: allocate this rank's inbox; returns its 64-byte CUDA IPC handle."""
+        buf = (C.c_uint8 * 64)()
+        _check(lib().gnn_exchange_export(self.h, rank, world, buf))
+        return bytes(buf)
+
+    def exchange_import(self, handles):
+        """gnn_exchange_import: map every rank's inbox (handles in rank order)."""
+        blob = b"".join(handles)
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(lib().gnn_exchange_import(self.h, buf))
 
     def comm_init(self, rank: int, world: int, uid: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
@@ -363,6 +379,16 @@ def _phases(self, n=32):
 Model.sampling_phases_us = _phases
 
 
+def _reuse(self):
+    """gnn_debug_get(GNN_DBG_REUSE): (steps whose batch was prefetched, steps that sampled first)."""
+    out = np.zeros(2, dtype=np.float32)
+    _check(lib().gnn_debug_get(self.h, 9, _ptr(out), 2))
+    return int(out[0]), int(out[1])
+
+
+Model.prefetch_reuse = _reuse
+
+
 def plan_step(n_train: int, batch_size: int, world: int, rank: int, step: int):
     """gnn_plan_step: (g, n, offset, b_total) of `rank` at `step` (host only)."""
     L = lib()
@@ -447,6 +473,27 @@ class ShardedGraph(Graph):
         L.gnn_shard_import.argtypes = [C.c_void_p, C.c_void_p]
         L.gnn_shard_import.restype = C.c_int32
         _check(L.gnn_shard_import(self.h, buf))
+
+
+class DeviceGraph(ShardedGraph):
+    """gnn_graph_create_device: the graph from device buffers, borrowed (no copy).  row_ptr,
+    col, X (this shard's rows), y: objects with a `.ptr` device address (or ints); they are kept
+    alive by this object and must not change while it lives."""
+
+    def __init__(self, num_nodes, row_ptr, col, X, y, num_classes, feat_dim, feat_stride, nshards=1, shard=0,
+                 device=0):
+        self._keep = (row_ptr, col, X, y)
+        self.num_nodes, self.num_classes, self.device = num_nodes, num_classes, device
+        self.feat_dim, self.nshards, self.shard = feat_dim, nshards, shard
+        addr = lambda o: C.c_void_p(getattr(o, "ptr", o))
+        L = lib()
+        L.gnn_graph_create_device.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        L.gnn_graph_create_device.restype = C.c_int32
+        h = C.c_void_p()
+        _check(L.gnn_graph_create_device(num_nodes, addr(row_ptr), addr(col), feat_dim, feat_stride, nshards, shard,
+                                         addr(X), addr(y), num_classes, device, C.byref(h)))
+        self.h = h
 
 
 def cache_plan_by_degree(row_ptr, nshards: int, shard: int, capacity: int) -> np.ndarray:

@@ -383,3 +383,36 @@ def test_set_train_nodes_drops_schedule():
     loss = m.train_minibatch(0, 15)                 # the ragged last batch under the default rule
     graph2 = dict(graph, train=inp["train"][:1000])
     check_train_step(m, w, graph2, inp["params"].astype(np.float64), 0, 15, perm, loss)
+
+
+def test_hub_row_beyond_block_sort():
+    """A transposed row longer than the sampling kernel's shared-memory sort (8192 entries) takes
+    its rank-counting fallback: node 0 is a neighbour of every node, the seeds
+    keep all of their ~31 neighbours and so does hop 1 (fanout 32 >= degree), so node 0's row of the
+    hop-1 transposed block holds every hop-1 destination (~30k).  Sampling bit-exact, one step
+    within 1e-4."""
+    from gnn_inputs import Workload, make_params
+    from gnn_inputs.synth import feature_rows, make_labels
+    n = 40_000
+    rng = np.random.default_rng(5)
+    a = np.concatenate([np.arange(1, n), np.repeat(np.arange(1, n), 15)])
+    b = np.concatenate([np.zeros(n - 1, np.int64), rng.integers(1, n, size=15 * (n - 1))])
+    keep = a != b
+    a, b = a[keep], b[keep]
+    keys = np.unique(np.concatenate([a * n + b, b * n + a]))
+    rows, cols = keys // n, (keys % n).astype(np.int32)
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    w = Workload("hub", n, int(rp[-1]), 32, 8, "sage", "neighbor", (2, 32, 32), 3, 32, 1024, n)
+    X = feature_rows(np.arange(n), 32, 7)
+    inp = dict(row_ptr=rp, col=cols, X=X, y=make_labels(n, 8, 7), train=np.arange(n, dtype=np.int32),
+               params=make_params(w.dims, "sage", 3))
+    graph = dict(row_ptr=rp, col=cols, X=X, y=inp["y"], train=inp["train"])
+    g, m = make_gpu(w, inp)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    want, _ = oracle.sample_batch(w, graph, 0, 0, perm)
+    got = m.sample(0, 0)
+    assert_blocks_equal(got, want)
+    assert int(np.sum(want[1]["blk_nbr"] == 0)) > 8192      # node 0's transposed row at hop 1
+    loss = m.train_minibatch(0, 0)
+    check_train_step(m, w, graph, inp["params"].astype(np.float64), 0, 0, perm, loss)

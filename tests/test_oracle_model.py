@@ -322,3 +322,15 @@ def test_library_planner_matches_oracle_plan():
         n, P = int(rng.integers(0, 300)), int(rng.integers(1, 9))
         work = rng.integers(0, 50, size=n).astype(np.int64)   # many ties
         assert list(plan_balanced(work, P)) == balance.plan(work, P), (n, P)
+
+
+def test_formula_recompute_feature_mode(tiny_inputs):
+    """The oracle's formula-recompute mode (X given as a function of the row ids, used for
+    configs[4] whose 57 GB table is never on the host) gives exactly the array mode's step."""
+    from gnn_inputs import feature_rows
+    w, inp = tiny_inputs
+    graph = dict(row_ptr=inp["row_ptr"], col=inp["col"], X=inp["X"][:, :w.feat_dim], y=inp["y"], train=inp["train"])
+    a = oracle.train_step(w, graph, inp["params"], 0, 3, 1)
+    graph_f = dict(graph, X=lambda ids: feature_rows(ids, w.feat_dim, w.graph_seed))
+    b = oracle.train_step(w, graph_f, inp["params"], 0, 3, 1)
+    assert a["loss"] == b["loss"] and np.array_equal(a["grad"], b["grad"])
