@@ -176,6 +176,11 @@ struct gnn_model {
     float* bal_part = nullptr;
     int32_t* bal_cnt = nullptr;
     uint32_t* rf_mask = nullptr;
+    // receptive-field compaction of layer L-1 (R19): its rows, their positions, the
+    // traversal row pointers (block; transposed block when not symmetric), scratch
+    bool rf_compact = false;
+    int32_t *rf_list = nullptr, *rf_pos = nullptr, *rf_sub = nullptr, *rf_sub_t = nullptr;
+    void* rf_scratch = nullptr;
     uint32_t seq = 0;                    // sampling-launch sequence number (scan-word tags)
     bool full_train = true;              // training needs the last hop's relabel (GCN, ShaDow)
     bool last_full = true;               // mode of the last sampling launch (phase readout)
@@ -276,6 +281,7 @@ PackAll pack_desc(gnn_model* m) {
 const int32_t* rows_ptr(gnn_model* m, int set, int li) {   // output rows of layer li (0-based)
     StepState* st = m->bs[set].st;
     if (m->shadow && li == m->L - 1) return &st->batch_n;
+    if (m->rf_compact && li == m->L - 2) return &st->n_rf;
     return &st->n_dst[m->layers[li].blk];
 }
 
@@ -296,6 +302,10 @@ void enqueue_training(gnn_model* m, int set) {
     if (m->shadow && L >= 2)
         K(m, s, GNN_K_AGG, [&] {
             launch_rf_mark(&B.st->batch_n, B.rowptr[m->slot], B.col[m->slot], &B.st->seq, m->rf_mask, s);
+            if (m->rf_compact)
+                launch_rf_compact(m->rf_mask, &B.st->seq, (int)m->nodes_cap, B.rowptr[m->slot],
+                                  B.trowptr[m->slot] ? B.trowptr[m->slot] : B.rowptr[m->slot], m->rf_scratch,
+                                  m->rf_list, m->rf_pos, m->rf_sub, m->rf_sub_t, &B.st->n_rf, s);
         });
     auto bal = [&](bool bwd, int li, const int32_t* rows) {
         const Layer& ly = m->layers[li];
@@ -304,26 +314,37 @@ void enqueue_training(gnn_model* m, int set) {
         b.bwd = bwd;
         b.gcn = !m->sage;
         b.ndst_ptr = &B.st->n_dst[blk];
-        b.rmask = li == L - 2 ? m->rf_mask : nullptr;
+        const bool cmp = m->rf_compact;
+        b.rmask = !cmp && li == L - 2 ? m->rf_mask : nullptr;
         b.tag_ptr = &B.st->seq;
         b.in_pad = ly.in_pad;
         b.part = m->bal_part;
         b.cnt = m->bal_cnt;
+        const int32_t* trow = B.trowptr[blk] ? B.trowptr[blk] : B.rowptr[blk];   // symmetric block: its own transpose
         if (!bwd) {
             b.n_ptr = rows;
             b.rowptr = B.rowptr[blk]; b.col = B.col[blk];
-            b.orow = B.trowptr[blk] ? B.trowptr[blk] : B.rowptr[blk];   // symmetric block: its own transpose
+            b.orow = trow;
             b.H = li == 0 ? g->rows() : FeatRows{m->layers[li - 1].H, nullptr, 0};
             b.gmap = li == 0 ? B.nodes : nullptr;
+            if (cmp && li == L - 2) {   // only the receptive field's rows, written compactly
+                b.rlist = m->rf_list; b.rowptr = m->rf_sub; b.brow = B.rowptr[blk];
+            }
+            if (cmp && li == L - 1) b.gmap = m->rf_pos;   // H of layer L-1 is compact
             b.out = ly.A;
             b.out_w = m->sage ? 2 * ly.in_pad : ly.k_pad;
         } else {
             b.n_ptr = &B.st->n_src[blk];
             b.dlim_ptr = rows;
-            b.rowptr = B.trowptr[blk] ? B.trowptr[blk] : B.rowptr[blk];
+            b.rowptr = trow;
             b.col = B.tdst_s[blk] ? B.tdst_s[blk] : B.col[blk];
             b.orow = B.rowptr[blk];
             b.dA = ly.dA;
+            if (cmp && li == L - 1) {   // gradient reaches only the receptive field: compact dPre of layer L-1
+                b.n_ptr = &B.st->n_rf;
+                b.rlist = m->rf_list; b.rowptr = m->rf_sub_t; b.brow = trow;
+            }
+            if (cmp && li == L - 2) b.dmap = m->rf_pos;   // dA of layer L-1 is compact
             b.hmask = m->layers[li - 1].hmask;
             b.mask_ld = m->layers[li - 1].mask_ld;
             b.out = m->layers[li - 1].dPre;
@@ -349,7 +370,8 @@ void enqueue_training(gnn_model* m, int set) {
             const int fixed_k = direct && !m->full_train ? m->bs[set].sp.hop[blk].k : 0;
             K(m, s, kid, [&] {
                 launch_agg_sage(rows, Hrows, ly.in_pad, direct ? nullptr : self_ids, self_ids, B.rowptr[blk],
-                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, direct ? m->bs[set].sp.hop[blk].k : 0, s);
+                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, direct ? m->bs[set].sp.hop[blk].k : 0,
+                                &B.st->l1_queue, s);
             });
         } else {
             K(m, s, kid, [&] {
@@ -526,6 +548,10 @@ gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const i
                         int32_t b_total, int64_t epoch, int64_t g, bool full) {
     BatchSet& B = m->bs[set];
     if (B.trained_once) CK(cudaStreamWaitEvent(m->sstream, B.trained, 0));
+    // A/B diagnostic GS_SERIAL=1: sampling never runs concurrently with training (it also waits for
+    // the step trained last, whichever set it used)
+    static const bool serial = [] { const char* e = std::getenv("GS_SERIAL"); return e && e[0] == '1'; }();
+    if (serial && m->last >= 0 && m->bs[m->last].trained_once) CK(cudaStreamWaitEvent(m->sstream, m->bs[m->last].trained, 0));
     const int32_t* src = seeds_dev;
     if (!src) {
         if (n) {
@@ -1006,7 +1032,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         return s;
     };
     gnn_status s;
-#define AL(p, n) if ((s = dalloc(&(p), (n), m->owned)) != GNN_OK) return cleanup(s)
+#define AL(p, n) do { if ((s = dalloc(&(p), (n), m->owned)) != GNN_OK) return cleanup(s); } while (0)
 
     // ---- capacities
     int64_t cap_dst = c.batch_size;
@@ -1140,6 +1166,21 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         AL(m->bal_part, 2 * (int64_t)bal_units_cap() * maxw);
         AL(m->bal_cnt, m->nodes_cap + 1);
         AL(m->rf_mask, m->nodes_cap + 1);
+        // GS_RF_COMPACT=0: the uncompacted receptive-field path (rows outside it skipped in place)
+        const char* rc = std::getenv("GS_RF_COMPACT");
+        m->rf_compact = m->L >= 2 && !(rc && rc[0] == '0');
+        if (m->rf_compact) {
+            AL(m->rf_list, m->nodes_cap + 1);
+            AL(m->rf_pos, m->nodes_cap + 1);
+            AL(m->rf_sub, m->nodes_cap + 1);
+            if (m->hb[m->slot].need_t) {
+                AL(m->rf_sub_t, m->nodes_cap + 1);
+            } else {
+                m->rf_sub_t = m->rf_sub;
+            }
+            if ((s = dalloc((char**)&m->rf_scratch, (int64_t)rf_compact_scratch_bytes((int)m->nodes_cap), m->owned)) != GNN_OK)
+                return cleanup(s);
+        }
         CK(cudaMemset(m->bal_cnt, 0, sizeof(int32_t) * (m->nodes_cap + 1)));
         CK(cudaMemset(m->rf_mask, 0, sizeof(uint32_t) * (m->nodes_cap + 1)));
     }
@@ -1649,6 +1690,19 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
         const int rows = (m->shadow && li == m->L - 1) ? st.batch_n : st.n_dst[ly.blk];
         const int64_t need = (int64_t)rows * ly.out;
         if (n < need) return fail(GNN_ERR_BUFFER, "need rows*out = " + std::to_string(need));
+        if (m->rf_compact && li == m->L - 2) {   // compact receptive-field rows -> block rows (others 0)
+            std::memset(out_host, 0, sizeof(float) * need);
+            std::vector<int32_t> list(std::max(st.n_rf, 1));
+            std::vector<float> h((size_t)std::max(st.n_rf, 1) * ly.out);
+            if (st.n_rf) {
+                CK(cudaMemcpy(list.data(), m->rf_list, sizeof(int32_t) * st.n_rf, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy2D(h.data(), sizeof(float) * ly.out, ly.H, sizeof(float) * ly.n_pad, sizeof(float) * ly.out,
+                                st.n_rf, cudaMemcpyDeviceToHost));
+            }
+            for (int p = 0; p < st.n_rf; ++p)
+                std::memcpy(out_host + (int64_t)list[p] * ly.out, h.data() + (size_t)p * ly.out, sizeof(float) * ly.out);
+            return GNN_OK;
+        }
         if (need)
             CK(cudaMemcpy2D(out_host, sizeof(float) * ly.out, ly.H, sizeof(float) * ly.n_pad, sizeof(float) * ly.out,
                             rows, cudaMemcpyDeviceToHost));

@@ -3,6 +3,7 @@
 // packing for the tensor-core GEMMs (gemm_tc.cu), SGD.  All extents come from the device
 // StepState (graph-replayable).  GEMM operands are written as bf16 split planes.
 #include <cub/block/block_reduce.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cstdlib>
 #include <map>
 
@@ -196,7 +197,7 @@ template <int NB>
 __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __restrict__ rows_ptr,
         const float* __restrict__ X, int in_pad, const int32_t* __restrict__ smap,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col, Split A, int fixed_k, int slots,
-        int xpol, int apol) {
+        int xpol, int apol, int32_t* __restrict__ queue) {
     extern __shared__ __align__(128) unsigned char l1_smem[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     uint64_t* bar = reinterpret_cast<uint64_t*>(l1_smem) + warp * NB;
@@ -213,24 +214,41 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
     pdl_wait();
     const int n = *rows_ptr;
     const int nch = in_pad >> 2;
-    const int64_t W = total_warps();
-    const int64_t gw = global_warp();
+    const int W = total_warps();
+    const int gw = global_warp();
     // zero tail rows [n, round64(n)) of the operand planes
-    for (int64_t i = n + gw; i < round64(n); i += W)
+    for (int i = n + gw; i < round64(n); i += W)
         for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, tix(A, i, 4 * ch), kZero4);
     // L2 policies (A/B switches GS_L1_XPOL / GS_L1_APOL): feature rows 0 normal, 1 evict_last,
     // 2 evict_first; operand-plane stores 0 plain, 1 evict_first, 2 evict_last
     const uint64_t pol = xpol == 1 ? policy_evict_last() : xpol == 2 ? policy_evict_first() : policy_evict_normal();
     const uint64_t spol = apol == 2 ? policy_evict_last() : policy_evict_first();
+    // Destination rows in chunks of kL1Chunk from a queue (queue != null: an atomic counter zeroed
+    // by the sampling kernel; a block that starts late, its SM still held by the next batch's
+    // sampling kernel, just takes fewer chunks instead of holding up the whole grid); else static
+    // chunks gw, gw + W, ...  The next chunk is claimed one chunk ahead (its atomic overlaps work).
+    constexpr int kL1Chunk = 8;
+    int ck = 0;
+    auto claim = [&]() -> int {
+        if (!queue) return (gw + (ck++) * W) * kL1Chunk;
+        int v = 0;
+        if (lane == 0) v = atomicAdd(queue, kL1Chunk);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    int cur = claim(), left = kL1Chunk;
+    int nxt_chunk = claim();
+    auto next_row = [&]() -> int {
+        if (left == 0) { cur = nxt_chunk; left = kL1Chunk; nxt_chunk = claim(); }
+        return cur + (kL1Chunk - left--);
+    };
     // A destination row's indices: this lane's row to copy (lane 0: the self row, lane j: the
-    // neighbour j-1) and the row's degree.  Fetched one row ahead of their use, so the index loads
-    // overlap the wait for the rows in flight instead of stalling the copy issue.
+    // neighbour j-1) and the row's degree, fetched one row ahead of their use.
     struct Idx { int nb, self, c; };
-    auto fetch = [&](int64_t i) {
+    auto fetch = [&](int i) {
         Idx x{0, 0, 0};
         if (i >= n) return x;
         if (fixed_k) {   // fixed-stride rows: the count and the ids load in parallel
-            if (lane < fixed_k) x.nb = col[(int)i * fixed_k + lane];
+            if (lane < fixed_k) x.nb = col[i * fixed_k + lane];
             x.c = rowptr[i];
         } else {
             const int beg = rowptr[i];
@@ -251,66 +269,73 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
             bulk_g2s(buf + (size_t)lane * in_pad, X + (int64_t)r * in_pad, row_bytes, &bar[b], pol);
         }
     };
-    int cnt[NB];
+    int row_of[NB], cnt[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-        const int64_t i = gw + b * W;
-        const Idx x = fetch(i);
+        row_of[b] = next_row();
+        const Idx x = fetch(row_of[b]);
         cnt[b] = x.c;
-        if (i < n) issue(b, x);
+        if (row_of[b] < n) issue(b, x);
     }
-    Idx pend = fetch(gw + (int64_t)NB * W);   // the row that re-arms the first freed buffer
-    uint32_t phase = 0;   // parity bit of every buffer's current use (buffers are used round-robin)
-    int b = 0;
-    for (int64_t i = gw; i < n; i += W) {
-        const Idx nxt = fetch(i + (int64_t)(NB + 1) * W);   // loads in flight during this row
-        mbar_wait(&bar[b], phase);
-        const float* buf = ring + (size_t)b * slots * in_pad;
-        int c = cnt[0];
+    int ipend = next_row();
+    Idx pend = fetch(ipend);   // the row that re-arms the first freed buffer
+    uint32_t phase = 0;        // parity of every buffer's current use (buffers used round-robin)
+    bool done = false;
+    while (!done) {
 #pragma unroll
-        for (int q = 1; q < NB; ++q) if (b == q) c = cnt[q];
-        float4 sv = kZero4, acc = kZero4;
-        if (lane < nch) {
-            sv = reinterpret_cast<const float4*>(buf)[lane];
-            for (int j = 1; j <= c; ++j) acc = f4add(acc, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane]);
-        }
-        // rows of more than 128 floats: lanes take further chunks
-        float4 sv2 = kZero4, acc2 = kZero4;
-        const bool wide = nch > 32;
-        if (wide && lane + 32 < nch) {
-            sv2 = reinterpret_cast<const float4*>(buf)[lane + 32];
-            for (int j = 1; j <= c; ++j) acc2 = f4add(acc2, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane + 32]);
-        }
-        // the buffer is read: re-arm it with this warp's row i + NB*W (async-proxy writes after
-        // generic-proxy reads of the same shared memory need the proxy fence)
-        fence_async_smem();
-        __syncwarp();
-        const bool more = i + (int64_t)NB * W < n;
-        if (more) issue(b, pend);
-#pragma unroll
-        for (int q = 0; q < NB; ++q) if (b == q) cnt[q] = more ? pend.c : 0;
-        pend = nxt;
-        const float inv = c ? 1.0f / (float)c : 0.f;   // one division per row (R23)
-        if (apol) {
+        for (int b = 0; b < NB; ++b) {   // unrolled: b is a constant, row_of / cnt stay in registers
+            if (done) break;
+            const int i = row_of[b];
+            if (i >= n) { done = true; break; }
+            const int inxt = ipend < n ? next_row() : n;
+            const Idx nxt = fetch(inxt);   // loads in flight during this row
+            mbar_wait(&bar[b], phase);
+            const float* buf = ring + (size_t)b * slots * in_pad;
+            const int c = cnt[b];
+            float4 sv = kZero4, acc = kZero4;
             if (lane < nch) {
-                store_split4_pol(A, tix(A, i, 4 * lane), sv, spol);
-                store_split4_pol(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv), spol);
+                sv = reinterpret_cast<const float4*>(buf)[lane];
+                for (int j = 1; j <= c; ++j) acc = f4add(acc, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane]);
             }
+            // rows of more than 128 floats: lanes take further chunks
+            float4 sv2 = kZero4, acc2 = kZero4;
+            const bool wide = nch > 32;
             if (wide && lane + 32 < nch) {
-                store_split4_pol(A, tix(A, i, 4 * (lane + 32)), sv2, spol);
-                store_split4_pol(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv), spol);
+                sv2 = reinterpret_cast<const float4*>(buf)[lane + 32];
+                for (int j = 1; j <= c; ++j) acc2 = f4add(acc2, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane + 32]);
             }
-        } else {
-            if (lane < nch) {
-                store_split4(A, tix(A, i, 4 * lane), sv);
-                store_split4(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv));
-            }
-            if (wide && lane + 32 < nch) {
-                store_split4(A, tix(A, i, 4 * (lane + 32)), sv2);
-                store_split4(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv));
+            // the buffer is read: re-arm it with the pending row (async-proxy writes after
+            // generic-proxy reads of the same shared memory need the proxy fence)
+            fence_async_smem();
+            __syncwarp();
+            const bool more = ipend < n;
+            if (more) issue(b, pend);
+            cnt[b] = more ? pend.c : 0;
+            row_of[b] = more ? ipend : n;
+            pend = nxt;
+            ipend = inxt;
+            const float inv = c ? 1.0f / (float)c : 0.f;   // one division per row (R23)
+            if (apol) {
+                if (lane < nch) {
+                    store_split4_pol(A, tix(A, i, 4 * lane), sv, spol);
+                    store_split4_pol(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv), spol);
+                }
+                if (wide && lane + 32 < nch) {
+                    store_split4_pol(A, tix(A, i, 4 * (lane + 32)), sv2, spol);
+                    store_split4_pol(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv), spol);
+                }
+            } else {
+                if (lane < nch) {
+                    store_split4(A, tix(A, i, 4 * lane), sv);
+                    store_split4(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv));
+                }
+                if (wide && lane + 32 < nch) {
+                    store_split4(A, tix(A, i, 4 * (lane + 32)), sv2);
+                    store_split4(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv));
+                }
             }
         }
-        if (++b == NB) { b = 0; phase ^= 1u; }
+        phase ^= 1u;
     }
 }
 
@@ -534,6 +559,14 @@ struct BalArgs {
     int out_w;                 // columns of `out` (zero tail rows)
     float* part;               // partial rows [2 * units][in_pad]
     int32_t* cnt;              // per-row piece counters (zero between launches)
+    int ch0, nchp;             // column panel: float4 chunks [ch0, ch0 + nchp) of every row
+    // ShaDow receptive-field compaction (R19): traverse only the listed block rows
+    // rlist[0..n) (rowptr is then the listed rows' own prefix sum and edges are read at
+    // brow[rlist[r]] + offset; output row r is compact); BWD dmap[t] = dA row of destination t
+    // (-1: no gradient), replacing dlim / rmask.
+    const int32_t* rlist;
+    const int32_t* brow;
+    const int32_t* dmap;
 };
 
 template <int CPL, int MODE>   // MODE: 0 FWD SAGE, 1 FWD GCN, 2 BWD SAGE, 3 BWD GCN
@@ -544,9 +577,13 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
     const int n = *a.n_ptr;
     const int lane = lane_id();
     const int nch = a.in_pad >> 2;
+    // column panel of this launch: chunks [c0, c0 + pch) of every row (the launcher splits wide
+    // rows into panels whose working set fits in L2; partial slots and counters are per launch)
+    const int c0 = a.ch0, pch = a.nchp;
     const int W = total_warps();
-    for (int i = n + global_warp(); i < round64(n); i += W)
-        for (int ch = lane; ch < (a.out_w >> 2); ch += 32) store_split4(a.out, tix(a.out, i, 4 * ch), kZero4);
+    if (c0 == 0)
+        for (int i = n + global_warp(); i < round64(n); i += W)
+            for (int ch = lane; ch < (a.out_w >> 2); ch += 32) store_split4(a.out, tix(a.out, i, 4 * ch), kZero4);
     const int ndst = *a.ndst_ptr;
     const int dlim = BWD ? *a.dlim_ptr : 0;
     const uint32_t tag = a.rmask ? *a.tag_ptr : 0u;
@@ -557,18 +594,18 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
     const int64_t ldd = GCN ? a.in_pad : 2 * a.in_pad;   // BWD dA row (SAGE: [dSelf | dM])
 
     // finish row r from its full sum `acc` (fwd: normalise + self term; bwd: self term + ReLU')
-    auto finish = [&](int r, int rb, int re, float4 (&acc)[CPL], bool any) {
+    auto finish = [&](int r, int R, int rb, int re, float4 (&acc)[CPL], bool any) {
         if constexpr (!BWD) {
-            const int self = a.gmap ? a.gmap[r] : r;
+            const int self = a.gmap ? a.gmap[R] : R;
             const float4* ps = reinterpret_cast<const float4*>(a.H.row(self, a.in_pad));
             if constexpr (GCN) {
                 const float din = (float)(re - rb + 1);
-                const float dself = (float)(a.orow[r + 1] - a.orow[r] + (r < ndst ? 1 : 0));
+                const float dself = (float)(a.orow[R + 1] - a.orow[R] + (R < ndst ? 1 : 0));
                 const float ws = 1.0f / sqrtf(din * dself);
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
-                    if (ch < nch) store_split4(a.out, tix(a.out, r, 4 * ch), f4fma(ws, __ldg(ps + ch), acc[c]));
+                    if (ch < pch) store_split4(a.out, tix(a.out, r, 4 * (c0 + ch)), f4fma(ws, __ldg(ps + c0 + ch), acc[c]));
                 }
             } else {
                 const int deg = re - rb;
@@ -576,36 +613,38 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
-                    if (ch < nch) {
-                        store_split4(a.out, tix(a.out, r, 4 * ch), __ldg(ps + ch));
-                        store_split4(a.out, tix(a.out, r, 4 * (nch + ch)), f4scale(acc[c], inv));
+                    if (ch < pch) {
+                        store_split4(a.out, tix(a.out, r, 4 * (c0 + ch)), __ldg(ps + c0 + ch));
+                        store_split4(a.out, tix(a.out, r, 4 * (nch + c0 + ch)), f4scale(acc[c], inv));
                     }
                 }
             }
         } else {
-            const bool self_on = r < dlim && (!a.rmask || a.rmask[r] == tag);
+            const int sr = a.dmap ? a.dmap[R] : ((R < dlim && (!a.rmask || a.rmask[R] == tag)) ? R : -1);
+            const bool self_on = sr >= 0;
             float wself = 1.f;
             if (GCN && self_on) {
-                const float din = (float)(a.orow[r + 1] - a.orow[r] + 1);
-                const float dout = (float)(re - rb + (r < ndst ? 1 : 0));
+                const float din = (float)(a.orow[R + 1] - a.orow[R] + 1);
+                const float dout = (float)(re - rb + (R < ndst ? 1 : 0));
                 wself = 1.0f / sqrtf(din * dout);
             }
             const uint32_t* mp = a.hmask + (int64_t)r * a.mask_ld;
-            const float4* sp = reinterpret_cast<const float4*>(a.dA + (int64_t)r * ldd);
+            const float4* sp = reinterpret_cast<const float4*>(a.dA + (int64_t)max(sr, 0) * ldd);
             if (!any && !self_on) {   // no gradient reaches row r: dPre = 0 (no reads)
-                for (int ch = lane; ch < nch; ch += 32) store_split4(a.out, tix(a.out, r, 4 * ch), kZero4);
+                for (int ch = lane; ch < pch; ch += 32) store_split4(a.out, tix(a.out, r, 4 * (c0 + ch)), kZero4);
                 return;
             }
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
                 const int ch = lane + 32 * c;
-                if (ch < nch) {
+                if (ch < pch) {
+                    const int cc = c0 + ch;
                     float4 v = acc[c];
-                    if (self_on) v = GCN ? f4fma(wself, __ldg(sp + ch), v) : f4add(v, __ldg(sp + ch));
-                    const uint32_t h = __ldg(mp + (ch >> 3)) >> ((4 * ch) & 31);   // ReLU decisions
+                    if (self_on) v = GCN ? f4fma(wself, __ldg(sp + cc), v) : f4add(v, __ldg(sp + cc));
+                    const uint32_t h = __ldg(mp + (cc >> 3)) >> ((4 * cc) & 31);   // ReLU decisions
                     v.x = (h & 1u) ? v.x : 0.f; v.y = (h & 2u) ? v.y : 0.f;
                     v.z = (h & 4u) ? v.z : 0.f; v.w = (h & 8u) ? v.w : 0.f;
-                    store_split4(a.out, tix(a.out, r, 4 * ch), v);
+                    store_split4(a.out, tix(a.out, r, 4 * cc), v);
                 }
             }
         }
@@ -630,32 +669,37 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
             const int rb = __shfl_sync(kFull, rpw, r - wb), re = __shfl_sync(kFull, rpw, r - wb + 1);
             const int64_t fr = (int64_t)rb + r, fr1 = (int64_t)re + r + 1;
             if (r >= n || fr >= d1) break;
+            const int R = a.rlist ? a.rlist[r] : r;          // block row
+            const int eoff = a.rlist ? a.brow[R] - rb : 0;   // edge e of row r is block entry e + eoff
             if constexpr (!BWD) {
-                if (a.rmask && a.rmask[r] != tag) continue;   // row outside the receptive field
+                if (a.rmask && a.rmask[R] != tag) continue;   // row outside the receptive field
             }
             const int eb = max(rb, (int)(d0 - r)), ee = min(re, (int)(d1 - r));
             float4 acc[CPL];
 #pragma unroll
             for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
             const float din_r = (float)(re - rb + 1);                       // FWD GCN: d_in(r)
-            const float dout_r = (float)(re - rb + (r < ndst ? 1 : 0));     // BWD GCN: d_out(u)
+            const float dout_r = (float)(re - rb + (R < ndst ? 1 : 0));     // BWD GCN: d_out(u)
             bool any = false;   // a contributing edge was seen (else the row sum is exactly 0)
             for (int e0 = eb; e0 < ee; e0 += 32) {
                 const int m = min(32, ee - e0);
                 int myrow = -1;
                 float myw = 0.f;
                 if (lane < m) {
-                    const int c = a.col[e0 + lane];
+                    const int c = a.col[e0 + lane + eoff];
                     if constexpr (!BWD) {
                         myrow = a.gmap ? a.gmap[c] : c;
                         if (GCN) {
                             const float dout = (float)(a.orow[c + 1] - a.orow[c] + (c < ndst ? 1 : 0));
                             myw = 1.0f / sqrtf(din_r * dout);
                         }
-                    } else if (c < dlim && (!a.rmask || a.rmask[c] == tag)) {
-                        myrow = c;
-                        const float din = (float)(a.orow[c + 1] - a.orow[c] + (GCN ? 1 : 0));
-                        myw = GCN ? 1.0f / sqrtf(din * dout_r) : 1.0f / din;
+                    } else {
+                        const int dr = a.dmap ? a.dmap[c] : ((c < dlim && (!a.rmask || a.rmask[c] == tag)) ? c : -1);
+                        if (dr >= 0) {
+                            myrow = dr;
+                            const float din = (float)(a.orow[c + 1] - a.orow[c] + (GCN ? 1 : 0));
+                            myw = GCN ? 1.0f / sqrtf(din * dout_r) : 1.0f / din;
+                        }
                     }
                 }
                 int mv = m;
@@ -680,12 +724,12 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
                         ww[j] = __shfl_sync(kFull, myw, min(q + j, 31));
                         if (q + j >= mv) rr[j] = -1;
                         const float4* p;
-                        if constexpr (!BWD) p = reinterpret_cast<const float4*>(a.H.row(max(rr[j], 0), a.in_pad));
-                        else p = reinterpret_cast<const float4*>(a.dA + (int64_t)max(rr[j], 0) * ldd) + (GCN ? 0 : nch);
+                        if constexpr (!BWD) p = reinterpret_cast<const float4*>(a.H.row(max(rr[j], 0), a.in_pad)) + c0;
+                        else p = reinterpret_cast<const float4*>(a.dA + (int64_t)max(rr[j], 0) * ldd) + (GCN ? 0 : nch) + c0;
 #pragma unroll
                         for (int c = 0; c < CPL; ++c) {
                             const int ch = lane + 32 * c;
-                            v[j][c] = (ch < nch && rr[j] >= 0) ? __ldg(p + ch) : kZero4;
+                            v[j][c] = (ch < pch && rr[j] >= 0) ? __ldg(p + ch) : kZero4;
                         }
                     }
 #pragma unroll
@@ -698,13 +742,13 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
                 }
             }
             const bool started = fr >= d0, completed = fr1 <= d1;
-            if (started && completed) { finish(r, rb, re, acc, any); continue; }
+            if (started && completed) { finish(r, R, rb, re, acc, any); continue; }
             // a piece of a row spread over several units
             float* slot = a.part + (int64_t)(started ? 2 * u + 1 : 2 * u) * a.in_pad;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
                 const int ch = lane + 32 * c;
-                if (ch < nch) __stcg(reinterpret_cast<float4*>(slot) + ch, acc[c]);
+                if (ch < pch) __stcg(reinterpret_cast<float4*>(slot) + ch, acc[c]);
             }
             __threadfence();
             __syncwarp();
@@ -721,11 +765,11 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
-                    if (ch < nch) acc[c] = f4add(acc[c], __ldcg(ps + ch));
+                    if (ch < pch) acc[c] = f4add(acc[c], __ldcg(ps + ch));
                 }
             }
             if (lane == 0) a.cnt[r] = 0;
-            finish(r, rb, re, acc, true);
+            finish(r, R, rb, re, acc, true);
         }
     }
 }
@@ -751,6 +795,46 @@ __global__ void __launch_bounds__(256) k_rf_mark(const int32_t* __restrict__ nse
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int i = tid; i < b; i += nth) mask[i] = tag;
     for (int e = tid; e < ne; e += nth) mask[col[e]] = tag;
+}
+
+// Receptive-field compaction (launch_rf_compact): per block row r < cap, in = [mask[r] == tag].
+__global__ void k_rf_prep(const uint32_t* __restrict__ mask, const uint32_t* __restrict__ tag_ptr, int cap,
+                          const int32_t* __restrict__ rowptr, const int32_t* __restrict__ trow,
+                          int32_t* __restrict__ flags, int32_t* __restrict__ degf, int32_t* __restrict__ degt) {
+    pdl_trigger();
+    pdl_wait();
+    const uint32_t tag = *tag_ptr;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < cap; r += gridDim.x * blockDim.x) {
+        const bool in = mask[r] == tag;
+        flags[r] = in ? 1 : 0;
+        degf[r] = in ? rowptr[r + 1] - rowptr[r] : 0;
+        degt[r] = in ? trow[r + 1] - trow[r] : 0;
+    }
+}
+__global__ void k_rf_scatter(int cap, const int32_t* __restrict__ flags, const int32_t* __restrict__ degf,
+                             const int32_t* __restrict__ degt, const int32_t* __restrict__ pos,
+                             const int32_t* __restrict__ scf, const int32_t* __restrict__ sct, int32_t* __restrict__ rf_list,
+                             int32_t* __restrict__ rf_pos, int32_t* __restrict__ sub, int32_t* __restrict__ subt,
+                             int32_t* __restrict__ n_rf) {
+    pdl_trigger();
+    pdl_wait();
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < cap; r += gridDim.x * blockDim.x) {
+        if (flags[r]) {
+            const int p = pos[r];
+            rf_list[p] = r;
+            rf_pos[r] = p;
+            sub[p] = scf[r];
+            if (subt != sub) subt[p] = sct[r];
+        } else {
+            rf_pos[r] = -1;
+        }
+        if (r == cap - 1) {
+            const int n = pos[r] + flags[r];
+            *n_rf = n;
+            sub[n] = scf[r] + degf[r];
+            if (subt != sub) subt[n] = sct[r] + degt[r];
+        }
+    }
 }
 
 // ------------------------------------------------------------------ weights, reduce, SGD
@@ -991,7 +1075,9 @@ int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
 template <int NB>
 static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, const int32_t* smap,
                            const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k, int slots,
-                           cudaStream_t s) {
+                           int32_t* queue, cudaStream_t s) {
+    static const int dyn = [] { const char* e = std::getenv("GS_L1_DYN"); return e ? std::atoi(e) : 1; }();
+    if (!dyn) queue = nullptr;
     size_t smem = 128 + (size_t)kL1Warps * NB * slots * in_pad * 4;
     if (smem > 200 * 1024) return false;
     // GS_L1_BPS = b: pad the request just past the (b+1)-blocks threshold, so that at most b blocks
@@ -1002,6 +1088,12 @@ static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, 
     int& grid = grids[smem];
     if (!grid) {
         cudaFuncSetAttribute(k_agg_l1_bulk<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // the SMs this kernel runs on are configured with the whole 228 KB as shared memory, so a
+        // block of the next batch's sampling kernel (35 KB) still fits beside the 3 gather blocks
+        // (the driver otherwise picks the smallest split that holds them, 200 KB, and the sampling
+        // kernel, which overlaps training, cannot co-reside: measured -12 % mini-batches/s)
+        static const int carve = [] { const char* e = std::getenv("GS_L1_CARVE"); return e ? std::atoi(e) : 100; }();
+        if (carve >= 0) cudaFuncSetAttribute(k_agg_l1_bulk<NB>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         int per_sm = 0, dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1014,25 +1106,28 @@ static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, 
     static const int pdl = [] { const char* e = std::getenv("GS_L1_PDL"); return e ? std::atoi(e) : 1; }();
     if (pdl)
         launch_pdl(k_agg_l1_bulk<NB>, grid, kL1Warps * 32, smem, s, rows_ptr, X, in_pad, smap, blk_rowptr, col, A,
-                   fixed_k, slots, xpol, apol);
+                   fixed_k, slots, xpol, apol, queue);
     else
+    {
+        apply_carveout((const void*)k_agg_l1_bulk<NB>);
         k_agg_l1_bulk<NB><<<grid, kL1Warps * 32, smem, s>>>(rows_ptr, X, in_pad, smap, blk_rowptr, col, A, fixed_k,
-                                                           slots, xpol, apol);
+                                                           slots, xpol, apol, queue);
+    }
     return true;
 }
 
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
-                     int k_max, cudaStream_t s) {
+                     int k_max, int32_t* queue, cudaStream_t s) {
     // layer 1 of the neighbour sampler on a local table: rows staged by the bulk-copy engine
     // (GS_L1_BULK=0: register loads, for A/B; GS_L1_NB: buffers per warp)
     static const int bulk = [] { const char* e = std::getenv("GS_L1_BULK"); return e ? std::atoi(e) : 1; }();
     static const int nb = [] { const char* e = std::getenv("GS_L1_NB"); return e ? std::atoi(e) : 2; }();
     if (bulk && !H.shards && !gmap && smap && k_max > 0 && k_max <= 31 && in_pad * 4 <= 1024) {
         const bool ok = nb == 3 ? launch_l1_bulk<3>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
-                                                     1 + k_max, s)
+                                                     1 + k_max, queue, s)
                                 : launch_l1_bulk<2>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
-                                                     1 + k_max, s);
+                                                     1 + k_max, queue, s);
         if (ok) return;
     }
     // A/B diagnostic only: GS_AGG_DUMMY_SMEM = bytes of (unused) dynamic shared memory for the
@@ -1076,11 +1171,8 @@ void launch_spmm_bwd(bool gcn, int h, const StepState* st, const int32_t* dlim, 
 
 int bal_units_cap() { return kBalUnits; }
 
-void launch_agg_bal(const BalLaunch& b, cudaStream_t s) {
-    BalArgs a{b.n_ptr, b.ndst_ptr, b.dlim_ptr, b.rowptr, b.col, b.orow, b.rmask, b.tag_ptr, b.H, b.gmap,
-              b.dA, b.hmask, b.mask_ld, b.in_pad, b.out, b.out_w, b.part, b.cnt};
-    const int mode = (b.bwd ? 2 : 0) + (b.gcn ? 1 : 0);
-    const int cpl = cpl_of(b.in_pad);
+static void launch_agg_bal_panel(const BalArgs& a, int mode, int nchp, cudaStream_t s) {
+    const int cpl = (nchp + 31) / 32;
     const int c = cpl <= 1 ? 1 : cpl <= 2 ? 2 : cpl <= 4 ? 4 : 8;
 #define GS_BAL(C, M) if (c == C && mode == M) {                                                  \
         if constexpr (M >= 2) launch_pdl(k_agg_bal_bwd<C, M>, kWarpGrid, 256, 0, s, a);            \
@@ -1092,6 +1184,56 @@ void launch_agg_bal(const BalLaunch& b, cudaStream_t s) {
     GS_BAL(4, 0) GS_BAL(4, 1) GS_BAL(4, 2) GS_BAL(4, 3)
     GS_BAL(8, 0) GS_BAL(8, 1) GS_BAL(8, 2) GS_BAL(8, 3)
 #undef GS_BAL
+}
+
+// Forward launches over wide rows are split into column panels (GS_BAL_PANEL_CH float4 chunks
+// each; 0 = whole rows): the edge-wise row reads of a ShaDow block revisit every row many times,
+// and a panel's working set (|S| x panel bytes) fits in L2 where whole rows do not.
+void launch_agg_bal(const BalLaunch& b, cudaStream_t s) {
+    BalArgs a{b.n_ptr, b.ndst_ptr, b.dlim_ptr, b.rowptr, b.col, b.orow, b.rmask, b.tag_ptr, b.H, b.gmap,
+              b.dA, b.hmask, b.mask_ld, b.in_pad, b.out, b.out_w, b.part, b.cnt, 0, b.in_pad >> 2,
+              b.rlist, b.brow, b.dmap};
+    const int mode = (b.bwd ? 2 : 0) + (b.gcn ? 1 : 0);
+    static const int pch = [] { const char* e = std::getenv("GS_BAL_PANEL_CH"); return e ? std::atoi(e) : 0; }();
+    const int nch = b.in_pad >> 2;
+    if (b.bwd || pch <= 0 || pch >= nch) {
+        launch_agg_bal_panel(a, mode, nch, s);
+        return;
+    }
+    for (int c0 = 0; c0 < nch; c0 += pch) {
+        a.ch0 = c0;
+        a.nchp = std::min(pch, nch - c0);
+        launch_agg_bal_panel(a, mode, a.nchp, s);
+    }
+}
+
+static size_t rf_scan_bytes(int cap) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const int32_t*)nullptr, (int32_t*)nullptr, cap);
+    return b;
+}
+size_t rf_compact_scratch_bytes(int cap) { return 7 * ((size_t)cap * 4 + 256) + rf_scan_bytes(cap) + 256; }
+
+void launch_rf_compact(const uint32_t* mask, const uint32_t* tag_ptr, int cap, const int32_t* rowptr,
+                       const int32_t* deg_rowptr, void* scratch, int32_t* rf_list, int32_t* rf_pos, int32_t* sub_rowptr,
+                       int32_t* sub_rowptr_t, int32_t* n_rf, cudaStream_t s) {
+    char* p = static_cast<char*>(scratch);
+    auto take = [&](size_t bytes) { char* q = p; p += (bytes + 255) & ~size_t(255); return q; };
+    int32_t* flags = reinterpret_cast<int32_t*>(take(4 * (size_t)cap));
+    int32_t* degf = reinterpret_cast<int32_t*>(take(4 * (size_t)cap));
+    int32_t* degt = reinterpret_cast<int32_t*>(take(4 * (size_t)cap));
+    int32_t* pos = reinterpret_cast<int32_t*>(take(4 * (size_t)cap));
+    int32_t* scf = reinterpret_cast<int32_t*>(take(4 * (size_t)cap));
+    int32_t* sct = reinterpret_cast<int32_t*>(take(4 * (size_t)cap));
+    size_t tb = rf_scan_bytes(cap);
+    void* tmp = take(tb);
+    const bool two = sub_rowptr_t != sub_rowptr;
+    launch_pdl(k_rf_prep, 148 * 4, 256, 0, s, mask, tag_ptr, cap, rowptr, two ? deg_rowptr : rowptr, flags, degf, degt);
+    cub::DeviceScan::ExclusiveSum(tmp, tb, flags, pos, cap, s);
+    cub::DeviceScan::ExclusiveSum(tmp, tb, degf, scf, cap, s);
+    if (two) cub::DeviceScan::ExclusiveSum(tmp, tb, degt, sct, cap, s);
+    launch_pdl(k_rf_scatter, 148 * 4, 256, 0, s, cap, flags, degf, degt, pos, scf, sct, rf_list, rf_pos, sub_rowptr,
+               sub_rowptr_t, n_rf);
 }
 
 void launch_rf_mark(const int32_t* nseed_ptr, const int32_t* rowptr, const int32_t* col, const uint32_t* tag_ptr,

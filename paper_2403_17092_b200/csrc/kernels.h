@@ -20,9 +20,15 @@ namespace gs {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// A/B switch GS_CARVEOUT = p (0..100): every training kernel asks for the same L1/shared-memory
+// split (cudaFuncAttributePreferredSharedMemoryCarveout), so consecutive or concurrent kernels
+// never need an SM reconfiguration.  Unset: the driver's per-kernel choice.
+void apply_carveout(const void* kernel);
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
+    apply_carveout((const void*)kernel);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -155,7 +161,7 @@ void launch_cache_fill(FeatRows src, const int32_t* ids, int64_t n, int ld, floa
 // (rows have at most k_max sources); layer 1 on a local table then stages rows by bulk copy.
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
-                     int k_max, cudaStream_t s);
+                     int k_max, int32_t* queue, cudaStream_t s);   // queue: row-chunk counter, zeroed per batch (nullable)
 // GCN aggregation A = Â H (self loop included) for rows i < *rows_ptr of a block with
 // *ndst_ptr destinations; d_out from the transposed row pointer.  col must be local ids.
 void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,
@@ -184,9 +190,24 @@ struct BalLaunch {
     int out_w;
     float* part;               // [2 * bal_units_cap()][in_pad] floats
     int32_t* cnt;              // [rows cap] zero-initialised
+    // receptive-field compaction (nullable): traverse block rows rlist[0..*n_ptr) with rowptr =
+    // their own prefix sum, edges at brow[rlist[r]] + offset, compact output rows; BWD dmap[t] =
+    // dA row of destination t or -1 (replaces dlim / rmask)
+    const int32_t* rlist = nullptr;
+    const int32_t* brow = nullptr;
+    const int32_t* dmap = nullptr;
 };
 int bal_units_cap();   // partial slots needed: 2 * bal_units_cap() rows of in_pad floats
 void launch_agg_bal(const BalLaunch& b, cudaStream_t s);
+// Receptive-field list of the last layer (after launch_rf_mark): flags / degrees indexed by block
+// row, exclusive scans (CUB) over `cap` rows, then rf_list[p] = p-th row in the field (ascending),
+// rf_pos[r] = p or -1, sub_rowptr[p] = Σ_{q<p} deg(rf_list[q]) with degrees from `deg_rowptr`
+// (the traversed CSR of the backward: the block, or its transpose), *n_rf.  scratch: see
+// rf_compact_scratch_bytes(cap).
+size_t rf_compact_scratch_bytes(int cap);
+void launch_rf_compact(const uint32_t* mask, const uint32_t* tag_ptr, int cap, const int32_t* rowptr,
+                       const int32_t* deg_rowptr, void* scratch, int32_t* rf_list, int32_t* rf_pos, int32_t* sub_rowptr,
+                       int32_t* sub_rowptr_t, int32_t* n_rf, cudaStream_t s);
 // mask[r] = *tag_ptr for the seeds r < *nseed_ptr and their in-neighbours in the block.
 void launch_rf_mark(const int32_t* nseed_ptr, const int32_t* rowptr, const int32_t* col, const uint32_t* tag_ptr,
                     uint32_t* mask, cudaStream_t s);

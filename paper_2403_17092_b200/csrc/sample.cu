@@ -1,5 +1,9 @@
 // Epoch permutation keys (sm_100a).  The sampling phases themselves
 // are one persistent kernel in sample_step.cu.
+#include <cstdlib>
+#include <mutex>
+#include <set>
+
 #include "kernels.h"
 
 namespace gs {
@@ -93,6 +97,15 @@ int validate_graph(const int64_t* row_ptr, const int32_t* col, int64_t n, const 
     ok = ok && cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
     cudaFree(d);
     return ok ? h : -1;
+}
+
+void apply_carveout(const void* kernel) {
+    static const int pct = [] { const char* e = std::getenv("GS_CARVEOUT"); return e ? std::atoi(e) : -1; }();
+    if (pct < 0) return;
+    static std::mutex mu;
+    static std::set<const void*> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert(kernel).second) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
 bool check_symmetric(const int64_t* row_ptr, const int32_t* col, int64_t n, bool* symmetric) {

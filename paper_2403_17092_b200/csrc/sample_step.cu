@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, GS_SAMPLE_MINB) k_sample_step(Sample
         st->g = g;
         st->loss = 0.f;
         st->seq = tag;
+        st->l1_queue = 0;
     }
     for (int i = gtid; i < P.n_seeds; i += nthreads) {   // nodes[i] = seed_i, map[seed_i] = i
         const int v = P.seed_src[i];
@@ -547,6 +548,9 @@ int sample_step_grid() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_sample_step, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
+        // A/B switch GS_SAMPLE_CARVE: the sampling kernel's preferred L1/shared split (unset: driver)
+        if (const char* e = std::getenv("GS_SAMPLE_CARVE"))
+            cudaFuncSetAttribute(k_sample_step, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_step, kThreads, kSortSmem);
         grid = std::max(1, std::min(per_sm, 1)) * std::max(sms, 1);
     }
@@ -572,6 +576,7 @@ void launch_sample_step(const SampleParams& p, cudaStream_t s) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = coop ? 1 : 0;
+    apply_carveout((const void*)k_sample_step);
     cudaLaunchKernelEx(&cfg, k_sample_step, p);
 }
 
