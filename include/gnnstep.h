@@ -297,7 +297,11 @@ gnn_status gnn_synchronize(gnn_model* m);
  * (layer l's output H^(l) of the last step, 0-based l, rows x out, fp32; its sign pattern
  * is the ReLU decision the backward pass used).  BUFFER if n is too small. */
 enum { GNN_DBG_LOGITS = 0, GNN_DBG_GRADS = 1, GNN_DBG_LOSS = 2, GNN_DBG_PHASES = 8, GNN_DBG_REUSE = 9,
-       GNN_DBG_ACT = 16 };
+       GNN_DBG_TIMELINE = 10, GNN_DBG_ACT = 16 };
+/* GNN_DBG_TIMELINE (diagnostics, when the environment has GS_TIMELINE=1 at model creation): the
+ * step timeline since the last read, out[0] = k steps, then per step 4 values in microseconds from
+ * the first recorded training start: sampling launch start / end, training start / end (CUDA
+ * events on the sampling and training streams).  BUFFER if n < 4k + 1. */
 /* GNN_DBG_REUSE: 2 values, the training calls (train_minibatch / train_batch_host / train_epoch
  * steps) whose batch was found already sampled (prefetched while the previous step trained) and
  * those that had to sample it first, since the model was created. */

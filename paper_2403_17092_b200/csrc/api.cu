@@ -127,6 +127,7 @@ struct BatchSet {
     int32_t *trowptr[kMaxHops + 1] = {}, *tdst_s[kMaxHops + 1] = {};
     SampleParams sp{};
     cudaEvent_t sampled = nullptr, trained = nullptr;
+    cudaEvent_t l1done = nullptr;    // recorded after this set's layer-1 aggregation (GS_SAMPLE_AFTER_L1)
     bool trained_once = false;
     // the batch this set holds (valid until trained or overwritten)
     bool valid = false;
@@ -216,6 +217,16 @@ struct gnn_model {
     int64_t launches_per_step = 0;
 
     int64_t reuse_hits = 0, reuse_misses = 0;   // steps that found / did not find their batch prefetched
+    // step timeline (GS_TIMELINE=1, diagnostics): events around every sampling launch (sampling
+    // stream) and every training launch (training stream), read back by gnn_debug_get
+    bool timeline = false;
+    // A batch's sampling waits until the training step in flight has finished its layer-1
+    // aggregation: the bulk-copy gather (3 x 58 KB of shared memory per SM) then runs alone at full
+    // bandwidth, and the sampling kernel overlaps the rest of the step (timeline, DESIGN.md §6.1:
+    // products 3780 -> 4290 mini-batches/s, epoch 51.8 -> 43.9 ms; with sampling co-running the
+    // gather the training span grew from ~186 to ~267 µs)
+    bool sample_after_l1 = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tl_sample, tl_train;
     bool profiling = false;
     std::vector<ProfPair> pending;
     std::vector<cudaEvent_t> free_events;
@@ -370,14 +381,19 @@ void enqueue_training(gnn_model* m, int set) {
             const int fixed_k = direct && !m->full_train ? m->bs[set].sp.hop[blk].k : 0;
             K(m, s, kid, [&] {
                 launch_agg_sage(rows, Hrows, ly.in_pad, direct ? nullptr : self_ids, self_ids, B.rowptr[blk],
-                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, direct ? m->bs[set].sp.hop[blk].k : 0,
-                                &B.st->l1_queue, s);
+                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, direct ? m->bs[set].sp.hop[blk].k : 0, s);
             });
         } else {
             K(m, s, kid, [&] {
                 launch_agg_gcn(rows, &B.st->n_dst[blk], Hrows, ly.in_pad, ly.k_pad, self_ids, self_ids,
                                B.rowptr[blk], B.col[blk], B.trowptr[blk], ly.A, s);
             });
+        }
+        if (li == 0 && m->sample_after_l1) {   // the next batch's sampling may start now (see issue_sample)
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(s, &cs);
+            cudaEventRecordWithFlags(B.l1done, s, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                                    : cudaEventRecordDefault);
         }
         if (li == L - 1 && ly.n_pad <= 64) {
             // logits = A W with the softmax cross-entropy in the GEMM epilogue
@@ -552,6 +568,8 @@ gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const i
     // the step trained last, whichever set it used)
     static const bool serial = [] { const char* e = std::getenv("GS_SERIAL"); return e && e[0] == '1'; }();
     if (serial && m->last >= 0 && m->bs[m->last].trained_once) CK(cudaStreamWaitEvent(m->sstream, m->bs[m->last].trained, 0));
+    if (m->sample_after_l1 && m->last >= 0 && m->last != set && m->bs[m->last].trained_once)
+        CK(cudaStreamWaitEvent(m->sstream, m->bs[m->last].l1done, 0));
     const int32_t* src = seeds_dev;
     if (!src) {
         if (n) {
@@ -571,7 +589,10 @@ gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const i
     sp.tag = m->seq;
     sp.full = full ? 1 : 0;
     m->last_full = full;
+    cudaEvent_t ta = nullptr, tb = nullptr;
+    if (m->timeline) { ta = take_event(m); tb = take_event(m); CK(cudaEventRecord(ta, m->sstream)); }
     K(m, m->sstream, GNN_K_SAMPLE, [&] { launch_sample_step(sp, m->sstream); });
+    if (m->timeline) { CK(cudaEventRecord(tb, m->sstream)); m->tl_sample.emplace_back(ta, tb); }
     CK(cudaGetLastError());
     CK(cudaEventRecord(B.sampled, m->sstream));
     B.valid = true;
@@ -647,6 +668,8 @@ int other_set(gnn_model* m) { return m->last < 0 ? 0 : 1 - m->last; }
 gnn_status train_set(gnn_model* m, int set, float* loss_dst = nullptr) {
     BatchSet& B = m->bs[set];
     CK(cudaStreamWaitEvent(m->stream, B.sampled, 0));
+    cudaEvent_t ta = nullptr, tb = nullptr;
+    if (m->timeline) { ta = take_event(m); tb = take_event(m); CK(cudaEventRecord(ta, m->stream)); }
     if (m->cfg.use_graph && !m->profiling) {
         TRY(build_graph(m, set, false));
         CK(cudaGraphLaunch(B.gexec, m->stream));
@@ -666,6 +689,7 @@ gnn_status train_set(gnn_model* m, int set, float* loss_dst = nullptr) {
         enqueue_training(m, set);
         CK(cudaGetLastError());
     }
+    if (m->timeline) { CK(cudaEventRecord(tb, m->stream)); m->tl_train.emplace_back(ta, tb); }
     if (loss_dst) CK(cudaMemcpyAsync(loss_dst, &B.st->loss, sizeof(float), cudaMemcpyDefault, m->stream));
     CK(cudaEventRecord(B.trained, m->stream));
     B.trained_once = true;
@@ -1244,6 +1268,15 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         m->opt.beta1 = c.beta1; m->opt.beta2 = c.beta2; m->opt.eps = c.eps;
     }
 #undef AL
+    { const char* e = std::getenv("GS_TIMELINE"); m->timeline = e && e[0] == '1'; }
+    {   // default: on when layer 1 is the bulk-copy gather (SAGE + neighbour sampler, local table,
+        // rows <= 1 KB; dense.cu launch_agg_sage); GS_SAMPLE_AFTER_L1=0/1 overrides
+        const char* e = std::getenv("GS_SAMPLE_AFTER_L1");
+        const char* b = std::getenv("GS_L1_BULK");
+        const bool bulk = m->sage && !m->shadow && !g->nshards && g->stride * 4 <= 1024 && !(b && b[0] == '0');
+        m->sample_after_l1 = e ? e[0] == '1' : bulk;
+    }
+    for (auto& B : m->bs) CK(cudaEventCreateWithFlags(&B.l1done, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&m->sstream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&m->wstream, cudaStreamNonBlocking));
@@ -1277,6 +1310,7 @@ gnn_status gnn_model_destroy(gnn_model* m) {
         for (auto& p : B.prof_pairs) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
         if (B.sampled) cudaEventDestroy(B.sampled);
         if (B.trained) cudaEventDestroy(B.trained);
+        if (B.l1done) cudaEventDestroy(B.l1done);
     }
     if (m->comm) ncclCommDestroy(m->comm);
     for (void* p : m->xopened) cudaIpcCloseMemHandle(p);
@@ -1662,6 +1696,29 @@ gnn_status gnn_debug_get(gnn_model* m, int32_t what, float* out_host, int64_t n)
         if (need)
             CK(cudaMemcpy2D(out_host, sizeof(float) * ly.out, ly.H, sizeof(float) * ly.n_pad, sizeof(float) * ly.out,
                             st.batch_n, cudaMemcpyDeviceToHost));
+        return GNN_OK;
+    }
+    if (what == GNN_DBG_TIMELINE) {
+        // 4 values per step (µs from the first recorded training start): sampling start, sampling
+        // end, training start, training end (step k = k-th sampling and k-th training launch
+        // recorded; with overlap the k-th sampling belongs to training k+1); resets the record
+        const size_t k = std::min(m->tl_sample.size(), m->tl_train.size());
+        if (n < (int64_t)(4 * k + 1)) return fail(GNN_ERR_BUFFER, "need 4*steps+1 = " + std::to_string(4 * k + 1));
+        out_host[0] = (float)k;
+        if (k) {
+            cudaEvent_t t0 = m->tl_train[0].first;
+            auto rel = [&](cudaEvent_t e) { float ms = 0.f; cudaEventElapsedTime(&ms, t0, e); return ms * 1e3f; };
+            for (size_t i = 0; i < k; ++i) {
+                out_host[1 + 4 * i] = rel(m->tl_sample[i].first);
+                out_host[2 + 4 * i] = rel(m->tl_sample[i].second);
+                out_host[3 + 4 * i] = rel(m->tl_train[i].first);
+                out_host[4 + 4 * i] = rel(m->tl_train[i].second);
+            }
+        }
+        for (auto& v : {&m->tl_sample, &m->tl_train})
+            for (auto& pr : *v) { m->free_events.push_back(pr.first); m->free_events.push_back(pr.second); }
+        m->tl_sample.clear();
+        m->tl_train.clear();
         return GNN_OK;
     }
     if (what == GNN_DBG_REUSE) {   // steps whose batch was / was not found prefetched (since creation)

@@ -21,8 +21,7 @@ struct StepState {
     uint32_t ce_done;     // CE blocks finished (reset by the last one)
     uint32_t seq;         // step sequence number (tags the sampling kernel's scan words)
     int32_t n_rf;         // ShaDow: rows of the last layer's receptive field (compacted layer L-1)
-    int32_t l1_queue;     // row-chunk counter of the layer-1 bulk gather (zeroed by the sampling kernel)
-    int32_t pad2;
+    int32_t pad2[2];
     float row_loss[1024]; // ℓ_i of the batch rows (batch_size <= 1024)
 };
 

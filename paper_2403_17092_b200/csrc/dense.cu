@@ -197,7 +197,7 @@ template <int NB>
 __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __restrict__ rows_ptr,
         const float* __restrict__ X, int in_pad, const int32_t* __restrict__ smap,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col, Split A, int fixed_k, int slots,
-        int xpol, int apol, int32_t* __restrict__ queue) {
+        int xpol, int apol) {
     extern __shared__ __align__(128) unsigned char l1_smem[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     uint64_t* bar = reinterpret_cast<uint64_t*>(l1_smem) + warp * NB;
@@ -214,41 +214,24 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
     pdl_wait();
     const int n = *rows_ptr;
     const int nch = in_pad >> 2;
-    const int W = total_warps();
-    const int gw = global_warp();
+    const int64_t W = total_warps();
+    const int64_t gw = global_warp();
     // zero tail rows [n, round64(n)) of the operand planes
-    for (int i = n + gw; i < round64(n); i += W)
+    for (int64_t i = n + gw; i < round64(n); i += W)
         for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, tix(A, i, 4 * ch), kZero4);
     // L2 policies (A/B switches GS_L1_XPOL / GS_L1_APOL): feature rows 0 normal, 1 evict_last,
     // 2 evict_first; operand-plane stores 0 plain, 1 evict_first, 2 evict_last
     const uint64_t pol = xpol == 1 ? policy_evict_last() : xpol == 2 ? policy_evict_first() : policy_evict_normal();
     const uint64_t spol = apol == 2 ? policy_evict_last() : policy_evict_first();
-    // Destination rows in chunks of kL1Chunk from a queue (queue != null: an atomic counter zeroed
-    // by the sampling kernel; a block that starts late, its SM still held by the next batch's
-    // sampling kernel, just takes fewer chunks instead of holding up the whole grid); else static
-    // chunks gw, gw + W, ...  The next chunk is claimed one chunk ahead (its atomic overlaps work).
-    constexpr int kL1Chunk = 8;
-    int ck = 0;
-    auto claim = [&]() -> int {
-        if (!queue) return (gw + (ck++) * W) * kL1Chunk;
-        int v = 0;
-        if (lane == 0) v = atomicAdd(queue, kL1Chunk);
-        return __shfl_sync(0xffffffffu, v, 0);
-    };
-    int cur = claim(), left = kL1Chunk;
-    int nxt_chunk = claim();
-    auto next_row = [&]() -> int {
-        if (left == 0) { cur = nxt_chunk; left = kL1Chunk; nxt_chunk = claim(); }
-        return cur + (kL1Chunk - left--);
-    };
     // A destination row's indices: this lane's row to copy (lane 0: the self row, lane j: the
-    // neighbour j-1) and the row's degree, fetched one row ahead of their use.
+    // neighbour j-1) and the row's degree.  Fetched one row ahead of their use, so the index loads
+    // overlap the wait for the rows in flight instead of stalling the copy issue.
     struct Idx { int nb, self, c; };
-    auto fetch = [&](int i) {
+    auto fetch = [&](int64_t i) {
         Idx x{0, 0, 0};
         if (i >= n) return x;
         if (fixed_k) {   // fixed-stride rows: the count and the ids load in parallel
-            if (lane < fixed_k) x.nb = col[i * fixed_k + lane];
+            if (lane < fixed_k) x.nb = col[(int)i * fixed_k + lane];
             x.c = rowptr[i];
         } else {
             const int beg = rowptr[i];
@@ -269,73 +252,66 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
             bulk_g2s(buf + (size_t)lane * in_pad, X + (int64_t)r * in_pad, row_bytes, &bar[b], pol);
         }
     };
-    int row_of[NB], cnt[NB];
+    int cnt[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-        row_of[b] = next_row();
-        const Idx x = fetch(row_of[b]);
+        const int64_t i = gw + b * W;
+        const Idx x = fetch(i);
         cnt[b] = x.c;
-        if (row_of[b] < n) issue(b, x);
+        if (i < n) issue(b, x);
     }
-    int ipend = next_row();
-    Idx pend = fetch(ipend);   // the row that re-arms the first freed buffer
-    uint32_t phase = 0;        // parity of every buffer's current use (buffers used round-robin)
-    bool done = false;
-    while (!done) {
+    Idx pend = fetch(gw + (int64_t)NB * W);   // the row that re-arms the first freed buffer
+    uint32_t phase = 0;   // parity bit of every buffer's current use (buffers are used round-robin)
+    int b = 0;
+    for (int64_t i = gw; i < n; i += W) {
+        const Idx nxt = fetch(i + (int64_t)(NB + 1) * W);   // loads in flight during this row
+        mbar_wait(&bar[b], phase);
+        const float* buf = ring + (size_t)b * slots * in_pad;
+        int c = cnt[0];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {   // unrolled: b is a constant, row_of / cnt stay in registers
-            if (done) break;
-            const int i = row_of[b];
-            if (i >= n) { done = true; break; }
-            const int inxt = ipend < n ? next_row() : n;
-            const Idx nxt = fetch(inxt);   // loads in flight during this row
-            mbar_wait(&bar[b], phase);
-            const float* buf = ring + (size_t)b * slots * in_pad;
-            const int c = cnt[b];
-            float4 sv = kZero4, acc = kZero4;
+        for (int q = 1; q < NB; ++q) if (b == q) c = cnt[q];
+        float4 sv = kZero4, acc = kZero4;
+        if (lane < nch) {
+            sv = reinterpret_cast<const float4*>(buf)[lane];
+            for (int j = 1; j <= c; ++j) acc = f4add(acc, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane]);
+        }
+        // rows of more than 128 floats: lanes take further chunks
+        float4 sv2 = kZero4, acc2 = kZero4;
+        const bool wide = nch > 32;
+        if (wide && lane + 32 < nch) {
+            sv2 = reinterpret_cast<const float4*>(buf)[lane + 32];
+            for (int j = 1; j <= c; ++j) acc2 = f4add(acc2, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane + 32]);
+        }
+        // the buffer is read: re-arm it with this warp's row i + NB*W (async-proxy writes after
+        // generic-proxy reads of the same shared memory need the proxy fence)
+        fence_async_smem();
+        __syncwarp();
+        const bool more = i + (int64_t)NB * W < n;
+        if (more) issue(b, pend);
+#pragma unroll
+        for (int q = 0; q < NB; ++q) if (b == q) cnt[q] = more ? pend.c : 0;
+        pend = nxt;
+        const float inv = c ? 1.0f / (float)c : 0.f;   // one division per row (R23)
+        if (apol) {
             if (lane < nch) {
-                sv = reinterpret_cast<const float4*>(buf)[lane];
-                for (int j = 1; j <= c; ++j) acc = f4add(acc, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane]);
+                store_split4_pol(A, tix(A, i, 4 * lane), sv, spol);
+                store_split4_pol(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv), spol);
             }
-            // rows of more than 128 floats: lanes take further chunks
-            float4 sv2 = kZero4, acc2 = kZero4;
-            const bool wide = nch > 32;
             if (wide && lane + 32 < nch) {
-                sv2 = reinterpret_cast<const float4*>(buf)[lane + 32];
-                for (int j = 1; j <= c; ++j) acc2 = f4add(acc2, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane + 32]);
+                store_split4_pol(A, tix(A, i, 4 * (lane + 32)), sv2, spol);
+                store_split4_pol(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv), spol);
             }
-            // the buffer is read: re-arm it with the pending row (async-proxy writes after
-            // generic-proxy reads of the same shared memory need the proxy fence)
-            fence_async_smem();
-            __syncwarp();
-            const bool more = ipend < n;
-            if (more) issue(b, pend);
-            cnt[b] = more ? pend.c : 0;
-            row_of[b] = more ? ipend : n;
-            pend = nxt;
-            ipend = inxt;
-            const float inv = c ? 1.0f / (float)c : 0.f;   // one division per row (R23)
-            if (apol) {
-                if (lane < nch) {
-                    store_split4_pol(A, tix(A, i, 4 * lane), sv, spol);
-                    store_split4_pol(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv), spol);
-                }
-                if (wide && lane + 32 < nch) {
-                    store_split4_pol(A, tix(A, i, 4 * (lane + 32)), sv2, spol);
-                    store_split4_pol(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv), spol);
-                }
-            } else {
-                if (lane < nch) {
-                    store_split4(A, tix(A, i, 4 * lane), sv);
-                    store_split4(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv));
-                }
-                if (wide && lane + 32 < nch) {
-                    store_split4(A, tix(A, i, 4 * (lane + 32)), sv2);
-                    store_split4(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv));
-                }
+        } else {
+            if (lane < nch) {
+                store_split4(A, tix(A, i, 4 * lane), sv);
+                store_split4(A, tix(A, i, 4 * (nch + lane)), f4scale(acc, inv));
+            }
+            if (wide && lane + 32 < nch) {
+                store_split4(A, tix(A, i, 4 * (lane + 32)), sv2);
+                store_split4(A, tix(A, i, 4 * (nch + lane + 32)), f4scale(acc2, inv));
             }
         }
-        phase ^= 1u;
+        if (++b == NB) { b = 0; phase ^= 1u; }
     }
 }
 
@@ -1075,9 +1051,7 @@ int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
 template <int NB>
 static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, const int32_t* smap,
                            const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k, int slots,
-                           int32_t* queue, cudaStream_t s) {
-    static const int dyn = [] { const char* e = std::getenv("GS_L1_DYN"); return e ? std::atoi(e) : 1; }();
-    if (!dyn) queue = nullptr;
+                           cudaStream_t s) {
     size_t smem = 128 + (size_t)kL1Warps * NB * slots * in_pad * 4;
     if (smem > 200 * 1024) return false;
     // GS_L1_BPS = b: pad the request just past the (b+1)-blocks threshold, so that at most b blocks
@@ -1106,28 +1080,28 @@ static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, 
     static const int pdl = [] { const char* e = std::getenv("GS_L1_PDL"); return e ? std::atoi(e) : 1; }();
     if (pdl)
         launch_pdl(k_agg_l1_bulk<NB>, grid, kL1Warps * 32, smem, s, rows_ptr, X, in_pad, smap, blk_rowptr, col, A,
-                   fixed_k, slots, xpol, apol, queue);
+                   fixed_k, slots, xpol, apol);
     else
     {
         apply_carveout((const void*)k_agg_l1_bulk<NB>);
         k_agg_l1_bulk<NB><<<grid, kL1Warps * 32, smem, s>>>(rows_ptr, X, in_pad, smap, blk_rowptr, col, A, fixed_k,
-                                                           slots, xpol, apol, queue);
+                                                           slots, xpol, apol);
     }
     return true;
 }
 
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
-                     int k_max, int32_t* queue, cudaStream_t s) {
+                     int k_max, cudaStream_t s) {
     // layer 1 of the neighbour sampler on a local table: rows staged by the bulk-copy engine
     // (GS_L1_BULK=0: register loads, for A/B; GS_L1_NB: buffers per warp)
     static const int bulk = [] { const char* e = std::getenv("GS_L1_BULK"); return e ? std::atoi(e) : 1; }();
     static const int nb = [] { const char* e = std::getenv("GS_L1_NB"); return e ? std::atoi(e) : 2; }();
     if (bulk && !H.shards && !gmap && smap && k_max > 0 && k_max <= 31 && in_pad * 4 <= 1024) {
         const bool ok = nb == 3 ? launch_l1_bulk<3>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
-                                                     1 + k_max, queue, s)
+                                                     1 + k_max, s)
                                 : launch_l1_bulk<2>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
-                                                     1 + k_max, queue, s);
+                                                     1 + k_max, s);
         if (ok) return;
     }
     // A/B diagnostic only: GS_AGG_DUMMY_SMEM = bytes of (unused) dynamic shared memory for the

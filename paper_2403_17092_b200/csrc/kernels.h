@@ -161,7 +161,7 @@ void launch_cache_fill(FeatRows src, const int32_t* ids, int64_t n, int ld, floa
 // (rows have at most k_max sources); layer 1 on a local table then stages rows by bulk copy.
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
-                     int k_max, int32_t* queue, cudaStream_t s);   // queue: row-chunk counter, zeroed per batch (nullable)
+                     int k_max, cudaStream_t s);
 // GCN aggregation A = Â H (self loop included) for rows i < *rows_ptr of a block with
 // *ndst_ptr destinations; d_out from the transposed row pointer.  col must be local ids.
 void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,

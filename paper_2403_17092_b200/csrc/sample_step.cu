@@ -292,7 +292,6 @@ __global__ void __launch_bounds__(kThreads, GS_SAMPLE_MINB) k_sample_step(Sample
         st->g = g;
         st->loss = 0.f;
         st->seq = tag;
-        st->l1_queue = 0;
     }
     for (int i = gtid; i < P.n_seeds; i += nthreads) {   // nodes[i] = seed_i, map[seed_i] = i
         const int v = P.seed_src[i];

@@ -1,10 +1,13 @@
 #!/bin/bash
-# One round-end measurement pass on a GPU box: the ncu launch list of the bench workload (and the
-# per-class DRAM traffic it implies, read by bench.py), bench lines for every workload, one
-# --set full capture of a step, sampling phase times and the random-gather ceiling.
+# One measurement pass on a GPU box (round 2): the full -m gpu suite, smoke, ncu launch lists of the
+# bench workloads (and the per-class DRAM traffic bench.py reads), bench lines for every workload,
+# one --set full capture of a products step, sampling phases, the timeline, the gather ceiling,
+# the reference arm, compute-sanitizer logs of the tiny configs.
 set -u
 out=${1:-gpurun_out/final}
 mkdir -p "$out"
+timeout 2400 python -m pytest tests -m gpu -q -s > "$out/gpu_tests.log" 2>&1; echo "rc=$?" >> "$out/gpu_tests.log"
+python -c "import __graft_entry__ as g; g.smoke()" > "$out/smoke.log" 2>&1
 for c in products reddit products_shadow; do
     ncu --nvtx --nvtx-include "steps/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
         --clock-control none --csv --log-file "$out/launches_$c.csv" python tools/profile_step.py --config $c --steps 2 --graph \
@@ -13,14 +16,18 @@ for c in products reddit products_shadow; do
 done
 cp profiles/ncu_traffic.json "$out/ncu_traffic.json"
 python bench.py > "$out/bench_products.json" 2> "$out/bench_products.err"
-for c in reddit products_shadow products_gcn products_sage_shadow products_shadow_l5 tiny; do
+python bench.py --steps 400 --warmup 20 > "$out/bench_products_long.json" 2> "$out/bench_products_long.err"
+for c in reddit products_shadow products_gcn products_sage_shadow products_shadow_l5 tiny papers100m; do
     python bench.py --config $c --no-cpu-baseline > "$out/bench_$c.json" 2> "$out/bench_$c.err"
 done
 python bench.py --precision bf16 --no-cpu-baseline > "$out/bench_products_bf16.json" 2> "$out/bench_products_bf16.err"
+python bench.py --optimizer adam --no-cpu-baseline > "$out/bench_products_adam.json" 2> "$out/bench_products_adam.err"
 python bench.py --impl reference --steps 2 --warmup 0 > "$out/bench_reference.json" 2> "$out/bench_reference.err"
 ncu --nvtx --nvtx-include "steps/" --set full --import-source on --clock-control none -o "$out/step_full" \
     python tools/profile_step.py --config products --steps 1 --graph > "$out/ncu_full.log" 2>&1
 python tools/phase_times.py products > "$out/phases_products.txt" 2>&1
-python tools/phase_times.py products_shadow > "$out/phases_products_shadow.txt" 2>&1
+python tools/timeline.py products 30 > "$out/timeline_products.txt" 2>&1
 python tools/gather_ceiling.py > "$out/gather_ceiling.txt" 2>&1
-python bench.py --optimizer adam --no-cpu-baseline > "$out/bench_products_adam.json" 2> "$out/bench_products_adam.err"
+timeout 900 compute-sanitizer --tool memcheck python tools/sanitize.py > "$out/sanitize_memcheck.log" 2>&1
+timeout 900 compute-sanitizer --tool racecheck python tools/sanitize.py > "$out/sanitize_racecheck.log" 2>&1
+timeout 900 compute-sanitizer --tool synccheck python tools/sanitize.py > "$out/sanitize_synccheck.log" 2>&1
