@@ -295,8 +295,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         m.comm_init(rank, world, obj[0])
     # a real (non-legacy) stream shared by torch's events and the library's launches
-    # (GS_SAMPLE_PRIO=low: the training stream at the highest priority, sampling at the lowest)
-    stream = torch.cuda.Stream(priority=-1 if os.environ.get("GS_SAMPLE_PRIO") == "low" else 0)
+    stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     m.set_stream(stream)
     steps_per_epoch = (w.n_batches + world - 1) // world

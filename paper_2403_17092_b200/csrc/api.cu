@@ -1278,18 +1278,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     }
     for (auto& B : m->bs) CK(cudaEventCreateWithFlags(&B.l1done, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
-    {   // sampling stream priority (A/B switch GS_SAMPLE_PRIO = low | high; default: the default
-        // priority).  Lower numbers are higher priorities.
-        int lo = 0, hi = 0;
-        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        const char* e = std::getenv("GS_SAMPLE_PRIO");
-        const int prio = !e ? 0 : (std::strcmp(e, "low") == 0 ? lo : std::strcmp(e, "high") == 0 ? hi : 0);
-        CK(cudaStreamCreateWithPriority(&m->sstream, cudaStreamNonBlocking, prio));
-        // the library's own training stream: the highest priority under GS_SAMPLE_PRIO=low
-        if (e && std::strcmp(e, "low") == 0) {
-            CK(cudaStreamDestroy(m->own_stream));
-            CK(cudaStreamCreateWithPriority(&m->own_stream, cudaStreamNonBlocking, hi));
-        }
+    CK(cudaStreamCreateWithFlags(&m->sstream, cudaStreamNonBlocking));
     }
     CK(cudaStreamCreateWithFlags(&m->wstream, cudaStreamNonBlocking));
     for (int li = 0; li < m->L; ++li) CK(cudaEventCreateWithFlags(&m->ev_dpre[li], cudaEventDisableTiming));

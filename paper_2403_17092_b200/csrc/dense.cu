@@ -85,12 +85,21 @@ __device__ __forceinline__ void prefetch_rows_l2(const float* a, const float* b,
     }
 }
 constexpr float4 kZero4 = {0.f, 0.f, 0.f, 0.f};
+// Row r of an aggregation input.  SH: the row-sharded table (FeatRows::row picks local shard /
+// cache replica / peer, with the optional read counters); else plain pointer arithmetic.  The
+// kernels are instantiated per case so the local-table gathers carry no shard branches or atomics
+// (with them inlined the compiler serialised the in-flight row loads: Reddit gather 96 -> 111 µs).
+template <bool SH>
+__device__ __forceinline__ const float4* frow(const FeatRows& H, int r, int ld) {
+    if constexpr (SH) return reinterpret_cast<const float4*>(H.row(r, ld));
+    else return reinterpret_cast<const float4*>(H.base + (int64_t)r * ld);
+}
 
 // ------------------------------------------------------------------ forward aggregation
 // Warp per destination row; lanes own 16-byte chunks of the feature row (CPL chunks each).
 // Neighbour indices are fetched 32 at a time by the warp and broadcast with shuffles; the
 // sum runs in CSR row order with plain fp32 adds, then a true division by the degree.
-template <int CPL>
+template <int CPL, bool SH>
 __global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
         FeatRows H, int in_pad, const int32_t* __restrict__ gmap,
         const int32_t* __restrict__ smap, const int32_t* __restrict__ rowptr,
@@ -108,7 +117,7 @@ __global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
             continue;
         }
         // the self row does not depend on the edge chain: issue its loads first
-        const float4* ps = reinterpret_cast<const float4*>(H.row(smap ? smap[i] : i, in_pad));
+        const float4* ps = frow<SH>(H, smap ? smap[i] : i, in_pad);
         float4 sv[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) sv[c] = (lane + 32 * c) < nch ? __ldg(ps + lane + 32 * c) : kZero4;
@@ -130,7 +139,7 @@ __global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
                 float4 v[kAggU][CPL];
 #pragma unroll
                 for (int u = 0; u < kAggU; ++u) {
-                    const float4* pu = reinterpret_cast<const float4*>(H.row(__shfl_sync(kFull, myidx, q + u), in_pad));
+                    const float4* pu = frow<SH>(H, __shfl_sync(kFull, myidx, q + u), in_pad);
 #pragma unroll
                     for (int c = 0; c < CPL; ++c) {
                         const int ch = lane + 32 * c;
@@ -144,8 +153,8 @@ __global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
             }
             for (; q + 2 <= m; q += 2) {
                 const int r0 = __shfl_sync(kFull, myidx, q), r1 = __shfl_sync(kFull, myidx, q + 1);
-                const float4* p0 = reinterpret_cast<const float4*>(H.row(r0, in_pad));
-                const float4* p1 = reinterpret_cast<const float4*>(H.row(r1, in_pad));
+                const float4* p0 = frow<SH>(H, r0, in_pad);
+                const float4* p1 = frow<SH>(H, r1, in_pad);
                 float4 v0[CPL], v1[CPL];
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
@@ -158,7 +167,7 @@ __global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
             }
             if (q < m) {
                 const int r0 = __shfl_sync(kFull, myidx, q);
-                const float4* p0 = reinterpret_cast<const float4*>(H.row(r0, in_pad));
+                const float4* p0 = frow<SH>(H, r0, in_pad);
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
 
 // GCN: A[i] = Σ_e H[c_e] / sqrt(d_in(i) d_out(c_e)) + H[i] / sqrt(d_in(i) d_out(i)),
 // d_in(i) = deg(i) + 1, d_out(c) = outdeg_blk(c) + [c < n_dst]  (R12).
-template <int CPL>
+template <int CPL, bool SH>
 __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ rows_ptr,
         const int32_t* __restrict__ ndst_ptr, FeatRows H, int in_pad, int lda,
         const int32_t* __restrict__ gmap, const int32_t* __restrict__ smap,
@@ -353,7 +362,7 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
             for (int q = 0; q < m; ++q) {
                 const int r = __shfl_sync(kFull, myrow, q);
                 const float w = __shfl_sync(kFull, myw, q);
-                const float4* p = reinterpret_cast<const float4*>(H.row(r, in_pad));
+                const float4* p = frow<SH>(H, r, in_pad);
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(256) k_agg_gcn(const int32_t* __restrict__ row
         const float dself = (float)(trowptr[i + 1] - trowptr[i] + 1);
         const float ws = 1.0f / sqrtf(din * dself);
         const int self = smap ? smap[i] : i;
-        const float4* ps = reinterpret_cast<const float4*>(H.row(self, in_pad));
+        const float4* ps = frow<SH>(H, self, in_pad);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
             const int ch = lane + 32 * c;
@@ -545,7 +554,7 @@ struct BalArgs {
     const int32_t* dmap;
 };
 
-template <int CPL, int MODE>   // MODE: 0 FWD SAGE, 1 FWD GCN, 2 BWD SAGE, 3 BWD GCN
+template <int CPL, int MODE, bool SH = false>   // MODE: 0 FWD SAGE, 1 FWD GCN, 2 BWD SAGE, 3 BWD GCN
 __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
     constexpr bool BWD = MODE >= 2, GCN = (MODE & 1) != 0;
     pdl_trigger();
@@ -573,7 +582,7 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
     auto finish = [&](int r, int R, int rb, int re, float4 (&acc)[CPL], bool any) {
         if constexpr (!BWD) {
             const int self = a.gmap ? a.gmap[R] : R;
-            const float4* ps = reinterpret_cast<const float4*>(a.H.row(self, a.in_pad));
+            const float4* ps = frow<SH>(a.H, self, a.in_pad);
             if constexpr (GCN) {
                 const float din = (float)(re - rb + 1);
                 const float dself = (float)(a.orow[R + 1] - a.orow[R] + (R < ndst ? 1 : 0));
@@ -700,7 +709,7 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
                         ww[j] = __shfl_sync(kFull, myw, min(q + j, 31));
                         if (q + j >= mv) rr[j] = -1;
                         const float4* p;
-                        if constexpr (!BWD) p = reinterpret_cast<const float4*>(a.H.row(max(rr[j], 0), a.in_pad)) + c0;
+                        if constexpr (!BWD) p = frow<SH>(a.H, max(rr[j], 0), a.in_pad) + c0;
                         else p = reinterpret_cast<const float4*>(a.dA + (int64_t)max(rr[j], 0) * ldd) + (GCN ? 0 : nch) + c0;
 #pragma unroll
                         for (int c = 0; c < CPL; ++c) {
@@ -753,8 +762,8 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
 // Forward and backward instantiations differ in register demand: the backward ones are capped
 // at 3 blocks/SM (<= 85 registers; uncapped the GCN backward compiles to 101, 2 blocks/SM),
 // the forward ones keep the compiler's choice (a cap measured slower).
-template <int CPL, int MODE>
-__global__ void __launch_bounds__(256) k_agg_bal(BalArgs a) { agg_bal_body<CPL, MODE>(a); }
+template <int CPL, int MODE, bool SH>
+__global__ void __launch_bounds__(256) k_agg_bal(BalArgs a) { agg_bal_body<CPL, MODE, SH>(a); }
 template <int CPL, int MODE>
 __global__ void __launch_bounds__(256, 3) k_agg_bal_bwd(BalArgs a) { agg_bal_body<CPL, MODE>(a); }
 
@@ -1036,17 +1045,26 @@ __global__ void k_init(float* p, int64_t cnt, float bound, uint64_t seed, uint32
 int cpl_of(int in_pad) { return (in_pad / 4 + 31) / 32; }
 }  // namespace
 
-#define GS_CPL_DISPATCH(cpl, KERNEL, ...)                                           \
-    switch (cpl) {                                                                  \
-        case 1: launch_pdl(KERNEL<1>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
-        case 2: launch_pdl(KERNEL<2>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
-        case 3: launch_pdl(KERNEL<3>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
-        case 4: launch_pdl(KERNEL<4>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
-        case 5: launch_pdl(KERNEL<5>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
-        case 6: launch_pdl(KERNEL<6>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
-        case 7: launch_pdl(KERNEL<7>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;            \
-        default: launch_pdl(KERNEL<8>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;           \
+#define GS_CPL_DISPATCH_SH(cpl, SHV, KERNEL, ...)                                       \
+    switch (cpl) {                                                                      \
+        case 1: launch_pdl(KERNEL<1, SHV>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;       \
+        case 2: launch_pdl(KERNEL<2, SHV>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;       \
+        case 3: launch_pdl(KERNEL<3, SHV>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;       \
+        case 4: launch_pdl(KERNEL<4, SHV>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;       \
+        case 5: launch_pdl(KERNEL<5, SHV>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;       \
+        case 6: launch_pdl(KERNEL<6, SHV>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;       \
+        case 7: launch_pdl(KERNEL<7, SHV>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;       \
+        default: launch_pdl(KERNEL<8, SHV>, kWarpGrid, 256, 0, s, __VA_ARGS__); break;      \
     }
+// local table, or the row-sharded one (FeatRows::shards set; GS_AGG_FORCE_SH=1: the sharded
+// instantiation for local tables too, A/B of the code generation only)
+static bool force_sh() {
+    static const bool f = [] { const char* e = std::getenv("GS_AGG_FORCE_SH"); return e && e[0] == '1'; }();
+    return f;
+}
+#define GS_CPL_DISPATCH(cpl, H, KERNEL, ...)                                             \
+    if ((H).shards || force_sh()) { GS_CPL_DISPATCH_SH(cpl, true, KERNEL, __VA_ARGS__) }   \
+    else { GS_CPL_DISPATCH_SH(cpl, false, KERNEL, __VA_ARGS__) }
 
 template <int NB>
 static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, const int32_t* smap,
@@ -1107,20 +1125,20 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
     // A/B diagnostic only: GS_AGG_DUMMY_SMEM = bytes of (unused) dynamic shared memory for the
     // register-load layer-1 gather (does a shared-memory footprint alone change the step?)
     static const int dummy = [] { const char* e = std::getenv("GS_AGG_DUMMY_SMEM"); return e ? std::atoi(e) : 0; }();
-    if (dummy && k_max > 0 && !gmap && cpl_of(in_pad) == 1) {
+    if (dummy && k_max > 0 && !gmap && !H.shards && cpl_of(in_pad) == 1) {
         static bool set = false;
-        if (!set) { cudaFuncSetAttribute(k_agg_sage<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, dummy); set = true; }
-        launch_pdl(k_agg_sage<1>, kWarpGrid, 256, (size_t)dummy, s, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A,
+        if (!set) { cudaFuncSetAttribute(k_agg_sage<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dummy); set = true; }
+        launch_pdl(k_agg_sage<1, false>, kWarpGrid, 256, (size_t)dummy, s, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A,
                    fixed_k);
         return;
     }
-    GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A, fixed_k);
+    GS_CPL_DISPATCH(cpl_of(in_pad), H, k_agg_sage, rows_ptr, H, in_pad, gmap, smap, blk_rowptr, col, A, fixed_k);
 }
 
 void launch_agg_gcn(const int32_t* rows_ptr, const int32_t* ndst_ptr, FeatRows H, int in_pad, int lda,
                     const int32_t* gmap, const int32_t* smap, const int32_t* blk_rowptr,
                     const int32_t* col, const int32_t* trowptr, Split A, cudaStream_t s) {
-    GS_CPL_DISPATCH(cpl_of(in_pad), k_agg_gcn, rows_ptr, ndst_ptr, H, in_pad, lda, gmap, smap, blk_rowptr,
+    GS_CPL_DISPATCH(cpl_of(in_pad), H, k_agg_gcn, rows_ptr, ndst_ptr, H, in_pad, lda, gmap, smap, blk_rowptr,
                     col, trowptr, A);
 }
 
@@ -1150,7 +1168,8 @@ static void launch_agg_bal_panel(const BalArgs& a, int mode, int nchp, cudaStrea
     const int c = cpl <= 1 ? 1 : cpl <= 2 ? 2 : cpl <= 4 ? 4 : 8;
 #define GS_BAL(C, M) if (c == C && mode == M) {                                                  \
         if constexpr (M >= 2) launch_pdl(k_agg_bal_bwd<C, M>, kWarpGrid, 256, 0, s, a);            \
-        else launch_pdl(k_agg_bal<C, M>, kWarpGrid, 256, 0, s, a);                                 \
+        else if (a.H.shards) launch_pdl(k_agg_bal<C, M, true>, kWarpGrid, 256, 0, s, a);           \
+        else launch_pdl(k_agg_bal<C, M, false>, kWarpGrid, 256, 0, s, a);                          \
         return;                                                                                   \
     }
     GS_BAL(1, 0) GS_BAL(1, 1) GS_BAL(1, 2) GS_BAL(1, 3)

@@ -109,7 +109,7 @@ template <int BN>
 struct TileCfg {
     static constexpr int kAStage = kBM * kBK * 2;                    // 16 KB per plane
     static constexpr int kBStage = ((BN + 63) / 64) * 64 * kBK * 2;  // whole 64-wide boxes (MN-major)
-    static constexpr int kAccCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;   // one accumulator
+    static constexpr int kAccCols = BN <= 32 ? 32 : BN <= 64 ? 64 : 128;      // one accumulator
     static constexpr int kTmemCols = 2 * kAccCols;                            // double buffered
     // bytes one stage's TMA boxes deliver (OOB parts are zero-filled but still counted)
     static constexpr int kBBytesK = BN * kBK * 2;                     // K-major: box {64, BN}
@@ -559,9 +559,6 @@ cudaError_t dispatch_bn(int bn, int grid, const TcGemmMaps& mp, const GemmArgs& 
         case 64: return launch_tc<64, 4, TERMS, MODE>(grid, mp, a, s);
         case 96: return launch_tc<96, GS_TC_STAGES_WIDE, TERMS, MODE>(grid, mp, a, s);
         case 128: return launch_tc<128, GS_TC_STAGES_WIDE, TERMS, MODE>(grid, mp, a, s);
-        case 256:   // forward only: the whole 256-wide output row in one tile (A read once), 2 stages
-            if constexpr (MODE == 2) return launch_tc<256, 2, TERMS, MODE>(grid, mp, a, s);
-            return cudaErrorInvalidValue;
         default: return cudaErrorInvalidValue;
     }
 }
@@ -594,9 +591,7 @@ static int gemm_diag() {
 cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_static,
                            int m_cap, int n_pad, int k_pad, float* C, int ldc, int n_store, bool relu, int splits,
                            int64_t split_stride, cudaStream_t s, uint32_t* relu_mask, int mask_ld) {
-    // GS_TC_BN256=1 (A/B): forward GEMMs with a 256-wide output take one 128 x 256 tile per row block
-    static const bool bn256 = [] { const char* e = getenv("GS_TC_BN256"); return e && e[0] == '1'; }();
-    const int bn = (bn256 && mode == 2 && n_pad == 256) ? 256 : tc_tile_n(n_pad);
+    const int bn = tc_tile_n(n_pad);
     GemmArgs a{};
     a.mask = relu ? relu_mask : nullptr;
     a.mask_ld = mask_ld;
