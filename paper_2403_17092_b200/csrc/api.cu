@@ -1279,7 +1279,6 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     for (auto& B : m->bs) CK(cudaEventCreateWithFlags(&B.l1done, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&m->sstream, cudaStreamNonBlocking));
-    }
     CK(cudaStreamCreateWithFlags(&m->wstream, cudaStreamNonBlocking));
     for (int li = 0; li < m->L; ++li) CK(cudaEventCreateWithFlags(&m->ev_dpre[li], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
