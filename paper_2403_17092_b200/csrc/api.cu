@@ -113,6 +113,7 @@ namespace {
 struct HopBufs {
     int64_t cap_dst = 0, cap_edges = 0, cap_src = 0;
     bool need_t = false;
+    bool count_only = false;   // only the out-degrees (transposed row pointer): GCN's layer-1 block
     int32_t *tcount = nullptr, *tcursor = nullptr, *tdst = nullptr;   // shared by both batch sets
     int32_t* erow = nullptr;             // destination row of every edge (transposed fill)
 };
@@ -1068,6 +1069,9 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         b.cap_src = std::min<int64_t>(g->N, cap_dst + b.cap_edges);
         b.cap_src = std::max(b.cap_src, cap_dst);
         b.need_t = !m->shadow && (!m->sage || h <= m->L - 2);
+        // GCN's layer-1 block (the last hop) needs only d_out for its normalisation: no backward
+        // aggregation runs over it, so its transposed block is not filled or sorted
+        b.count_only = !m->shadow && !m->sage && h == m->hops - 1;
         cap_dst = b.cap_src;
     }
     m->nodes_cap = m->hb[m->hops - 1].cap_src;
@@ -1105,8 +1109,10 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         if (b.need_t) {
             AL(b.tcount, b.cap_src + 1);
             AL(b.tcursor, b.cap_src + 1);
-            AL(b.erow, b.cap_edges);
-            AL(b.tdst, b.cap_edges);
+            if (!b.count_only) {
+                AL(b.erow, b.cap_edges);
+                AL(b.tdst, b.cap_edges);
+            }
             CK(cudaMemset(b.tcount, 0, sizeof(int32_t) * (b.cap_src + 1)));
         }
     }
@@ -1145,7 +1151,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
             if (h < m->hops) AL(B.nbr[h], b.cap_edges);
             if (b.need_t) {
                 AL(B.trowptr[h], b.cap_src + 1);
-                AL(B.tdst_s[h], b.cap_edges);
+                if (!b.count_only) AL(B.tdst_s[h], b.cap_edges);
             }
             HopIO& io = sp.hop[h];
             io.k = h < m->hops ? c.fanouts[m->hops - 1 - h] : 0;
@@ -1153,6 +1159,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
             io.tcount = b.need_t ? b.tcount : nullptr;
             io.trowptr = B.trowptr[h]; io.tcursor = b.tcursor; io.tdst = b.tdst; io.tdst_s = B.tdst_s[h];
             io.erow = b.need_t ? b.erow : nullptr;
+            io.count_only = b.count_only ? 1 : 0;
         }
     }
 
@@ -1269,11 +1276,12 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     }
 #undef AL
     { const char* e = std::getenv("GS_TIMELINE"); m->timeline = e && e[0] == '1'; }
-    {   // default: on when layer 1 is the bulk-copy gather (SAGE + neighbour sampler, local table,
-        // rows <= 1 KB; dense.cu launch_agg_sage); GS_SAMPLE_AFTER_L1=0/1 overrides
+    {   // default: on when layer 1 is a bulk-copy gather (SAGE + neighbour sampler, local table,
+        // k_agg_l1_bulk / k_agg_l1_stream; dense.cu launch_agg_sage); GS_SAMPLE_AFTER_L1=0/1 overrides
         const char* e = std::getenv("GS_SAMPLE_AFTER_L1");
         const char* b = std::getenv("GS_L1_BULK");
-        const bool bulk = m->sage && !m->shadow && !g->nshards && g->stride * 4 <= 1024 && !(b && b[0] == '0');
+        const bool bulk = m->sage && !m->shadow && !g->nshards && g->stride <= 1024 && c.fanouts[0] <= 31 &&
+                          !(b && b[0] == '0');
         m->sample_after_l1 = e ? e[0] == '1' : bulk;
     }
     for (auto& B : m->bs) CK(cudaEventCreateWithFlags(&B.l1done, cudaEventDisableTiming));

@@ -324,6 +324,129 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
     }
 }
 
+// ------------------------------------------------------------------ layer-1 gather, wide rows
+// k_agg_l1_bulk for rows wider than 1 KB (Reddit: 604 floats = 2.4 KB): a destination row's items
+// (self row, then its c neighbours in CSR order) are streamed through the warp's NB buffers in
+// chunks of G rows (G sized so the buffers of 4 warps fit one block per SM, 7 for Reddit); the
+// warp accumulates a row over its chunks and writes [self | mean] after the last one.  Same
+// arithmetic and order as k_agg_sage (bit-identical operand planes).
+template <int NB, int CPL>
+__global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_stream(const int32_t* __restrict__ rows_ptr,
+        const float* __restrict__ X, int in_pad, const int32_t* __restrict__ smap,
+        const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col, Split A, int fixed_k, int G) {
+    extern __shared__ __align__(128) unsigned char l1_smem[];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    uint64_t* bar = reinterpret_cast<uint64_t*>(l1_smem) + warp * NB;
+    const uint32_t row_bytes = (uint32_t)in_pad * 4u;
+    float* ring = reinterpret_cast<float*>(l1_smem + 128 + (size_t)warp * NB * G * row_bytes);
+    if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_async_smem();
+    }
+    __syncwarp();
+    pdl_trigger();
+    pdl_wait();
+    const int n = *rows_ptr;
+    const int nch = in_pad >> 2;
+    const int W = total_warps();
+    const int gw = global_warp();
+    for (int i = n + gw; i < round64(n); i += W)
+        for (int ch = lane; ch < 2 * nch; ch += 32) store_split4(A, tix(A, i, 4 * ch), kZero4);
+    const uint64_t pol = policy_evict_normal();
+    struct Idx { int nb, self, c; };
+    auto fetch = [&](int i) {
+        Idx x{0, 0, 0};
+        if (i >= n) return x;
+        if (fixed_k) {
+            if (lane < fixed_k) x.nb = col[i * fixed_k + lane];
+            x.c = rowptr[i];
+        } else {
+            const int beg = rowptr[i];
+            x.c = rowptr[i + 1] - beg;
+            if (lane < x.c) x.nb = col[beg + lane];
+        }
+        x.self = smap[i];
+        return x;
+    };
+    // producer state: the row being issued (its indices), the chunk within it, the next row
+    int prow = gw, pq = 0;
+    Idx px = fetch(prow);
+    int nrow = gw + W;
+    Idx nx = fetch(nrow);
+    int mrow[NB], mq[NB], mitems[NB], mlast[NB];   // what each buffer holds
+    auto issue = [&](int b) {
+        if (prow >= n) { mrow[b] = n; return; }
+        const int tot = px.c + 1;                    // items of the row: self + neighbours
+        const int items = min(G, tot - pq * G);
+        float* buf = ring + (size_t)b * G * in_pad;
+        if (lane == 0) mbar_expect_tx(&bar[b], (uint32_t)items * row_bytes);
+        __syncwarp();
+        const int it = pq * G + lane;                // this lane's item
+        const int nbv = __shfl_sync(0xffffffffu, px.nb, max(it - 1, 0) & 31);
+        if (lane < items) {
+            const int r = it == 0 ? px.self : nbv;
+            bulk_g2s(buf + (size_t)lane * in_pad, X + (int64_t)r * in_pad, row_bytes, &bar[b], pol);
+        }
+        mrow[b] = prow; mq[b] = pq; mitems[b] = items; mlast[b] = (pq + 1) * G >= tot;
+        if (mlast[b]) { prow = nrow; px = nx; pq = 0; nrow += W; nx = fetch(nrow); }
+        else ++pq;
+    };
+#pragma unroll
+    for (int b = 0; b < NB; ++b) issue(b);
+    uint32_t phase = 0;
+    float4 sv[CPL], acc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) { sv[c] = kZero4; acc[c] = kZero4; }
+    bool done = false;
+    while (!done) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            if (done) break;
+            const int i = mrow[b];
+            if (i >= n) { done = true; break; }
+            const int q = mq[b], items = mitems[b], last = mlast[b];
+            mbar_wait(&bar[b], phase);
+            const float* buf = ring + (size_t)b * G * in_pad;
+            int j0 = 0;
+            if (q == 0) {   // a new row: its self row opens the chunk
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    sv[c] = ch < nch ? reinterpret_cast<const float4*>(buf)[ch] : kZero4;
+                    acc[c] = kZero4;
+                }
+                j0 = 1;
+            }
+            for (int j = j0; j < items; ++j) {
+                const float4* rowp = reinterpret_cast<const float4*>(buf + (size_t)j * in_pad);
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    if (ch < nch) acc[c] = f4add(acc[c], rowp[ch]);
+                }
+            }
+            fence_async_smem();
+            __syncwarp();
+            issue(b);   // re-arm with the next chunk of the stream
+            if (last) {
+                const int c_tot = q * G + items - 1;   // neighbours of row i
+                const float inv = c_tot ? 1.0f / (float)c_tot : 0.f;   // one division per row (R23)
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int ch = lane + 32 * c;
+                    if (ch < nch) {
+                        store_split4(A, tix(A, i, 4 * ch), sv[c]);
+                        store_split4(A, tix(A, i, 4 * (nch + ch)), f4scale(acc[c], inv));
+                    }
+                }
+            }
+        }
+        phase ^= 1u;
+    }
+}
+
 // GCN: A[i] = Σ_e H[c_e] / sqrt(d_in(i) d_out(c_e)) + H[i] / sqrt(d_in(i) d_out(i)),
 // d_in(i) = deg(i) + 1, d_out(c) = outdeg_blk(c) + [c < n_dst]  (R12).
 template <int CPL, bool SH>
@@ -1108,6 +1231,29 @@ static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, 
     return true;
 }
 
+template <int CPL>
+static bool launch_l1_stream(const int32_t* rows_ptr, const float* X, int in_pad, const int32_t* smap,
+                             const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k, cudaStream_t s) {
+    constexpr int NB = 2;
+    const int G = std::max(2, std::min(16, 155000 / (kL1Warps * NB * in_pad * 4)));
+    const size_t smem = 128 + (size_t)kL1Warps * NB * G * in_pad * 4;
+    static std::map<size_t, int> grids;
+    int& grid = grids[smem];
+    if (!grid) {
+        cudaFuncSetAttribute(k_agg_l1_stream<NB, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_agg_l1_stream<NB, CPL>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_l1_stream<NB, CPL>, kL1Warps * 32, smem);
+        if (per_sm < 1) return false;
+        grid = per_sm * sms;
+    }
+    launch_pdl(k_agg_l1_stream<NB, CPL>, grid, kL1Warps * 32, smem, s, rows_ptr, X, in_pad, smap, blk_rowptr, col, A,
+               fixed_k, G);
+    return true;
+}
+
 void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int32_t* gmap,
                      const int32_t* smap, const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k,
                      int k_max, cudaStream_t s) {
@@ -1120,6 +1266,21 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
                                                      1 + k_max, s)
                                 : launch_l1_bulk<2>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
                                                      1 + k_max, s);
+        if (ok) return;
+    }
+    // wider rows (> 1 KB): streamed in chunks (GS_L1_STREAM=0: register loads)
+    static const int stream = [] { const char* e = std::getenv("GS_L1_STREAM"); return e ? std::atoi(e) : 1; }();
+    if (stream && bulk && !H.shards && !gmap && smap && k_max > 0 && k_max <= 31 && in_pad * 4 > 1024) {
+        bool ok = false;
+        switch (cpl_of(in_pad)) {
+            case 3: ok = launch_l1_stream<3>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, s); break;
+            case 4: ok = launch_l1_stream<4>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, s); break;
+            case 5: ok = launch_l1_stream<5>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, s); break;
+            case 6: ok = launch_l1_stream<6>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, s); break;
+            case 7: ok = launch_l1_stream<7>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, s); break;
+            case 8: ok = launch_l1_stream<8>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, s); break;
+            default: break;
+        }
         if (ok) return;
     }
     // A/B diagnostic only: GS_AGG_DUMMY_SMEM = bytes of (unused) dynamic shared memory for the

@@ -73,6 +73,7 @@ struct HopIO {
     int32_t *rowptr, *nbr, *col;
     int32_t *tcount, *trowptr, *tcursor, *tdst, *tdst_s;
     int32_t* erow;    // destination row of each edge (when tcount is set)
+    int count_only;   // only the transposed row pointer (out-degrees) is wanted: no fill, no sort
 };
 struct SampleParams {
     StepState* st;

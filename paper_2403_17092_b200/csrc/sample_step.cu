@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, GS_SAMPLE_MINB) k_sample_step(Sample
         const int tot = chunk_scan(sm, ns, [&](int u) { return H.tcount[u]; },
                                    [&](int u, int ex, int cnt) {
                                        H.trowptr[u] = ex; H.tcursor[u] = ex; H.tcount[u] = 0;
-                                       if (cnt > kWarpSort) P.hubs[2] = 1;   // a hub row exists
+                                       if (cnt > kWarpSort && !H.count_only) P.hubs[2] = 1;   // a hub row exists
                                    },
                                    P.status + (site++) * G, tag);
         if (tot >= 0 && threadIdx.x == 0) H.trowptr[ns] = tot;
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, GS_SAMPLE_MINB) k_sample_step(Sample
     grid_sync(P.bar);
     for (int h = 0; h <= P.hops; ++h) {   // edge-parallel fill (erow = each edge's destination row)
         const HopIO& H = P.hop[h];
-        if (!H.tcount) continue;
+        if (!H.tcount || H.count_only) continue;
         const int ne = st->n_edges[h];
         for (int e = gtid; e < ne; e += nthreads) H.tdst[atomicAdd(&H.tcursor[H.col[e]], 1)] = H.erow[e];
     }
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, GS_SAMPLE_MINB) k_sample_step(Sample
     int* wbuf = dyn + wib * kWarpSort;
     for (int h = 0; h <= P.hops; ++h) {
         const HopIO& H = P.hop[h];
-        if (!H.tcount) continue;
+        if (!H.tcount || H.count_only) continue;
         const int ns = st->n_src[h];
         for (int u0 = (blockIdx.x * kWarps + wib) * 32; u0 < ns; u0 += G * kWarps * 32) {
             const int ul = u0 + lane;
