@@ -382,7 +382,7 @@ void enqueue_training(gnn_model* m, int set) {
             const int fixed_k = direct && !m->full_train ? m->bs[set].sp.hop[blk].k : 0;
             K(m, s, kid, [&] {
                 launch_agg_sage(rows, Hrows, ly.in_pad, direct ? nullptr : self_ids, self_ids, B.rowptr[blk],
-                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, direct ? m->bs[set].sp.hop[blk].k : 0, s);
+                                direct ? B.nbr[blk] : B.col[blk], ly.A, fixed_k, m->bs[set].sp.hop[blk].k, s);
             });
         } else {
             K(m, s, kid, [&] {

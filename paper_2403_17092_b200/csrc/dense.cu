@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
             x.c = rowptr[i + 1] - beg;
             if (lane < x.c) x.nb = col[beg + lane];
         }
-        x.self = smap[i];
+        x.self = smap ? smap[i] : i;
         return x;
     };
     // arm buffer b with a row: self row -> slot 0, neighbour j -> slot 1 + j
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_stream(const int32_t* 
             x.c = rowptr[i + 1] - beg;
             if (lane < x.c) x.nb = col[beg + lane];
         }
-        x.self = smap[i];
+        x.self = smap ? smap[i] : i;
         return x;
     };
     // producer state: the row being issued (its indices), the chunk within it, the next row
@@ -1261,7 +1261,9 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
     // (GS_L1_BULK=0: register loads, for A/B; GS_L1_NB: buffers per warp)
     static const int bulk = [] { const char* e = std::getenv("GS_L1_BULK"); return e ? std::atoi(e) : 1; }();
     static const int nb = [] { const char* e = std::getenv("GS_L1_NB"); return e ? std::atoi(e) : 2; }();
-    if (bulk && !H.shards && !gmap && smap && k_max > 0 && k_max <= 31 && in_pad * 4 <= 1024) {
+    // GS_AGG_BULK_ALL=1 (A/B): the later layers' aggregations (local H rows, self row = i) too
+    static const int bulk_all = [] { const char* e = std::getenv("GS_AGG_BULK_ALL"); return e ? std::atoi(e) : 0; }();
+    if (bulk && !H.shards && !gmap && (smap || bulk_all) && k_max > 0 && k_max <= 31 && in_pad * 4 <= 1024) {
         const bool ok = nb == 3 ? launch_l1_bulk<3>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
                                                      1 + k_max, s)
                                 : launch_l1_bulk<2>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
@@ -1270,7 +1272,7 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
     }
     // wider rows (> 1 KB): streamed in chunks (GS_L1_STREAM=0: register loads)
     static const int stream = [] { const char* e = std::getenv("GS_L1_STREAM"); return e ? std::atoi(e) : 1; }();
-    if (stream && bulk && !H.shards && !gmap && smap && k_max > 0 && k_max <= 31 && in_pad * 4 > 1024) {
+    if (stream && bulk && !H.shards && !gmap && (smap || bulk_all) && k_max > 0 && k_max <= 31 && in_pad * 4 > 1024) {
         bool ok = false;
         switch (cpl_of(in_pad)) {
             case 3: ok = launch_l1_stream<3>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, s); break;

@@ -25,6 +25,9 @@
 #ifndef GS_TC_STAGES_WIDE
 #define GS_TC_STAGES_WIDE 3   // pipeline stages of the 96/128-column tiles
 #endif
+#ifndef GS_TC_STAGES_NARROW
+#define GS_TC_STAGES_NARROW 4   // pipeline stages of the <= 64-column tiles
+#endif
 
 namespace gs {
 namespace {
@@ -553,10 +556,10 @@ cudaError_t launch_tc(int grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStr
 template <int TERMS, int MODE>
 cudaError_t dispatch_bn(int bn, int grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
     switch (bn) {
-        case 16: return launch_tc<16, 4, TERMS, MODE>(grid, mp, a, s);
-        case 32: return launch_tc<32, 4, TERMS, MODE>(grid, mp, a, s);
-        case 48: return launch_tc<48, 4, TERMS, MODE>(grid, mp, a, s);
-        case 64: return launch_tc<64, 4, TERMS, MODE>(grid, mp, a, s);
+        case 16: return launch_tc<16, GS_TC_STAGES_NARROW, TERMS, MODE>(grid, mp, a, s);
+        case 32: return launch_tc<32, GS_TC_STAGES_NARROW, TERMS, MODE>(grid, mp, a, s);
+        case 48: return launch_tc<48, GS_TC_STAGES_NARROW, TERMS, MODE>(grid, mp, a, s);
+        case 64: return launch_tc<64, GS_TC_STAGES_NARROW, TERMS, MODE>(grid, mp, a, s);
         case 96: return launch_tc<96, GS_TC_STAGES_WIDE, TERMS, MODE>(grid, mp, a, s);
         case 128: return launch_tc<128, GS_TC_STAGES_WIDE, TERMS, MODE>(grid, mp, a, s);
         default: return cudaErrorInvalidValue;
@@ -565,10 +568,10 @@ cudaError_t dispatch_bn(int bn, int grid, const TcGemmMaps& mp, const GemmArgs& 
 template <int TERMS>
 cudaError_t dispatch_ce(int bn, int grid, const TcGemmMaps& mp, const GemmArgs& a, cudaStream_t s) {
     switch (bn) {
-        case 16: return launch_tc<16, 4, TERMS, 3>(grid, mp, a, s);
-        case 32: return launch_tc<32, 4, TERMS, 3>(grid, mp, a, s);
-        case 48: return launch_tc<48, 4, TERMS, 3>(grid, mp, a, s);
-        case 64: return launch_tc<64, 4, TERMS, 3>(grid, mp, a, s);
+        case 16: return launch_tc<16, GS_TC_STAGES_NARROW, TERMS, 3>(grid, mp, a, s);
+        case 32: return launch_tc<32, GS_TC_STAGES_NARROW, TERMS, 3>(grid, mp, a, s);
+        case 48: return launch_tc<48, GS_TC_STAGES_NARROW, TERMS, 3>(grid, mp, a, s);
+        case 64: return launch_tc<64, GS_TC_STAGES_NARROW, TERMS, 3>(grid, mp, a, s);
         default: return cudaErrorInvalidValue;
     }
 }
