@@ -151,6 +151,10 @@ struct Layer {
     uint32_t* hmask = nullptr;   // ReLU decisions of H (bit per element; layers with ReLU)
     int mask_ld = 0;             // words per hmask row
     TcGemmMaps map_fwd{}, map_dgrad{}, map_wgrad{};
+    // layer 1 with its gather on the sampling stream (gnn_model::l1_on_sampler): batch set 1's
+    // copy of the operand planes and of the maps that read them (set 0 uses A / map_fwd / map_wgrad)
+    Split A1{};
+    TcGemmMaps map_fwd1{}, map_wgrad1{};
 };
 
 struct ProfPair { int kid; cudaEvent_t a, b; };
@@ -227,6 +231,10 @@ struct gnn_model {
     // products 3780 -> 4290 mini-batches/s, epoch 51.8 -> 43.9 ms; with sampling co-running the
     // gather the training span grew from ~186 to ~267 µs)
     bool sample_after_l1 = false;
+    // layer 1's gather + mean (S4+S5) runs on the sampling stream right after the batch's sampling
+    // kernel, into the batch set's own operand planes: the training graph starts at the first GEMM,
+    // and the gather of step s+1 overlaps the tail of step s (GS_L1_ON_SAMPLER)
+    bool l1_on_sampler = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tl_sample, tl_train;
     bool profiling = false;
     std::vector<ProfPair> pending;
@@ -295,6 +303,15 @@ const int32_t* rows_ptr(gnn_model* m, int set, int li) {   // output rows of lay
     if (m->shadow && li == m->L - 1) return &st->batch_n;
     if (m->rf_compact && li == m->L - 2) return &st->n_rf;
     return &st->n_dst[m->layers[li].blk];
+}
+
+// layer 1's operand planes and GEMM maps of batch set `set` (per set when layer 1's gather runs
+// on the sampling stream: the gather of the next batch writes the other set's planes)
+const TcGemmMaps& fwd_map(const gnn_model* m, const Layer& ly, int li, int set) {
+    return (li == 0 && m->l1_on_sampler && set == 1) ? ly.map_fwd1 : ly.map_fwd;
+}
+const TcGemmMaps& wgrad_map(const gnn_model* m, const Layer& ly, int li, int set) {
+    return (li == 0 && m->l1_on_sampler && set == 1) ? ly.map_wgrad1 : ly.map_wgrad;
 }
 
 // The gradient exchange of a step (§2.2): NCCL all-reduce between the
@@ -373,7 +390,9 @@ void enqueue_training(gnn_model* m, int set) {
         const FeatRows Hrows = li == 0 ? g->rows() : FeatRows{m->layers[li - 1].H, nullptr, 0};
         const int kid = li == 0 ? GNN_K_AGG_L1 : GNN_K_AGG;
         const int32_t* self_ids = li == 0 ? B.nodes : nullptr;
-        if (m->shadow) {
+        if (li == 0 && m->l1_on_sampler) {
+            // gathered by the sampling stream (issue_sample) before B.sampled was recorded
+        } else if (m->shadow) {
             K(m, s, kid, [&] { bal(false, li, rows); });
         } else if (m->sage) {
             // layer 1 of the neighbour sampler reads X rows directly by global neighbour id
@@ -399,14 +418,14 @@ void enqueue_training(gnn_model* m, int set) {
         if (li == L - 1 && ly.n_pad <= 64) {
             // logits = A W with the softmax cross-entropy in the GEMM epilogue
             K(m, s, GNN_K_GEMM_FWD, [&] {
-                launch_gemm_tc_ce(m->bf16x3, ly.map_fwd, rows, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, B.st, g->C,
+                launch_gemm_tc_ce(m->bf16x3, fwd_map(m, ly, li, set), rows, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, B.st, g->C,
                                   g->y, B.nodes, ly.dPre, s);
             });
             break;
         }
         // Pre = A W (+ReLU) -> H (fp32)
         K(m, s, GNN_K_GEMM_FWD, [&] {
-            launch_gemm_tc(2, m->bf16x3, ly.map_fwd, rows, 0, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, ly.n_pad,
+            launch_gemm_tc(2, m->bf16x3, fwd_map(m, ly, li, set), rows, 0, (int)ly.m_cap, ly.n_pad, ly.k_pad, ly.H, ly.n_pad,
                            ly.n_pad, li < L - 1, 1, 0, s, ly.hmask, ly.mask_ld);
         });
         if (li == L - 1) {   // ---- loss (wide logits rows: separate kernel)
@@ -426,7 +445,7 @@ void enqueue_training(gnn_model* m, int set) {
         cudaStreamWaitEvent(ws, m->ev_dpre[li], 0);
         // dW = A^T dPre (deterministic split over rows)
         K(m, ws, GNN_K_GEMM_WGRAD, [&] {
-            launch_gemm_tc(1, m->bf16x3, ly.map_wgrad, rows, ly.k_pad, ly.k_pad, ly.n_pad, 0, ly.wpart, ly.n_pad,
+            launch_gemm_tc(1, m->bf16x3, wgrad_map(m, ly, li, set), rows, ly.k_pad, ly.k_pad, ly.n_pad, 0, ly.wpart, ly.n_pad,
                            ly.n_pad, false, ly.splits, stride, ws);
         });
         // the exchange of layer li's gradient starts now, while the backward of the layers below
@@ -519,6 +538,7 @@ gnn_status check_ready(gnn_model* m) {
         ncclUniqueId id;   // GNN_EXCH_NCCL on one rank: a communicator of one
         CKN(ncclGetUniqueId(&id));
         CKN(ncclCommInitRank(&m->comm, 1, id, 0));
+        (void)cudaGetLastError();   // NCCL's probing may leave a stale runtime error
     }
     return GNN_OK;
 }
@@ -545,6 +565,10 @@ int64_t steps_per_epoch(const gnn_model* m) {
 
 gnn_status set_device(int dev) {
     CK(cudaSetDevice(dev));
+    // every API call starts here: drop a stale error another library left in the runtime's
+    // per-thread "last error" (NCCL's device probing leaves cudaErrorInvalidDevice behind), so
+    // the launch checks below see only this call's launches
+    (void)cudaGetLastError();
     return GNN_OK;
 }
 
@@ -593,6 +617,15 @@ gnn_status issue_sample(gnn_model* m, int set, const int32_t* seeds_dev, const i
     cudaEvent_t ta = nullptr, tb = nullptr;
     if (m->timeline) { ta = take_event(m); tb = take_event(m); CK(cudaEventRecord(ta, m->sstream)); }
     K(m, m->sstream, GNN_K_SAMPLE, [&] { launch_sample_step(sp, m->sstream); });
+    if (m->l1_on_sampler && !full) {
+        // layer 1's fused gather + mean of this batch (its fixed-stride last hop, X by global id)
+        const Layer& ly = m->layers[0];
+        const int blk = ly.blk;
+        K(m, m->sstream, GNN_K_AGG_L1, [&] {
+            launch_agg_sage(rows_ptr(m, set, 0), m->g->rows(), ly.in_pad, nullptr, B.nodes, B.rowptr[blk], B.nbr[blk],
+                            set == 1 ? ly.A1 : ly.A, B.sp.hop[blk].k, B.sp.hop[blk].k, m->sstream);
+        });
+    }
     if (m->timeline) { CK(cudaEventRecord(tb, m->sstream)); m->tl_sample.emplace_back(ta, tb); }
     CK(cudaGetLastError());
     CK(cudaEventRecord(B.sampled, m->sstream));
@@ -1050,6 +1083,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     m->slot = m->shadow ? m->hops : -1;
     m->bf16x3 = c.precision == GNN_FP32;
     m->full_train = !(m->sage && !m->shadow);
+    { const char* e = std::getenv("GS_L1_ON_SAMPLER"); m->l1_on_sampler = !m->full_train && e && e[0] == '1'; }
     auto cleanup = [&](gnn_status s) {
         for (void* p : m->owned) cudaFree(p);
         for (void* p : m->owned_host) cudaFreeHost(p);
@@ -1259,6 +1293,16 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         ok &= make_tmap_f32(&ly.map_wgrad.c, ly.wpart, ly.k_pad, ly.n_pad, ly.n_pad, ly.splits,
                             (int64_t)ly.k_pad * ly.n_pad);
         if (li > 0) ok &= make_tmap_f32(&ly.map_dgrad.c, ly.dA, ly.m_cap, ly.k_pad, ly.k_pad, 1, 0);
+        if (li == 0 && m->l1_on_sampler) {   // set 1's planes and the maps that read them
+            if ((s = split(ly.A1, ly.rows_alloc * round_up(ly.k_pad, 64))) != GNN_OK) return cleanup(s);
+            ly.A1.rows = ly.rows_alloc;
+            ly.map_fwd1 = ly.map_fwd;
+            ly.map_wgrad1 = ly.map_wgrad;
+            ok &= make_tmap_bf16_tiled(&ly.map_fwd1.a_hi, ly.A1.hi, ly.rows_alloc, ly.k_pad, 128);
+            ok &= make_tmap_bf16_tiled(&ly.map_fwd1.a_lo, lo_or_hi(ly.A1), ly.rows_alloc, ly.k_pad, 128);
+            ok &= make_tmap_bf16_tiled(&ly.map_wgrad1.a_hi, ly.A1.hi, ly.rows_alloc, ly.k_pad, 64);
+            ok &= make_tmap_bf16_tiled(&ly.map_wgrad1.a_lo, lo_or_hi(ly.A1), ly.rows_alloc, ly.k_pad, 64);
+        }
         if (!ok) return cleanup(fail(GNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(li)));
     }
     AL(m->params, m->pcount);
@@ -1282,7 +1326,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
         const char* b = std::getenv("GS_L1_BULK");
         const bool bulk = m->sage && !m->shadow && !g->nshards && g->stride <= 1024 && c.fanouts[0] <= 31 &&
                           !(b && b[0] == '0');
-        m->sample_after_l1 = e ? e[0] == '1' : bulk;
+        m->sample_after_l1 = m->l1_on_sampler ? false : e ? e[0] == '1' : bulk;
     }
     for (auto& B : m->bs) CK(cudaEventCreateWithFlags(&B.l1done, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
@@ -1437,6 +1481,7 @@ gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_
         ncclUniqueId id;
         std::memcpy(&id, id_host, 128);
         CKN(ncclCommInitRank(&m->comm, world, id, rank));
+        (void)cudaGetLastError();   // NCCL's probing may leave a stale runtime error
     }
     m->rank = rank;
     m->world = world;

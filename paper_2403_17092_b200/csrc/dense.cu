@@ -548,6 +548,17 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
         // registers held across its edge loop)
         if (un < dlim) prefetch_rows_l2(dA + (int64_t)un * lda, nullptr, in_pad, lane);
         const float dout = (float)(ce - cb + (u < ndst ? 1 : 0));
+        // this row's ReLU bits and dA-self row do not depend on the edge loop: in flight with it
+        const uint32_t* mp = hmask + (int64_t)u * mask_ld;
+        const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
+        uint32_t hv[CPL];
+        float4 sv[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            hv[c] = ch < nch ? __ldg(mp + (ch >> 3)) >> ((4 * ch) & 31) : 0u;
+            sv[c] = (ch < nch && u < dlim) ? __ldg(sp + ch) : kZero4;
+        }
         float4 acc[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) acc[c] = kZero4;
@@ -605,16 +616,6 @@ __global__ void __launch_bounds__(256, 4) k_spmm_bwd(int h, const StepState* __r
         if (GCN && u < dlim) {
             const float din = (float)(rowptr[u + 1] - rowptr[u] + 1);
             wself = 1.0f / sqrtf(din * dout);
-        }
-        const uint32_t* mp = hmask + (int64_t)u * mask_ld;
-        const float4* sp = reinterpret_cast<const float4*>(dA + (int64_t)u * lda);
-        uint32_t hv[CPL];
-        float4 sv[CPL];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-            const int ch = lane + 32 * c;
-            hv[c] = ch < nch ? __ldg(mp + (ch >> 3)) >> ((4 * ch) & 31) : 0u;
-            sv[c] = (ch < nch && u < dlim) ? __ldg(sp + ch) : kZero4;
         }
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
@@ -700,6 +701,7 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
     const int T = (int)max((int64_t)kBalTmin, (items + kBalUnits - 1) / kBalUnits);
     const int nunits = (int)((items + T - 1) / T);
     const int64_t ldd = GCN ? a.in_pad : 2 * a.in_pad;   // BWD dA row (SAGE: [dSelf | dM])
+    auto put = [&](int64_t idx, float4 v) { store_split4(a.out, idx, v); };
 
     // finish row r from its full sum `acc` (fwd: normalise + self term; bwd: self term + ReLU')
     auto finish = [&](int r, int R, int rb, int re, float4 (&acc)[CPL], bool any) {
@@ -713,7 +715,7 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
-                    if (ch < pch) store_split4(a.out, tix(a.out, r, 4 * (c0 + ch)), f4fma(ws, __ldg(ps + c0 + ch), acc[c]));
+                    if (ch < pch) put(tix(a.out, r, 4 * (c0 + ch)), f4fma(ws, __ldg(ps + c0 + ch), acc[c]));
                 }
             } else {
                 const int deg = re - rb;
@@ -722,8 +724,8 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
                 for (int c = 0; c < CPL; ++c) {
                     const int ch = lane + 32 * c;
                     if (ch < pch) {
-                        store_split4(a.out, tix(a.out, r, 4 * (c0 + ch)), __ldg(ps + c0 + ch));
-                        store_split4(a.out, tix(a.out, r, 4 * (nch + c0 + ch)), f4scale(acc[c], inv));
+                        put(tix(a.out, r, 4 * (c0 + ch)), __ldg(ps + c0 + ch));
+                        put(tix(a.out, r, 4 * (nch + c0 + ch)), f4scale(acc[c], inv));
                     }
                 }
             }
@@ -752,7 +754,7 @@ __device__ __forceinline__ void agg_bal_body(const BalArgs& a) {
                     const uint32_t h = __ldg(mp + (cc >> 3)) >> ((4 * cc) & 31);   // ReLU decisions
                     v.x = (h & 1u) ? v.x : 0.f; v.y = (h & 2u) ? v.y : 0.f;
                     v.z = (h & 4u) ? v.z : 0.f; v.w = (h & 8u) ? v.w : 0.f;
-                    store_split4(a.out, tix(a.out, r, 4 * cc), v);
+                    put(tix(a.out, r, 4 * cc), v);
                 }
             }
         }

@@ -176,8 +176,9 @@ __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t, int M) {
 // Softmax cross-entropy of one logits row held by this thread (zr: fp32 bits, columns >= C
 // ignored) (R15): l = max + log sum exp(z - max) - z_y;  dZ = (softmax - onehot) /
 // b_total as split planes; rows in [M, round64(M)) get zero dZ (the wgrad reduction pads to 64).
+// Returns the row's loss (0 outside [0, M)).
 template <int BN>
-__device__ __forceinline__ void ce_rows(const GemmArgs& args, uint32_t (&zr)[(BN + 31) / 32][32], int row, int M) {
+__device__ __forceinline__ float ce_rows(const GemmArgs& args, uint32_t (&zr)[(BN + 31) / 32][32], int row, int M) {
     constexpr int kZ = (BN + 31) / 32 * 32;
     const int C = args.classes;
     const float inv_bt = 1.0f / (float)max(args.st->b_total, 1);
@@ -214,8 +215,7 @@ __device__ __forceinline__ void ce_rows(const GemmArgs& args, uint32_t (&zr)[(BN
             *reinterpret_cast<uint4*>(args.dz.hi + tix(args.dz, row, c)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
             if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + tix(args.dz, row, c)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
         }
-        args.st->row_loss[row] = (mx + logf(s)) - zy;
-        __threadfence();
+        return (mx + logf(s)) - zy;
     } else if (row < ((M + 63) & ~63)) {      // zero tail rows of the dZ planes
 #pragma unroll
         for (int c = 0; c < BN; c += 8) {
@@ -223,6 +223,7 @@ __device__ __forceinline__ void ce_rows(const GemmArgs& args, uint32_t (&zr)[(BN
             if (args.dz.lo) *reinterpret_cast<uint4*>(args.dz.lo + tix(args.dz, row, c)) = make_uint4(0u, 0u, 0u, 0u);
         }
     }
+    return 0.f;
 }
 
 // MODE 0 = dgrad (A, B K-major), MODE 1 = wgrad (A, B MN-major, split z), MODE 2 = fwd (A K-major,
@@ -243,7 +244,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int ce_last;
-    __shared__ float ce_part[kThreads / 32];
+    __shared__ float ce_warp[2][4];   // MODE 3: per-tile sums of the 4 epilogue warps (double buffered)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pdl_trigger();
@@ -439,7 +440,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                 for (int c0 = 0; c0 < kZ; c0 += 32)
                     tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::kAccCols + c0), zr[c0 / 32]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                ce_rows<BN>(args, zr, row0 + lane, M);
+                float l = ce_rows<BN>(args, zr, row0 + lane, M);
+                // the tile's loss: lanes (fixed tree), then the 4 warps in order -> row_loss[tile]
+                // (one partial per 128-row tile; the last CTA sums the tiles in order)
+                for (int o = 16; o; o >>= 1) l += __shfl_down_sync(0xffffffffu, l, o);
+                if (lane == 0) ce_warp[j & 1][q] = l;
+                asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
+                if (q == 0 && lane == 0) {
+                    args.st->row_loss[ti.tm] = ((ce_warp[j & 1][0] + ce_warp[j & 1][1]) + ce_warp[j & 1][2]) + ce_warp[j & 1][3];
+                    __threadfence();
+                }
             }
             if (has) {
                 tc_fence_before();
@@ -457,19 +467,15 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
     }
     if (MODE == 3 && !(args.diag & 16)) {
-        // the last CTA to finish sums the row losses in row order (deterministic)
+        // the last CTA to finish sums the per-tile losses in tile order (deterministic)
         if (threadIdx.x == 0) ce_last = atomicAdd(&args.st->ce_done, 1u) == gridDim.x - 1;
         __syncthreads();
         if (!ce_last) return;
         __threadfence();
-        float part = 0.f;
-        for (int r = threadIdx.x; r < M; r += kThreads) part += args.st->row_loss[r];
-        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) ce_part[warp] = part;
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0) {   // the tiles' partials in tile order
             float tot = 0.f;
-            for (int w = 0; w < kThreads / 32; ++w) tot += ce_part[w];
+            const int nt = (M + kBM - 1) / kBM;
+            for (int t = 0; t < nt; ++t) tot += __ldcg(&args.st->row_loss[t]);
             args.st->loss = tot * (1.0f / (float)max(args.st->b_total, 1));
             args.st->ce_done = 0u;
         }

@@ -294,7 +294,7 @@ cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const 
 
 // Last layer, fused: Z = A W (logits, stored like mode 2) and, in the epilogue, the softmax
 // cross-entropy of every row < *m_ptr (= batch_n): st->row_loss, dZ split planes [rows x n_pad]
-// (+ zero tail rows to a multiple of 64) and st->loss = Σ ℓ / b_total (last CTA, row order).
+// (+ zero tail rows to a multiple of 64) and st->loss = Σ ℓ / b_total (per-tile sums, then the last CTA adds the tiles in order).
 // n_pad <= 64 (one thread holds a row).
 cudaError_t launch_gemm_tc_ce(bool bf16x3, const TcGemmMaps& maps, const int32_t* m_ptr, int m_cap, int n_pad,
                               int k_pad, float* Z, StepState* st, int classes, const int32_t* labels,

@@ -94,3 +94,25 @@ def test_fullsize_exchange_nccl_equals_fused(name):
         m.close(); g.close()
     for a, b in zip(*runs):
         assert np.array_equal(a, b)
+
+
+
+@pytest.mark.parametrize("name", ["products", "reddit"])
+def test_fullsize_l1_on_sampler_bitidentical(name, monkeypatch):
+    """Layer 1's gather on the sampling stream (GS_L1_ON_SAMPLER=1: per-set operand planes, the
+    gather of step s+1 overlapping step s) trains bit-identically to the in-graph gather: losses,
+    gradients and parameters over 4 steps, then the end-to-end host call on the ragged last batch."""
+    w, inp, graph = inputs_for(name)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    last = w.n_batches - 1
+    seeds = OS.batch_seeds(perm, w.batch_size, last)
+    runs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("GS_L1_ON_SAMPLER", mode)
+        g, m = make_gpu(w, inp)
+        losses = [m.train_minibatch(0, s) for s in range(4)]
+        losses.append(m.train_batch_host(seeds, len(seeds), 0, last))
+        runs.append((np.array(losses), m.grads(), m.get_params()))
+        m.close(); g.close()
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)

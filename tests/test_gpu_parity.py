@@ -40,6 +40,23 @@ def test_tiny_epoch_training_parity(use_graph):
     print(f"worst per-step rel err {worst:.2e}, kink-ambiguous ReLU decisions {flips}")
 
 
+def test_tiny_epoch_training_parity_l1_on_sampler(monkeypatch):
+    """Layer 1's gather on the sampling stream (GS_L1_ON_SAMPLER=1): every step of a whole epoch
+    within tolerance of the oracle, then gnn_train_epoch of the next epoch."""
+    monkeypatch.setenv("GS_L1_ON_SAMPLER", "1")
+    w, inp, graph = inputs_for("tiny")
+    g, m = make_gpu(w, inp)
+    params = inp["params"].astype(np.float64)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    for step in range(w.n_batches):
+        loss = m.train_minibatch(0, step)
+        out = check_train_step(m, w, graph, params, 0, step, perm, loss)
+        params = out["params"]
+    assert rel(m.get_params(), params) <= TOL_FP32
+    st = m.train_epoch(1)
+    assert st["steps"] == w.n_batches
+
+
 def test_tiny_determinism_and_graph_equals_eager():
     w, inp, graph = inputs_for("tiny")
     runs = []
