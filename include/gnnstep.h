@@ -219,8 +219,19 @@ gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_
  *     communicator (the multi-rank branch, verifiable on one GPU: results are bit-identical to
  *     AUTO, since a one-rank all-reduce is a copy and both reduce in the same fixed order).
  * Synchronizes; the next step recaptures.  PARAM for an unknown mode. */
-enum { GNN_EXCH_AUTO = 0, GNN_EXCH_NCCL = 1, GNN_EXCH_PEER = 2 };
+enum { GNN_EXCH_AUTO = 0, GNN_EXCH_NCCL = 1, GNN_EXCH_PEER = 2, GNN_EXCH_HOST = 3 };
 gnn_status gnn_set_exchange(gnn_model* m, int32_t mode);
+/* GNN_EXCH_HOST (the Unified CPU-GPU protocol, §3: GPU and host-core
+ * trainer ranks "generate a local gradient; the local gradients are then gathered" for sync SGD):
+ * a step ends with this rank's reduced gradient (read it with gnn_debug_get(GNN_DBG_GRADS)) and
+ * does not update; the caller all-reduces it with the other ranks (e.g. torch.distributed gloo,
+ * the host ranks of include/gnnhost.h) and calls gnn_apply_update(summed gradient, host, n =
+ * param_count; NULL: the device gradient as it stands), which runs the update kernel
+ * (SGD/Adam) and synchronizes.  STATE outside GNN_EXCH_HOST, SHAPE for a wrong n.
+ * gnn_set_rank: this model's rank/world for the batch -> rank rule without an NCCL
+ * communicator (PARAM for bad values or a world differing from an existing communicator's). */
+gnn_status gnn_apply_update(gnn_model* m, const float* grads_host, int64_t n);
+gnn_status gnn_set_rank(gnn_model* m, int32_t rank, int32_t world);
 /* GNN_EXCH_PEER: a deterministic one-shot all-reduce over peer memory, fused with the update and
  * independent of NCCL.  Each rank owns an inbox [2 (step parity)][world][param_count] fp32 and a
  * flag array [world] u64 in one device allocation; gnn_exchange_export(rank, world) allocates it,

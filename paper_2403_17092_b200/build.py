@@ -70,6 +70,26 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return target
 
 
+HOST_SRC = os.path.join(HERE, "host", "gnnhost.cpp")
+HOST_LIB = os.path.join(HERE, "libgnnhost.so")
+
+
+def build_host(force: bool = False) -> str:
+    """libgnnhost.so: the host-core trainer rank (include/gnnhost.h), g++ -O3 -fopenmp.
+    -ffp-contract=off: the arithmetic is the source's (the update's fma is explicit)."""
+    inc = os.path.join(os.path.dirname(HERE), "include", "gnnhost.h")
+    if not force and os.path.exists(HOST_LIB) and all(os.path.getmtime(d) <= os.path.getmtime(HOST_LIB)
+                                                      for d in (HOST_SRC, inc)):
+        return HOST_LIB
+    tmp = HOST_LIB + f".{os.getpid()}.tmp"
+    r = subprocess.run(["g++", "-O3", "-std=c++17", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
+                        "-I", os.path.dirname(inc), "-o", tmp, HOST_SRC], capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError(f"g++ failed on {HOST_SRC}:\n{r.stderr}")
+    os.replace(tmp, HOST_LIB)
+    return HOST_LIB
+
+
 if __name__ == "__main__":
     # python build.py [--force] [-v] [--out PATH -DNAME=VAL ...]  (variants for A/B experiments)
     a = sys.argv[1:]

@@ -320,6 +320,9 @@ const TcGemmMaps& wgrad_map(const gnn_model* m, const Layer& ly, int li, int set
 bool uses_nccl(const gnn_model* m) {
     return m->exchange == GNN_EXCH_NCCL || (m->exchange == GNN_EXCH_AUTO && m->world > 1);
 }
+// GNN_EXCH_HOST: the step stops at the reduced gradient; the caller all-reduces it (with host
+// ranks, §3) and calls gnn_apply_update
+bool uses_host(const gnn_model* m) { return m->exchange == GNN_EXCH_HOST; }
 
 // ---------------------------------------------------------------- step bodies
 void enqueue_training(gnn_model* m, int set) {
@@ -436,7 +439,7 @@ void enqueue_training(gnn_model* m, int set) {
     // them before the update): they run on a forked stream as soon as their dPre is ready,
     // concurrently with the dgrad -> backward-aggregation chain, and join before the update.
     cudaStream_t ws = m->wstream;
-    const bool nccl = uses_nccl(m), peer = m->exchange == GNN_EXCH_PEER;
+    const bool nccl = uses_nccl(m), peer = m->exchange == GNN_EXCH_PEER, host = uses_host(m);
     for (int li = L - 1; li >= 0; --li) {
         Layer& ly = m->layers[li];
         const int32_t* rows = rows_ptr(m, set, li);
@@ -455,6 +458,8 @@ void enqueue_training(gnn_model* m, int set) {
                 launch_wgrad_reduce(pack_desc(m), li, li + 1, m->grads, PeerX{}, ws);
                 ncclAllReduce(m->grads + ly.poff, m->grads + ly.poff, (size_t)ly.pcnt, ncclFloat, ncclSum, m->comm, ws);
             });
+        } else if (host) {   // this layer's reduced gradient, for the caller's all-reduce
+            K(m, ws, GNN_K_ALLREDUCE, [&] { launch_wgrad_reduce(pack_desc(m), li, li + 1, m->grads, PeerX{}, ws); });
         } else if (peer) {
             PeerX x = m->px;
             x.signal = li == 0;   // the last bucket publishes the step
@@ -476,7 +481,9 @@ void enqueue_training(gnn_model* m, int set) {
     }
     cudaEventRecord(m->ev_join, ws);
     cudaStreamWaitEvent(s, m->ev_join, 0);
-    if (nccl) {
+    if (host) {
+        // ---- no update here: gnn_apply_update after the caller's all-reduce
+    } else if (nccl) {
         // ---- every layer's bucket is all-reduced: update
         K(m, s, GNN_K_SGD, [&] { launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, false, m->opt, s); });
     } else if (peer) {
@@ -1304,6 +1311,14 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
             ok &= make_tmap_bf16_tiled(&ly.map_wgrad1.a_lo, lo_or_hi(ly.A1), ly.rows_alloc, ly.k_pad, 64);
         }
         if (!ok) return cleanup(fail(GNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(li)));
+        // one dynamic-scheduler counter pair per GEMM launch site (the set-1 copies of layer 1's
+        // maps share set 0's: the two sets' steps never run concurrently)
+        for (TcGemmMaps* mp : {&ly.map_fwd, &ly.map_dgrad, &ly.map_wgrad}) {
+            AL(mp->sched, 2);
+            CK(cudaMemset(mp->sched, 0, 2 * sizeof(int)));
+        }
+        ly.map_fwd1.sched = ly.map_fwd.sched;
+        ly.map_wgrad1.sched = ly.map_wgrad.sched;
     }
     AL(m->params, m->pcount);
     AL(m->grads, m->pcount);
@@ -1492,7 +1507,7 @@ gnn_status gnn_comm_init(gnn_model* m, int32_t rank, int32_t world, const uint8_
 
 gnn_status gnn_set_exchange(gnn_model* m, int32_t mode) {
     if (!m) return fail(GNN_ERR_PARAM, "NULL model");
-    if (mode != GNN_EXCH_AUTO && mode != GNN_EXCH_NCCL && mode != GNN_EXCH_PEER)
+    if (mode != GNN_EXCH_AUTO && mode != GNN_EXCH_NCCL && mode != GNN_EXCH_PEER && mode != GNN_EXCH_HOST)
         return fail(GNN_ERR_PARAM, "unknown exchange mode");
     if (mode == GNN_EXCH_PEER && !m->peer_ready)
         return fail(GNN_ERR_STATE, "GNN_EXCH_PEER needs gnn_exchange_export + gnn_exchange_import first");
@@ -1502,6 +1517,31 @@ gnn_status gnn_set_exchange(gnn_model* m, int32_t mode) {
         m->exchange = mode;
         drop_graphs(m);   // the captured step holds the previous exchange
     }
+    return GNN_OK;
+}
+
+gnn_status gnn_set_rank(gnn_model* m, int32_t rank, int32_t world) {
+    if (!m || world < 1 || rank < 0 || rank >= world) return fail(GNN_ERR_PARAM, "bad arguments");
+    if (m->comm && m->world != world) return fail(GNN_ERR_PARAM, "world differs from the NCCL communicator's");
+    TRY(set_device(m->g->dev));
+    TRY(sync_all(m));
+    m->rank = rank;
+    m->world = world;
+    for (auto& B : m->bs) B.valid = false;   // prefetched batches followed the previous rule
+    return GNN_OK;
+}
+
+gnn_status gnn_apply_update(gnn_model* m, const float* grads_host, int64_t n) {
+    Range nvtx_("gnn_apply_update");
+    if (!m) return fail(GNN_ERR_PARAM, "NULL model");
+    if (!uses_host(m)) return fail(GNN_ERR_STATE, "gnn_apply_update needs GNN_EXCH_HOST");
+    if (grads_host && n != m->pcount) return fail(GNN_ERR_SHAPE, "n != param_count");
+    TRY(set_device(m->g->dev));
+    if (grads_host)
+        CK(cudaMemcpyAsync(m->grads, grads_host, sizeof(float) * m->pcount, cudaMemcpyHostToDevice, m->stream));
+    launch_sgd_pack(pack_desc(m), m->params, m->grads, m->cfg.lr, false, m->opt, m->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(m->stream));
     return GNN_OK;
 }
 

@@ -1087,7 +1087,7 @@ __global__ void k_sgd_pack(PackAll P, float* __restrict__ params, float* __restr
                     o.v[idx] = vv;
                     w = w - step * mm / (sqrtf(vv) * inv_sqrt_bc2 + o.eps);
                 } else {
-                    w = w - lr * gr;
+                    w = fmaf(-lr, gr, w);   // one rounding (the host rank's update, gnnhost.h)
                 }
                 params[idx] = w;
             }

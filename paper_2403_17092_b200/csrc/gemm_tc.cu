@@ -12,9 +12,15 @@
 //   dgrad dA  = dPre W^T    A: [M x N] K-major,   B = W   [K x N] K-major
 //   wgrad dW  = A^T dPre    A^T: MN-major,        B = dPre MN-major, split over M (deterministic)
 //
-// Persistent: one CTA per SM walks a static tile list (tile count read on the device).  Warp 0
-// = TMA producer, warp 1 = TMEM allocator + MMA issuer, warps 2..5 = epilogue (one TMEM lane
-// quarter each).  Two TMEM accumulators: the epilogue of tile j overlaps the MMAs of tile j+1.
+// Persistent: one CTA per SM; tiles are handed out dynamically (an atomic tile counter per launch
+// site, GemmArgs::sched): a CTA that starts late, because another kernel (the next batch's
+// sampling, a co-running gather) still holds its SM, takes fewer tiles instead of holding a fixed
+// share of them.  Warp 0 = TMA producer and tile scheduler (it publishes each tile index in a
+// 4-slot shared ring read by the MMA warp and the 4 epilogue warps), warp 1 = TMEM allocator +
+// MMA issuer, warps 2..5 = epilogue (one TMEM lane quarter each).  Two TMEM accumulators: the
+// epilogue of tile j overlaps the MMAs of tile j+1.  Every tile's result is independent of
+// which CTA computes it (split-K partials go to per-split slots, the CE loss to per-tile
+// partials), so the output is bit-identical under any schedule.
 #include <cuda.h>
 #include <cstdlib>
 #include <cuda_bf16.h>
@@ -145,7 +151,9 @@ struct GemmArgs {
     uint32_t* mask;         // MODE 2 with relu: sign bits of the stored H (nullable)
     int mask_ld;
     int diag;               // profiling diagnostics only (env GS_GEMM_DIAG): 1 skip C stores, 2 skip MMAs, 4 skip loads, 8 skip the CE epilogue, 16 skip the loss sum
+    int* sched;             // {next tile, CTAs done}: the dynamic tile scheduler (null: static tiles)
 };
+constexpr int kTileRing = 4;   // tile indices the scheduler may publish ahead of the epilogue
 
 struct TileInfo { int tm, tn, z, kb0, nkb; };
 
@@ -242,6 +250,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
+    __shared__ uint64_t ring_full[kTileRing], ring_empty[kTileRing];
+    __shared__ int ring_tile[kTileRing];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int ce_last;
     __shared__ float ce_warp[2][4];   // MODE 3: per-tile sums of the 4 epilogue warps (double buffered)
@@ -255,6 +265,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        for (int r = 0; r < kTileRing; ++r) { mbar_init(&ring_full[r], 1); mbar_init(&ring_empty[r], 5); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -273,12 +284,36 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     const int ntiles = MODE != 1 ? ((M + kBM - 1) / kBM) * args.n_tiles
                                  : ((args.m_static + kBM - 1) / kBM) * args.n_tiles * args.splits;
     const int t_first = (int)blockIdx.x, t_step = (int)gridDim.x;
+    // the j-th tile of this CTA: published by the producer (dynamic) or blockIdx + j * gridDim
+    const bool dyn = args.sched != nullptr;
+    auto next_tile = [&](int j) -> int {   // consumers (MMA thread, epilogue warps)
+        if (!dyn) return t_first + j * t_step;
+        const int r = j % kTileRing;
+        mbar_wait(&ring_full[r], (j / kTileRing) & 1);
+        const int t = ring_tile[r];
+        return t;
+    };
+    auto release_tile = [&](int j) {      // one arrival per consumer (MMA thread, 4 epilogue lane-0s)
+        if (dyn) mbar_arrive(&ring_empty[j % kTileRing]);
+    };
 
     if (warp == 0) {
         // ================= TMA producer
         if (lane == 0) {
             int it = 0;
-            for (int t = t_first; t < ntiles; t += t_step) {
+            for (int jt = 0;; ++jt) {
+                int t;
+                if (dyn) {   // claim a tile and publish it to the consumers
+                    const int r = jt % kTileRing;
+                    if (jt >= kTileRing) mbar_wait(&ring_empty[r], ((jt / kTileRing) - 1) & 1);
+                    t = atomicAdd(args.sched, 1);
+                    ring_tile[r] = t < ntiles ? t : -1;
+                    mbar_arrive(&ring_full[r]);   // (release: orders the ring write)
+                    if (t >= ntiles) break;
+                } else {
+                    t = t_first + jt * t_step;
+                    if (t >= ntiles) break;
+                }
                 const TileInfo ti = tile_info<MODE>(args, t, M);
                 const int tile_m = ti.tm * kBM, tile_n = ti.tn * BN;
                 for (int kb = 0; kb < ti.nkb; ++kb, ++it) {
@@ -330,7 +365,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
             // reduction extent: operands are zero past it, so the k16 steps beyond it are skipped
             const int klen = MODE == 1 ? M : args.k_len;
             int it = 0, j = 0;
-            for (int t = t_first; t < ntiles; t += t_step) {
+            for (int jt = 0;; ++jt) {
+                const int t = next_tile(jt);
+                release_tile(jt);
+                if (t < 0 || t >= ntiles) break;
                 const TileInfo ti = tile_info<MODE>(args, t, M);
                 if (ti.nkb == 0) continue;
                 const int acc = j & 1;
@@ -376,7 +414,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         const int q = warp & 3;                       // TMEM lane quarter this warp may access
         uint8_t* ebuf = smem + STAGES * kStageBytes + q * 2 * kEpiBuf;
         int j = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int jt = 0;; ++jt) {
+            const int t = next_tile(jt);
+            __syncwarp();
+            if (lane == 0) release_tile(jt);
+            if (t < 0 || t >= ntiles) break;
             const TileInfo ti = tile_info<MODE>(args, t, M);
             const int row0 = ti.tm * kBM + q * 32;
             const int tile_n = ti.tn * BN;
@@ -465,6 +507,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
+    }
+    if (dyn && threadIdx.x == 0) {
+        // every CTA has claimed its last (past-the-end) tile: the last one to finish re-arms the
+        // counter for the next launch from this site
+        __threadfence();   // this CTA's claims precede its "done" in every observer's view
+        if (atomicAdd(args.sched + 1, 1) == (int)gridDim.x - 1) {
+            args.sched[0] = 0;
+            args.sched[1] = 0;
+            __threadfence();
+        }
     }
     if (MODE == 3 && !(args.diag & 16)) {
         // the last CTA to finish sums the per-tile losses in tile order (deterministic)
@@ -588,6 +640,12 @@ int tc_tile_n(int n_pad) {
     return 128;
 }
 
+// GS_GEMM_DYN=0 (A/B): the static tile list (tile t on CTA t mod grid)
+bool dyn_sched() {
+    static const bool d = [] { const char* e = getenv("GS_GEMM_DYN"); return !(e && e[0] == '0'); }();
+    return d;
+}
+
 static int gemm_diag() {
     static int d = -1;
     if (d < 0) {
@@ -617,6 +675,7 @@ cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const 
     a.relu = relu ? 1 : 0;
     a.split_stride = split_stride;
     a.diag = gemm_diag();
+    a.sched = dyn_sched() ? maps.sched : nullptr;
     int tiles_cap;
     if (mode != 1) tiles_cap = a.m_tiles_cap * a.n_tiles;
     else tiles_cap = ((m_static + kBM - 1) / kBM) * a.n_tiles * splits;
@@ -649,6 +708,7 @@ cudaError_t launch_gemm_tc_ce(bool bf16x3, const TcGemmMaps& maps, const int32_t
     a.dz = dz;
     a.classes = classes;
     a.diag = gemm_diag();
+    a.sched = dyn_sched() ? maps.sched : nullptr;
     const int grid = std::max(1, std::min(kSMs, a.m_tiles_cap));
     return bf16x3 ? dispatch_ce<3>(n_pad, grid, maps, a, s) : dispatch_ce<1>(n_pad, grid, maps, a, s);
 }

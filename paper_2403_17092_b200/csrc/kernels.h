@@ -267,7 +267,9 @@ void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint3
                         cudaStream_t s);
 
 // ------------------------------------------------------------------ tensor-core GEMM (gemm_tc.cu)
-struct TcGemmMaps { CUtensorMap a_hi, a_lo, b_hi, b_lo, c; };
+// sched: the launch's dynamic tile scheduler {next tile, CTAs done} (2 ints, zero between
+// launches; one pair per GEMM launch site: GEMMs that may run concurrently must not share it)
+struct TcGemmMaps { CUtensorMap a_hi, a_lo, b_hi, b_lo, c; int* sched = nullptr; };
 // 2-D bf16 row-major [rows x cols], box {64 cols, box_rows}, 128B swizzle, OOB reads -> 0.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
 // k-block-tiled bf16 plane (Split layout, `rows` rows, `cols` columns): 3-D map {64, rows,

@@ -16,7 +16,7 @@ GNN_FP32, GNN_BF16_GEMM = 0, 1
 GNN_SRC_IDS, GNN_BLK_ROWPTR, GNN_BLK_COL, GNN_BLK_NBR = 0, 1, 2, 3
 GNN_DBG_LOGITS, GNN_DBG_GRADS, GNN_DBG_LOSS, GNN_DBG_ACT = 0, 1, 2, 16
 GNN_SGD, GNN_ADAM = 0, 1
-GNN_EXCH_AUTO, GNN_EXCH_NCCL, GNN_EXCH_PEER = 0, 1, 2
+GNN_EXCH_AUTO, GNN_EXCH_NCCL, GNN_EXCH_PEER, GNN_EXCH_HOST = 0, 1, 2, 3
 ABI_VERSION = 2   # include/gnnstep.h GNN_ABI_VERSION
 KERNEL_IDS = dict(sample=0, relabel=1, agg_l1=2, agg=3, gemm_fwd=4, gemm_dgrad=5, gemm_wgrad=6,
                   spmm_bwd=7, ce=8, sgd=9, transpose=10, induce=11, allreduce=12, scan=13, other=14)
@@ -83,6 +83,7 @@ def lib():
             "gnn_set_schedule": ([P, P, I64], I32), "gnn_set_exchange": ([P, I32], I32),
             "gnn_cache_stats": ([P, I32, P], I32), "gnn_exchange_export": ([P, I32, I32, P], I32),
             "gnn_exchange_import": ([P, P], I32),
+            "gnn_apply_update": ([P, P, I64], I32), "gnn_set_rank": ([P, I32, I32], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(_lib, name)
@@ -216,7 +217,20 @@ class Model:
         communicator) or "peer" (one-shot all-reduce over CUDA-IPC peer memory, after
         exchange_export / exchange_import)."""
         _check(lib().gnn_set_exchange(self.h, {"auto": GNN_EXCH_AUTO, "nccl": GNN_EXCH_NCCL,
-                                               "peer": GNN_EXCH_PEER}[mode]))
+                                               "peer": GNN_EXCH_PEER, "host": GNN_EXCH_HOST}[mode]))
+
+    def set_rank(self, rank: int, world: int):
+        """gnn_set_rank: rank/world of the batch -> rank rule without an NCCL communicator."""
+        _check(lib().gnn_set_rank(self.h, rank, world))
+
+    def apply_update(self, grads=None):
+        """gnn_apply_update (GNN_EXCH_HOST): the update with the all-reduced gradient (fp32 host
+        array of param_count; None: the device gradient as it stands)."""
+        if grads is None:
+            _check(lib().gnn_apply_update(self.h, None, 0))
+            return
+        g = np.ascontiguousarray(grads, dtype=np.float32)
+        _check(lib().gnn_apply_update(self.h, _ptr(g), g.shape[0]))
 
     def exchange_export(self, rank: int, world: int) -> bytes:
         """gnn_exchange_export: allocate this rank's inbox; returns its 64-byte CUDA IPC handle."""

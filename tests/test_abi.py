@@ -53,7 +53,7 @@ def test_oracle_not_linked_into_product():
     pkg = os.path.join(ROOT, "paper_2403_17092_b200")
     for dirpath, _, files in os.walk(pkg):
         for f in files:
-            if f.endswith((".py", ".cu", ".cuh", ".h")):
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
 
@@ -73,3 +73,18 @@ def test_cache_plan_by_degree_matches_definition():
             remote = [v for v in range(n) if not (b <= v < e)]
             want = sorted(sorted(remote, key=lambda v: (-deg[v], v))[:cap])
             assert list(cache_plan_by_degree(rp, P, shard, cap)) == want
+
+
+def test_host_rank_library_exports_its_header_and_is_separate():
+    """libgnnhost.so (the host-core trainer rank, include/gnnhost.h) exports every declared gnnh_
+    symbol; the GPU library neither defines nor references any of them (no CPU fallback path)."""
+    from paper_2403_17092_b200.hostrank import lib as hlib
+    txt = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "gnnhost.h")).read(), flags=re.S)
+    syms = sorted(set(re.findall(r"\b(gnnh_[a-z_0-9]+)\s*\(", txt)))
+    assert "gnnh_grads" in syms and "gnnh_apply" in syms
+    out = subprocess.run(["nm", "-D", "--defined-only", hlib()._name], capture_output=True, text=True).stdout
+    for s in syms:
+        assert re.search(rf"\bT {s}\b", out), s
+    from paper_2403_17092_b200 import lib
+    gpu = subprocess.run(["nm", "-D", lib()._name], capture_output=True, text=True).stdout
+    assert "gnnh_" not in gpu
