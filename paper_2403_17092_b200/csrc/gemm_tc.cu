@@ -12,10 +12,10 @@
 //   dgrad dA  = dPre W^T    A: [M x N] K-major,   B = W   [K x N] K-major
 //   wgrad dW  = A^T dPre    A^T: MN-major,        B = dPre MN-major, split over M (deterministic)
 //
-// Persistent: one CTA per SM; tiles are handed out dynamically (an atomic tile counter per launch
-// site, GemmArgs::sched): a CTA that starts late, because another kernel (the next batch's
-// sampling, a co-running gather) still holds its SM, takes fewer tiles instead of holding a fixed
-// share of them.  Warp 0 = TMA producer and tile scheduler (it publishes each tile index in a
+// Persistent: one CTA per SM walks a static tile list (t = blockIdx + j * gridDim), or (A/B switch
+// GS_GEMM_DYN=1, measured slower) tiles handed out dynamically by an atomic tile counter per launch
+// site (GemmArgs::sched), so that a CTA that starts late, because another kernel still holds its
+// SM, takes fewer tiles instead of holding a fixed share of them.  Warp 0 = TMA producer and tile scheduler (it publishes each tile index in a
 // 4-slot shared ring read by the MMA warp and the 4 epilogue warps), warp 1 = TMEM allocator +
 // MMA issuer, warps 2..5 = epilogue (one TMEM lane quarter each).  Two TMEM accumulators: the
 // epilogue of tile j overlaps the MMAs of tile j+1.  Every tile's result is independent of
@@ -640,9 +640,11 @@ int tc_tile_n(int n_pad) {
     return 128;
 }
 
-// GS_GEMM_DYN=0 (A/B): the static tile list (tile t on CTA t mod grid)
+// GS_GEMM_DYN=1 (A/B): the dynamic tile scheduler.  Measured slower than the static tile list
+// (tile t on CTA t mod grid): products GEMM classes fwd 63 -> 67, dgrad 27 -> 30, wgrad 54 ->
+// 61 µs per step (the claim + ring hand-off per tile costs more than late CTAs lose), so off.
 bool dyn_sched() {
-    static const bool d = [] { const char* e = getenv("GS_GEMM_DYN"); return !(e && e[0] == '0'); }();
+    static const bool d = [] { const char* e = getenv("GS_GEMM_DYN"); return e && e[0] == '1'; }();
     return d;
 }
 
