@@ -117,7 +117,12 @@ def kernel_work(w, sz, kind, terms=3, splits=None):
     (DESIGN.md "Roofline").  sz: per-hop sizes of the batch."""
     L = w.num_layers
     byt, flo = 0.0, 0.0
+    # the last layer with <= 64 classes runs fused on the CUDA cores (the "ce" class: logits, loss,
+    # dA = dZ W^T), not in the forward / dgrad GEMM classes (GS_LAST_FUSED=0 restores them)
+    fused_last = w.num_classes <= 64 and os.environ.get("GS_LAST_FUSED", "1") != "0"
     for li, (fi, fo, in_pad, k_pad, n_pad) in enumerate(layer_dims(w)):
+        if fused_last and li == L - 1 and kind in ("gemm_fwd", "gemm_dgrad"):
+            continue
         h = L - 1 - li if w.sampler == "neighbor" else len(w.fanouts)  # ShaDow: the induced block slot
         M, S, E = sz["n_dst"][h], sz["n_src"][h], sz["n_edges"][h]
         if w.sampler == "shadow" and li == L - 1:

@@ -323,6 +323,13 @@ bool uses_nccl(const gnn_model* m) {
 // GNN_EXCH_HOST: the step stops at the reduced gradient; the caller all-reduces it (with host
 // ranks, §3) and calls gnn_apply_update
 bool uses_host(const gnn_model* m) { return m->exchange == GNN_EXCH_HOST; }
+// the last layer on the CUDA cores (k_last_layer) when its classes fit a warp pair and W fits shared
+// memory; GS_LAST_FUSED=0: the tensor-core GEMM + CE epilogue and the dgrad GEMM (A/B)
+bool fused_last(const gnn_model* m) {
+    static const bool on = [] { const char* e = std::getenv("GS_LAST_FUSED"); return !(e && e[0] == '0'); }();
+    const Layer& ly = m->layers[m->L - 1];
+    return on && last_layer_fits(ly.k_pad, ly.out);
+}
 
 // ---------------------------------------------------------------- step bodies
 void enqueue_training(gnn_model* m, int set) {
@@ -418,6 +425,14 @@ void enqueue_training(gnn_model* m, int set) {
             cudaEventRecordWithFlags(B.l1done, s, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
                                                                                     : cudaEventRecordDefault);
         }
+        if (li == L - 1 && fused_last(m)) {
+            // logits, cross-entropy and dA = dZ W^T in one CUDA-core pass (dense.cu k_last_layer)
+            K(m, s, GNN_K_CE, [&] {
+                launch_last_layer(rows, (int)ly.m_cap, ly.A, ly.k_pad, ly.in, ly.in_pad, m->sage, m->params + ly.poff,
+                                  g->C, ly.n_pad, ly.H, ly.dPre, ly.dA, B.st, g->y, B.nodes, s);
+            });
+            break;
+        }
         if (li == L - 1 && ly.n_pad <= 64) {
             // logits = A W with the softmax cross-entropy in the GEMM epilogue
             K(m, s, GNN_K_GEMM_FWD, [&] {
@@ -466,8 +481,8 @@ void enqueue_training(gnn_model* m, int set) {
             K(m, ws, GNN_K_ALLREDUCE, [&] { launch_wgrad_reduce(pack_desc(m), li, li + 1, nullptr, x, ws); });
         }
         if (li == 0) break;
-        // dA = dPre W^T (fp32)
-        K(m, s, GNN_K_GEMM_DGRAD, [&] {
+        // dA = dPre W^T (fp32); the fused last layer computed it already
+        if (!(li == L - 1 && fused_last(m))) K(m, s, GNN_K_GEMM_DGRAD, [&] {
             launch_gemm_tc(0, m->bf16x3, ly.map_dgrad, rows, 0, (int)ly.m_cap, ly.k_pad, ly.n_pad, ly.dA, ly.k_pad,
                            ly.k_pad, false, 1, 0, s);
         });

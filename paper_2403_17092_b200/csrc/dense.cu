@@ -1408,6 +1408,144 @@ void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bo
     launch_pdl(k_sgd_pack, reduce ? 148 * 8 : 148 * 2, 256, 0, s, p, params, grads, lr, reduce ? 1 : 0, o, x);
 }
 
+// ------------------------------------------------------------------ the last layer, fused
+// The last layer of a model with C <= 64 classes, one warp per output row, on the CUDA cores in
+// fp32: Z = A W (logits; Eq. 1-2), the softmax cross-entropy of the row (Eq. 3, R15: l = max + log
+// Σ exp(z - max) - z_y, dZ = (softmax - onehot) / b_total), and dA = dZ W^T — every quantity of
+// the row is local to it, so the three products of the layer share one pass over W, which sits
+// in shared memory (k_pad x C fp32, row stride C|1 so both the k-major and the c-major sweeps are
+// bank-conflict free).  At M = 1024 rows the tensor-core GEMM + CE epilogue was latency-bound
+// (18 µs for 0.15 GFLOP, tensor pipe 9 % active) and its dgrad GEMM another 8 µs; here the layer
+// is ~1 wave of 128 blocks.  The weight gradient A^T dZ stays on the tensor cores (forked stream).
+// A is read from its split planes (hi + lo); W from the fp32 parameters (rows r of the [rows x C]
+// block: SAGE k -> (k / in_pad) * in + k % in_pad, GCN k -> k, zero beyond).
+constexpr int kLastRows = 8;   // rows (warps) per block
+struct LastArgs {
+    const int32_t* m_ptr;      // rows of the layer (batch rows)
+    Split A;                   // operand planes [rows x k_pad]
+    int k_pad, in, in_pad, sage;
+    const float* W;            // the layer's fp32 parameter block [rows x C]
+    int C, n_pad;
+    float* Z;                  // logits [rows x n_pad] (debug readout)
+    Split dz;                  // dZ planes [rows x n_pad] for the weight-gradient GEMM
+    float* dA;                 // [rows x k_pad] fp32 for the backward aggregation
+    StepState* st;
+    const int32_t* labels;
+    const int32_t* nodes;
+};
+__global__ void __launch_bounds__(kLastRows * 32) k_last_layer(LastArgs a) {
+    extern __shared__ __align__(16) float lsm[];
+    const int ldw = a.C | 1;
+    float* Ws = lsm;                                    // [k_pad][ldw]
+    float* As = lsm + (size_t)a.k_pad * ldw;            // [kLastRows][k_pad]
+    __shared__ float wloss[kLastRows];
+    __shared__ int is_last;
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    for (int x = threadIdx.x; x < a.k_pad * a.C; x += blockDim.x) {   // W: independent of the predecessor
+        const int k = x / a.C, c = x % a.C;
+        int r = -1;
+        if (a.sage) { const int half = k / a.in_pad, j = k % a.in_pad; if (half < 2 && j < a.in) r = half * a.in + j; }
+        else if (k < a.in) r = k;
+        Ws[k * ldw + c] = r >= 0 ? __ldg(a.W + (int64_t)r * a.C + c) : 0.f;
+    }
+    pdl_trigger();
+    pdl_wait();
+    const int M = *a.m_ptr;
+    const int row = blockIdx.x * kLastRows + warp;
+    float* Ar = As + (size_t)warp * a.k_pad;
+    if (row < M)
+        for (int k = lane; k < a.k_pad; k += 32) {
+            const int64_t ix = tix(a.A, row, k);
+            Ar[k] = __bfloat162float(a.A.hi[ix]) + (a.A.lo ? __bfloat162float(a.A.lo[ix]) : 0.f);
+        }
+    __syncthreads();
+    float l = 0.f;
+    if (row < M) {
+        // logits of classes lane and lane + 32 (k ascending)
+        const int c0 = lane, c1 = lane + 32;
+        const bool v0 = c0 < a.C, v1 = c1 < a.C;
+        float z0 = 0.f, z1 = 0.f;
+        for (int k = 0; k < a.k_pad; ++k) {
+            const float x = Ar[k];
+            if (v0) z0 = fmaf(x, Ws[k * ldw + c0], z0);
+            if (v1) z1 = fmaf(x, Ws[k * ldw + c1], z1);
+        }
+        if (v0) a.Z[(int64_t)row * a.n_pad + c0] = z0;
+        if (v1) a.Z[(int64_t)row * a.n_pad + c1] = z1;
+        // softmax cross-entropy of the row
+        float mx = fmaxf(v0 ? z0 : -INFINITY, v1 ? z1 : -INFINITY);
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+        const float e0 = v0 ? expf(z0 - mx) : 0.f, e1 = v1 ? expf(z1 - mx) : 0.f;
+        float ssum = e0 + e1;
+        for (int o = 16; o; o >>= 1) ssum += __shfl_xor_sync(kFull, ssum, o);
+        const int y = a.labels[a.nodes[row]];
+        const float zy = __shfl_sync(kFull, y < 32 ? z0 : z1, y & 31);
+        l = (mx + logf(ssum)) - zy;
+        const float inv_s = 1.0f / ssum, inv_bt = 1.0f / (float)max(a.st->b_total, 1);
+        const float d0 = v0 ? (e0 * inv_s - (c0 == y ? 1.f : 0.f)) * inv_bt : 0.f;
+        const float d1 = v1 ? (e1 * inv_s - (c1 == y ? 1.f : 0.f)) * inv_bt : 0.f;
+        if (c0 < a.n_pad) store_split1(a.dz, tix(a.dz, row, c0), d0);
+        if (c1 < a.n_pad) store_split1(a.dz, tix(a.dz, row, c1), d1);
+        // dA[row, k] = Σ_c dZ[row, c] W[k, c]  (c ascending), k = lane + 32 j
+        for (int k0 = 0; k0 < a.k_pad; k0 += 32 * 8) {
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            for (int c = 0; c < a.C; ++c) {
+                const float dc = __shfl_sync(kFull, c < 32 ? d0 : d1, c & 31);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int k = k0 + lane + 32 * j;
+                    if (k < a.k_pad) acc[j] = fmaf(dc, Ws[k * ldw + c], acc[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int k = k0 + lane + 32 * j;
+                if (k < a.k_pad) a.dA[(int64_t)row * a.k_pad + k] = acc[j];
+            }
+        }
+    } else if (row < ((M + 63) & ~63)) {   // zero tail rows of the dZ planes (the wgrad reduction pads to 64)
+        for (int c = lane; c < a.n_pad; c += 32) store_split1(a.dz, tix(a.dz, row, c), 0.f);
+    }
+    // the loss: the block's rows in order, then the blocks in order by the last block to finish
+    if (lane == 0) wloss[warp] = l;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < kLastRows; ++w) t += wloss[w];
+        a.st->row_loss[blockIdx.x] = t;
+        __threadfence();
+        is_last = atomicAdd(&a.st->ce_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last && threadIdx.x == 0) {
+        __threadfence();
+        float tot = 0.f;
+        for (int b = 0; b < (int)gridDim.x; ++b) tot += __ldcg(&a.st->row_loss[b]);
+        a.st->loss = tot * (1.0f / (float)max(a.st->b_total, 1));
+        a.st->ce_done = 0u;
+    }
+}
+
+void launch_last_layer(const int32_t* m_ptr, int m_cap, Split A, int k_pad, int in, int in_pad, bool sage,
+                       const float* W, int C, int n_pad, float* Z, Split dz, float* dA, StepState* st,
+                       const int32_t* labels, const int32_t* nodes, cudaStream_t s) {
+    const size_t smem = sizeof(float) * ((size_t)k_pad * (C | 1) + (size_t)kLastRows * k_pad);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(k_last_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    const int grid = (((m_cap + 63) & ~63) + kLastRows - 1) / kLastRows;
+    LastArgs a{m_ptr, A, k_pad, in, in_pad, sage ? 1 : 0, W, C, n_pad, Z, dz, dA, st, labels, nodes};
+    launch_pdl(k_last_layer, grid, kLastRows * 32, smem, s, a);
+}
+
+bool last_layer_fits(int k_pad, int C) {
+    return C <= 64 && sizeof(float) * ((size_t)k_pad * (C | 1) + (size_t)kLastRows * k_pad) <= 200 * 1024;
+}
+
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,
                Split dZ, cudaStream_t s) {
     launch_pdl(k_ce, 128, 256, 0, s, st, Z, ldz, C, labels, nodes, dZ, st->row_loss, &st->ce_done);

@@ -251,6 +251,13 @@ struct OptState { float* m; float* v; int32_t* t; unsigned* done; float beta1, b
 // every rank's flag (written to grads, then the update).
 void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bool reduce, const OptState& o,
                      cudaStream_t s, const PeerX& x = PeerX{});
+// The last layer fused on the CUDA cores (C <= 64): Z = A W, softmax CE (st->loss), dZ split
+// planes (+ zero tail rows to a multiple of 64), dA = dZ W^T (fp32 [rows x k_pad]).  Rows
+// [0, *m_ptr) of at most m_cap; W = the layer's fp32 parameter block [rows x C].
+void launch_last_layer(const int32_t* m_ptr, int m_cap, Split A, int k_pad, int in, int in_pad, bool sage,
+                       const float* W, int C, int n_pad, float* Z, Split dz, float* dA, StepState* st,
+                       const int32_t* labels, const int32_t* nodes, cudaStream_t s);
+bool last_layer_fits(int k_pad, int C);
 // Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total
 // written as split planes [rows x ldz] (+ zero tail rows).
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels,
