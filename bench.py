@@ -119,7 +119,7 @@ def kernel_work(w, sz, kind, terms=3, splits=None):
     byt, flo = 0.0, 0.0
     # the last layer with <= 64 classes runs fused on the CUDA cores (the "ce" class: logits, loss,
     # dA = dZ W^T), not in the forward / dgrad GEMM classes (GS_LAST_FUSED=0 restores them)
-    fused_last = w.num_classes <= 64 and os.environ.get("GS_LAST_FUSED", "1") != "0"
+    fused_last = w.num_classes <= 64 and os.environ.get("GS_LAST_FUSED", "0") == "1"
     for li, (fi, fo, in_pad, k_pad, n_pad) in enumerate(layer_dims(w)):
         if fused_last and li == L - 1 and kind in ("gemm_fwd", "gemm_dgrad"):
             continue

@@ -235,6 +235,7 @@ struct gnn_model {
     // kernel, into the batch set's own operand planes: the training graph starts at the first GEMM,
     // and the gather of step s+1 overlaps the tail of step s (GS_L1_ON_SAMPLER)
     bool l1_on_sampler = false;
+    bool last_fused = false;             // GS_LAST_FUSED=1 at model creation: k_last_layer (§6.9)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tl_sample, tl_train;
     bool profiling = false;
     std::vector<ProfPair> pending;
@@ -323,12 +324,13 @@ bool uses_nccl(const gnn_model* m) {
 // GNN_EXCH_HOST: the step stops at the reduced gradient; the caller all-reduces it (with host
 // ranks, §3) and calls gnn_apply_update
 bool uses_host(const gnn_model* m) { return m->exchange == GNN_EXCH_HOST; }
-// the last layer on the CUDA cores (k_last_layer) when its classes fit a warp pair and W fits shared
-// memory; GS_LAST_FUSED=0: the tensor-core GEMM + CE epilogue and the dgrad GEMM (A/B)
+// GS_LAST_FUSED=1 (A/B): the last layer on the CUDA cores (k_last_layer, with the layer's
+// aggregation for SAGE) when its classes fit a warp pair and W fits shared memory.  Measured: 30 µs
+// per step against 33 µs for the aggregation + tensor-core GEMM/CE + dgrad GEMM it replaces, and
+// the step no faster (products 4060-4110 vs 4235-4245 mini-batches/s): off by default
 bool fused_last(const gnn_model* m) {
-    static const bool on = [] { const char* e = std::getenv("GS_LAST_FUSED"); return !(e && e[0] == '0'); }();
     const Layer& ly = m->layers[m->L - 1];
-    return on && last_layer_fits(ly.k_pad, ly.out);
+    return m->last_fused && last_layer_fits(ly.k_pad, ly.out);
 }
 
 // ---------------------------------------------------------------- step bodies
@@ -400,8 +402,11 @@ void enqueue_training(gnn_model* m, int set) {
         const FeatRows Hrows = li == 0 ? g->rows() : FeatRows{m->layers[li - 1].H, nullptr, 0};
         const int kid = li == 0 ? GNN_K_AGG_L1 : GNN_K_AGG;
         const int32_t* self_ids = li == 0 ? B.nodes : nullptr;
+        // the last layer of SAGE + neighbour gathers its A inside k_last_layer (no aggregation launch)
+        const bool agg_in_last = li == L - 1 && li > 0 && fused_last(m) && m->sage && !m->shadow;
         if (li == 0 && m->l1_on_sampler) {
             // gathered by the sampling stream (issue_sample) before B.sampled was recorded
+        } else if (agg_in_last) {
         } else if (m->shadow) {
             K(m, s, kid, [&] { bal(false, li, rows); });
         } else if (m->sage) {
@@ -429,7 +434,8 @@ void enqueue_training(gnn_model* m, int set) {
             // logits, cross-entropy and dA = dZ W^T in one CUDA-core pass (dense.cu k_last_layer)
             K(m, s, GNN_K_CE, [&] {
                 launch_last_layer(rows, (int)ly.m_cap, ly.A, ly.k_pad, ly.in, ly.in_pad, m->sage, m->params + ly.poff,
-                                  g->C, ly.n_pad, ly.H, ly.dPre, ly.dA, B.st, g->y, B.nodes, s);
+                                  g->C, ly.n_pad, ly.H, ly.dPre, ly.dA, B.st, g->y, B.nodes,
+                                  agg_in_last ? m->layers[li - 1].H : nullptr, B.rowptr[blk], B.col[blk], s);
             });
             break;
         }
@@ -1106,6 +1112,7 @@ gnn_status gnn_model_create(gnn_graph* g, const gnn_model_config* cfg, gnn_model
     m->bf16x3 = c.precision == GNN_FP32;
     m->full_train = !(m->sage && !m->shadow);
     { const char* e = std::getenv("GS_L1_ON_SAMPLER"); m->l1_on_sampler = !m->full_train && e && e[0] == '1'; }
+    { const char* e = std::getenv("GS_LAST_FUSED"); m->last_fused = e && e[0] == '1'; }
     auto cleanup = [&](gnn_status s) {
         for (void* p : m->owned) cudaFree(p);
         for (void* p : m->owned_host) cudaFreeHost(p);

@@ -1419,7 +1419,7 @@ void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bo
 // is ~1 wave of 128 blocks.  The weight gradient A^T dZ stays on the tensor cores (forked stream).
 // A is read from its split planes (hi + lo); W from the fp32 parameters (rows r of the [rows x C]
 // block: SAGE k -> (k / in_pad) * in + k % in_pad, GCN k -> k, zero beyond).
-constexpr int kLastRows = 8;   // rows (warps) per block
+constexpr int kLastRows = 8;   // rows per block (two warps each)
 struct LastArgs {
     const int32_t* m_ptr;      // rows of the layer (batch rows)
     Split A;                   // operand planes [rows x k_pad]
@@ -1432,44 +1432,104 @@ struct LastArgs {
     StepState* st;
     const int32_t* labels;
     const int32_t* nodes;
+    // SAGE + neighbour sampler: the layer's aggregation too (Hp = H_{L-1} [rows x in_pad] fp32,
+    // rowptr/col = the block of hop 0 over local ids): A = [H_self | mean] is gathered here, as
+    // k_agg_sage computes it (CSR-order adds, times 1/deg), and written to A's planes for the
+    // weight-gradient GEMM; null Hp: A is read from its planes
+    const float* Hp;
+    const int32_t* rowptr;
+    const int32_t* col;
 };
-__global__ void __launch_bounds__(kLastRows * 32) k_last_layer(LastArgs a) {
+__global__ void __launch_bounds__(kLastRows * 64) k_last_layer(LastArgs a) {
+    // two warps per row: warp h (= warp / kLastRows) takes half of the k range of the logits and
+    // of dA; the halves' logits are added in a fixed order (half 0 + half 1)
     extern __shared__ __align__(16) float lsm[];
     const int ldw = a.C | 1;
     float* Ws = lsm;                                    // [k_pad][ldw]
     float* As = lsm + (size_t)a.k_pad * ldw;            // [kLastRows][k_pad]
+    __shared__ float zpart[kLastRows][64];
+    __shared__ float dzs[kLastRows][64];
     __shared__ float wloss[kLastRows];
     __shared__ int is_last;
     const int warp = threadIdx.x >> 5, lane = lane_id();
-    for (int x = threadIdx.x; x < a.k_pad * a.C; x += blockDim.x) {   // W: independent of the predecessor
-        const int k = x / a.C, c = x % a.C;
+    const int rl = warp % kLastRows, half = warp / kLastRows;
+    // W -> shared memory by asynchronous 4-byte copies, a warp per k row (its parameter row
+    // computed once), lanes over the classes; independent of the predecessor kernel
+    for (int k = warp; k < a.k_pad; k += 2 * kLastRows) {
         int r = -1;
-        if (a.sage) { const int half = k / a.in_pad, j = k % a.in_pad; if (half < 2 && j < a.in) r = half * a.in + j; }
-        else if (k < a.in) r = k;
-        Ws[k * ldw + c] = r >= 0 ? __ldg(a.W + (int64_t)r * a.C + c) : 0.f;
+        if (a.sage) {
+            const int hh = k >= a.in_pad ? 1 : 0, j = k - hh * a.in_pad;
+            if (j < a.in) r = hh * a.in + j;
+        } else if (k < a.in) {
+            r = k;
+        }
+        for (int c = lane; c < a.C; c += 32) {
+            if (r >= 0)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(Ws + k * ldw + c)),
+                             "l"(a.W + (int64_t)r * a.C + c) : "memory");
+            else
+                Ws[k * ldw + c] = 0.f;
+        }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     pdl_trigger();
     pdl_wait();
     const int M = *a.m_ptr;
-    const int row = blockIdx.x * kLastRows + warp;
-    float* Ar = As + (size_t)warp * a.k_pad;
-    if (row < M)
-        for (int k = lane; k < a.k_pad; k += 32) {
+    const int row = blockIdx.x * kLastRows + rl;
+    float* Ar = As + (size_t)rl * a.k_pad;
+    if (a.Hp) {
+        if (row < M) {
+            const int beg = a.rowptr[row], end = a.rowptr[row + 1];
+            const float inv = end > beg ? 1.0f / (float)(end - beg) : 0.f;   // one division per row (R23)
+            const int nch = a.in_pad >> 2;
+            const float4* H4 = reinterpret_cast<const float4*>(a.Hp);
+            for (int ch = lane + 32 * half; ch < nch; ch += 64) {   // 16-byte chunks; adds in CSR order
+                const float4 sv = H4[(int64_t)row * nch + ch];
+                float4 acc = kZero4;
+                for (int e = beg; e < end; ++e) acc = f4add(acc, H4[(int64_t)__ldg(a.col + e) * nch + ch]);
+                const float4 mv = f4scale(acc, inv);
+                *reinterpret_cast<float4*>(Ar + 4 * ch) = sv;
+                *reinterpret_cast<float4*>(Ar + a.in_pad + 4 * ch) = mv;
+                store_split4(a.A, tix(a.A, row, 4 * ch), sv);
+                store_split4(a.A, tix(a.A, row, a.in_pad + 4 * ch), mv);
+            }
+        } else if (row < ((M + 63) & ~63)) {   // zero tail rows of the operand planes
+            for (int k = lane + 32 * half; k < a.k_pad; k += 64) store_split1(a.A, tix(a.A, row, k), 0.f);
+        }
+    } else if (row < M) {
+        for (int k = lane + 32 * half; k < a.k_pad; k += 64) {
             const int64_t ix = tix(a.A, row, k);
             Ar[k] = __bfloat162float(a.A.hi[ix]) + (a.A.lo ? __bfloat162float(a.A.lo[ix]) : 0.f);
         }
+    }
+    __syncthreads();
+    const int K2 = a.k_pad / 2;            // k_pad is a multiple of 8
+    const int kb = half * K2;
+    const int c0 = lane, c1 = lane + 32;
+    const bool v0 = c0 < a.C, v1 = c1 < a.C;
+    float z0 = 0.f, z1 = 0.f;
+    if (row < M) {
+        // this half's logits: four partial sums per class (k mod 4, k ascending), fixed-order total
+        float p0[4] = {0.f, 0.f, 0.f, 0.f}, p1[4] = {0.f, 0.f, 0.f, 0.f};
+        const float* w0 = Ws + (v0 ? c0 : 0);
+        const float* w1 = Ws + (v1 ? c1 : 0);
+#pragma unroll 2
+        for (int k = kb; k < kb + K2; k += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(Ar + k);
+            p0[0] = fmaf(x.x, w0[(k + 0) * ldw], p0[0]); p1[0] = fmaf(x.x, w1[(k + 0) * ldw], p1[0]);
+            p0[1] = fmaf(x.y, w0[(k + 1) * ldw], p0[1]); p1[1] = fmaf(x.y, w1[(k + 1) * ldw], p1[1]);
+            p0[2] = fmaf(x.z, w0[(k + 2) * ldw], p0[2]); p1[2] = fmaf(x.z, w1[(k + 2) * ldw], p1[2]);
+            p0[3] = fmaf(x.w, w0[(k + 3) * ldw], p0[3]); p1[3] = fmaf(x.w, w1[(k + 3) * ldw], p1[3]);
+        }
+        z0 = (p0[0] + p0[1]) + (p0[2] + p0[3]);
+        z1 = (p1[0] + p1[1]) + (p1[2] + p1[3]);
+        if (half == 1) { zpart[rl][c0] = z0; zpart[rl][c1] = z1; }
+    }
     __syncthreads();
     float l = 0.f;
-    if (row < M) {
-        // logits of classes lane and lane + 32 (k ascending)
-        const int c0 = lane, c1 = lane + 32;
-        const bool v0 = c0 < a.C, v1 = c1 < a.C;
-        float z0 = 0.f, z1 = 0.f;
-        for (int k = 0; k < a.k_pad; ++k) {
-            const float x = Ar[k];
-            if (v0) z0 = fmaf(x, Ws[k * ldw + c0], z0);
-            if (v1) z1 = fmaf(x, Ws[k * ldw + c1], z1);
-        }
+    if (row < M && half == 0) {
+        z0 = v0 ? z0 + zpart[rl][c0] : 0.f;
+        z1 = v1 ? z1 + zpart[rl][c1] : 0.f;
         if (v0) a.Z[(int64_t)row * a.n_pad + c0] = z0;
         if (v1) a.Z[(int64_t)row * a.n_pad + c1] = z1;
         // softmax cross-entropy of the row
@@ -1484,32 +1544,37 @@ __global__ void __launch_bounds__(kLastRows * 32) k_last_layer(LastArgs a) {
         const float inv_s = 1.0f / ssum, inv_bt = 1.0f / (float)max(a.st->b_total, 1);
         const float d0 = v0 ? (e0 * inv_s - (c0 == y ? 1.f : 0.f)) * inv_bt : 0.f;
         const float d1 = v1 ? (e1 * inv_s - (c1 == y ? 1.f : 0.f)) * inv_bt : 0.f;
+        dzs[rl][c0] = d0;
+        dzs[rl][c1] = d1;
         if (c0 < a.n_pad) store_split1(a.dz, tix(a.dz, row, c0), d0);
         if (c1 < a.n_pad) store_split1(a.dz, tix(a.dz, row, c1), d1);
-        // dA[row, k] = Σ_c dZ[row, c] W[k, c]  (c ascending), k = lane + 32 j
-        for (int k0 = 0; k0 < a.k_pad; k0 += 32 * 8) {
+    } else if (half == 0 && row >= M && row < ((M + 63) & ~63)) {   // zero tail rows of the dZ planes
+        for (int c = lane; c < a.n_pad; c += 32) store_split1(a.dz, tix(a.dz, row, c), 0.f);
+    }
+    __syncthreads();
+    if (row < M) {
+        // dA[row, k] = Σ_c dZ[row, c] W[k, c]  (c ascending), this half's k = kb + lane + 32 j
+        for (int k0 = kb; k0 < kb + K2; k0 += 32 * 8) {
             float acc[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = 0.f;
             for (int c = 0; c < a.C; ++c) {
-                const float dc = __shfl_sync(kFull, c < 32 ? d0 : d1, c & 31);
+                const float dc = dzs[rl][c];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int k = k0 + lane + 32 * j;
-                    if (k < a.k_pad) acc[j] = fmaf(dc, Ws[k * ldw + c], acc[j]);
+                    if (k < kb + K2) acc[j] = fmaf(dc, Ws[k * ldw + c], acc[j]);
                 }
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int k = k0 + lane + 32 * j;
-                if (k < a.k_pad) a.dA[(int64_t)row * a.k_pad + k] = acc[j];
+                if (k < kb + K2) a.dA[(int64_t)row * a.k_pad + k] = acc[j];
             }
         }
-    } else if (row < ((M + 63) & ~63)) {   // zero tail rows of the dZ planes (the wgrad reduction pads to 64)
-        for (int c = lane; c < a.n_pad; c += 32) store_split1(a.dz, tix(a.dz, row, c), 0.f);
     }
     // the loss: the block's rows in order, then the blocks in order by the last block to finish
-    if (lane == 0) wloss[warp] = l;
+    if (lane == 0 && half == 0) wloss[rl] = l;
     __syncthreads();
     if (threadIdx.x == 0) {
         float t = 0.f;
@@ -1530,7 +1595,8 @@ __global__ void __launch_bounds__(kLastRows * 32) k_last_layer(LastArgs a) {
 
 void launch_last_layer(const int32_t* m_ptr, int m_cap, Split A, int k_pad, int in, int in_pad, bool sage,
                        const float* W, int C, int n_pad, float* Z, Split dz, float* dA, StepState* st,
-                       const int32_t* labels, const int32_t* nodes, cudaStream_t s) {
+                       const int32_t* labels, const int32_t* nodes, const float* Hp, const int32_t* rowptr,
+                       const int32_t* col, cudaStream_t s) {
     const size_t smem = sizeof(float) * ((size_t)k_pad * (C | 1) + (size_t)kLastRows * k_pad);
     static size_t attr = 0;
     if (smem > attr) {
@@ -1538,12 +1604,12 @@ void launch_last_layer(const int32_t* m_ptr, int m_cap, Split A, int k_pad, int 
         attr = smem;
     }
     const int grid = (((m_cap + 63) & ~63) + kLastRows - 1) / kLastRows;
-    LastArgs a{m_ptr, A, k_pad, in, in_pad, sage ? 1 : 0, W, C, n_pad, Z, dz, dA, st, labels, nodes};
-    launch_pdl(k_last_layer, grid, kLastRows * 32, smem, s, a);
+    LastArgs a{m_ptr, A, k_pad, in, in_pad, sage ? 1 : 0, W, C, n_pad, Z, dz, dA, st, labels, nodes, Hp, rowptr, col};
+    launch_pdl(k_last_layer, grid, kLastRows * 64, smem, s, a);
 }
 
 bool last_layer_fits(int k_pad, int C) {
-    return C <= 64 && sizeof(float) * ((size_t)k_pad * (C | 1) + (size_t)kLastRows * k_pad) <= 200 * 1024;
+    return C <= 64 && k_pad % 8 == 0 && sizeof(float) * ((size_t)k_pad * (C | 1) + (size_t)kLastRows * k_pad) <= 200 * 1024;
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,

@@ -256,7 +256,10 @@ void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bo
 // [0, *m_ptr) of at most m_cap; W = the layer's fp32 parameter block [rows x C].
 void launch_last_layer(const int32_t* m_ptr, int m_cap, Split A, int k_pad, int in, int in_pad, bool sage,
                        const float* W, int C, int n_pad, float* Z, Split dz, float* dA, StepState* st,
-                       const int32_t* labels, const int32_t* nodes, cudaStream_t s);
+                       const int32_t* labels, const int32_t* nodes, const float* Hp, const int32_t* rowptr,
+                       const int32_t* col, cudaStream_t s);
+// (Hp non-null, SAGE: the layer's aggregation A = [H_self | mean] is gathered in the same kernel
+// from Hp [rows x in_pad] over the CSR block rowptr/col and written to A's planes.)
 bool last_layer_fits(int k_pad, int C);
 // Softmax CE over rows [0, batch_n): st->loss = Σ ℓ_i / b_total, dZ = (softmax-onehot)/b_total
 // written as split planes [rows x ldz] (+ zero tail rows).

@@ -433,3 +433,18 @@ def test_hub_row_beyond_block_sort():
     assert int(np.sum(want[1]["blk_nbr"] == 0)) > 8192      # node 0's transposed row at hop 1
     loss = m.train_minibatch(0, 0)
     check_train_step(m, w, graph, inp["params"].astype(np.float64), 0, 0, perm, loss)
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_gcn"])
+def test_tiny_epoch_last_layer_fused(name, monkeypatch):
+    """GS_LAST_FUSED=1 (the last layer on the CUDA cores; SAGE with its
+    aggregation in the same kernel): every step of an epoch within tolerance of the oracle."""
+    monkeypatch.setenv("GS_LAST_FUSED", "1")
+    w, inp, graph = inputs_for(name)
+    g, m = make_gpu(w, inp)
+    params = inp["params"].astype(np.float64)
+    perm = OS.epoch_perm(graph["train"], w.sampler_seed, 0)
+    for step in range(w.n_batches):
+        loss = m.train_minibatch(0, step)
+        params = check_train_step(m, w, graph, params, 0, step, perm, loss)["params"]
+    assert rel(m.get_params(), params) <= TOL_FP32

@@ -1,0 +1,7 @@
+#!/bin/bash
+out=gpurun_out/r3n; mkdir -p $out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m gpu -k "tiny_epoch or determinism" > $out/parity.log 2>&1; echo "rc=$?" >> $out/parity.log
+for v in 0 1; do
+  GS_LAST_FUSED=$v python bench.py --steps 300 --warmup 20 --no-cpu-baseline --epochs 2 >> $out/bench_products.json 2>>$out/err; echo "products fused=$v" >> $out/bench_products.tags
+done
+ncu --nvtx --nvtx-include "steps/" -k regex:k_last_layer --metrics gpu__time_duration.sum --cache-control none --clock-control none --csv --log-file $out/last.csv python tools/profile_step.py --config products --steps 3 --graph > $out/ncu.log 2>&1
