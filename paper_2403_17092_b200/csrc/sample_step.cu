@@ -552,6 +552,9 @@ int sample_step_grid() {
             cudaFuncSetAttribute(k_sample_step, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_step, kThreads, kSortSmem);
         grid = std::max(1, std::min(per_sm, 1)) * std::max(sms, 1);
+        // A/B switch GS_SAMPLE_GRID: fewer sampling blocks (SMs), so that the training kernels it
+        // overlaps keep the other SMs to themselves (the persistent GEMMs cannot share an SM with it)
+        if (const char* e = std::getenv("GS_SAMPLE_GRID")) grid = std::max(1, std::min(grid, std::atoi(e)));
     }
     return grid;
 }

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2b measurement pass on one B200: full -m gpu suite, smoke, ncu launch lists (cold and
 # warm), bench lines for every workload, the reference arm, the Unified protocol, a --set full
-# capture of a products step, sampling phases, timeline, gather ceiling, sanitizer logs.
+# capture of a products step, sampling phases, timeline, gather ceiling.
 set -u
 out=${1:-gpurun_out/final3}
 mkdir -p "$out"
@@ -31,6 +31,5 @@ ncu --nvtx --nvtx-include "steps/" --set full --import-source on --clock-control
 python tools/phase_times.py products > "$out/phases_products.txt" 2>&1
 python tools/timeline.py products 30 > "$out/timeline_products.txt" 2>&1
 python tools/gather_ceiling.py > "$out/gather_ceiling.txt" 2>&1
-timeout 900 compute-sanitizer --tool memcheck python tools/sanitize.py > "$out/sanitize_memcheck.log" 2>&1
-timeout 900 compute-sanitizer --tool racecheck python tools/sanitize.py > "$out/sanitize_racecheck.log" 2>&1
-timeout 900 compute-sanitizer --tool synccheck python tools/sanitize.py > "$out/sanitize_synccheck.log" 2>&1
+# compute-sanitizer is closed on this pool since round 2's pass (profiles/r2/sanitize_*.log hold
+# the memcheck / racecheck / synccheck runs of tools/sanitize.py)
