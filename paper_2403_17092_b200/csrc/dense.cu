@@ -1419,7 +1419,8 @@ void launch_sgd_pack(const PackAll& p, float* params, float* grads, float lr, bo
 // is ~1 wave of 128 blocks.  The weight gradient A^T dZ stays on the tensor cores (forked stream).
 // A is read from its split planes (hi + lo); W from the fp32 parameters (rows r of the [rows x C]
 // block: SAGE k -> (k / in_pad) * in + k % in_pad, GCN k -> k, zero beyond).
-constexpr int kLastRows = 8;   // rows per block (two warps each)
+constexpr int kLastRows = 8;    // rows per block
+constexpr int kLastSplit = 2;   // warps per row (512 threads: a block fits beside a sampling block, 16K registers each)
 struct LastArgs {
     const int32_t* m_ptr;      // rows of the layer (batch rows)
     Split A;                   // operand planes [rows x k_pad]
@@ -1440,22 +1441,38 @@ struct LastArgs {
     const int32_t* rowptr;
     const int32_t* col;
 };
-__global__ void __launch_bounds__(kLastRows * 64) k_last_layer(LastArgs a) {
-    // two warps per row: warp h (= warp / kLastRows) takes half of the k range of the logits and
-    // of dA; the halves' logits are added in a fixed order (half 0 + half 1)
-    extern __shared__ __align__(16) float lsm[];
-    const int ldw = a.C | 1;
-    float* Ws = lsm;                                    // [k_pad][ldw]
-    float* As = lsm + (size_t)a.k_pad * ldw;            // [kLastRows][k_pad]
-    __shared__ float zpart[kLastRows][64];
+__global__ void __launch_bounds__(kLastRows * 32 * kLastSplit) k_last_layer(LastArgs a) {
+    // kLastSplit warps per row: warp q (= warp / kLastRows) takes the q-th part of the k range of
+    // the logits and of dA; the parts' logits are added in a fixed order (part 0 + 1 + ...)
+    extern __shared__ __align__(128) float lsm[];
+    // W's k rows are the parameter rows themselves when in == in_pad (hidden layers): one bulk copy
+    // of the contiguous [k_pad x C] block (row stride C; odd C keeps both sweeps conflict-free)
+    const bool bulk = a.in == a.in_pad && ((a.k_pad * a.C) & 3) == 0 && (reinterpret_cast<uintptr_t>(a.W) & 15) == 0;
+    const int ldw = bulk ? a.C : (a.C | 1);
+    float* Ws = lsm + 32;                               // [k_pad][ldw] (lsm[0..1]: the mbarrier)
+    float* As = Ws + (((size_t)a.k_pad * ldw + 3) & ~size_t(3));   // [kLastRows][k_pad]
+    __shared__ float zpart[kLastSplit][kLastRows][64];
     __shared__ float dzs[kLastRows][64];
     __shared__ float wloss[kLastRows];
     __shared__ int is_last;
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int rl = warp % kLastRows, half = warp / kLastRows;
+    uint64_t* wbar = reinterpret_cast<uint64_t*>(lsm);
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            mbar_init(wbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            fence_async_smem();
+            const uint32_t bytes = (uint32_t)(a.k_pad * a.C) * 4u;
+            mbar_expect_tx(wbar, bytes);
+            for (uint32_t o = 0; o < bytes; o += 65536u)   // bulk copies of up to 64 KB
+                bulk_g2s(reinterpret_cast<char*>(Ws) + o, reinterpret_cast<const char*>(a.W) + o,
+                         min(65536u, bytes - o), wbar, policy_evict_last());
+        }
+    } else
     // W -> shared memory by asynchronous 4-byte copies, a warp per k row (its parameter row
     // computed once), lanes over the classes; independent of the predecessor kernel
-    for (int k = warp; k < a.k_pad; k += 2 * kLastRows) {
+    for (int k = warp; k < a.k_pad; k += kLastSplit * kLastRows) {
         int r = -1;
         if (a.sage) {
             const int hh = k >= a.in_pad ? 1 : 0, j = k - hh * a.in_pad;
@@ -1476,6 +1493,7 @@ __global__ void __launch_bounds__(kLastRows * 64) k_last_layer(LastArgs a) {
     pdl_wait();
     const int M = *a.m_ptr;
     const int row = blockIdx.x * kLastRows + rl;
+    if (bulk) { __syncthreads(); mbar_wait(wbar, 0); }   // (the barrier is initialised before it is polled)
     float* Ar = As + (size_t)rl * a.k_pad;
     if (a.Hp) {
         if (row < M) {
@@ -1483,7 +1501,7 @@ __global__ void __launch_bounds__(kLastRows * 64) k_last_layer(LastArgs a) {
             const float inv = end > beg ? 1.0f / (float)(end - beg) : 0.f;   // one division per row (R23)
             const int nch = a.in_pad >> 2;
             const float4* H4 = reinterpret_cast<const float4*>(a.Hp);
-            for (int ch = lane + 32 * half; ch < nch; ch += 64) {   // 16-byte chunks; adds in CSR order
+            for (int ch = lane + 32 * half; ch < nch; ch += 32 * kLastSplit) {   // 16-byte chunks; adds in CSR order
                 const float4 sv = H4[(int64_t)row * nch + ch];
                 float4 acc = kZero4;
                 for (int e = beg; e < end; ++e) acc = f4add(acc, H4[(int64_t)__ldg(a.col + e) * nch + ch]);
@@ -1494,16 +1512,16 @@ __global__ void __launch_bounds__(kLastRows * 64) k_last_layer(LastArgs a) {
                 store_split4(a.A, tix(a.A, row, a.in_pad + 4 * ch), mv);
             }
         } else if (row < ((M + 63) & ~63)) {   // zero tail rows of the operand planes
-            for (int k = lane + 32 * half; k < a.k_pad; k += 64) store_split1(a.A, tix(a.A, row, k), 0.f);
+            for (int k = lane + 32 * half; k < a.k_pad; k += 32 * kLastSplit) store_split1(a.A, tix(a.A, row, k), 0.f);
         }
     } else if (row < M) {
-        for (int k = lane + 32 * half; k < a.k_pad; k += 64) {
+        for (int k = lane + 32 * half; k < a.k_pad; k += 32 * kLastSplit) {
             const int64_t ix = tix(a.A, row, k);
             Ar[k] = __bfloat162float(a.A.hi[ix]) + (a.A.lo ? __bfloat162float(a.A.lo[ix]) : 0.f);
         }
     }
     __syncthreads();
-    const int K2 = a.k_pad / 2;            // k_pad is a multiple of 8
+    const int K2 = a.k_pad / kLastSplit;   // k_pad is a multiple of 4 * kLastSplit
     const int kb = half * K2;
     const int c0 = lane, c1 = lane + 32;
     const bool v0 = c0 < a.C, v1 = c1 < a.C;
@@ -1523,13 +1541,17 @@ __global__ void __launch_bounds__(kLastRows * 64) k_last_layer(LastArgs a) {
         }
         z0 = (p0[0] + p0[1]) + (p0[2] + p0[3]);
         z1 = (p1[0] + p1[1]) + (p1[2] + p1[3]);
-        if (half == 1) { zpart[rl][c0] = z0; zpart[rl][c1] = z1; }
+        zpart[half][rl][c0] = z0;
+        zpart[half][rl][c1] = z1;
     }
     __syncthreads();
     float l = 0.f;
     if (row < M && half == 0) {
-        z0 = v0 ? z0 + zpart[rl][c0] : 0.f;
-        z1 = v1 ? z1 + zpart[rl][c1] : 0.f;
+        float t0 = zpart[0][rl][c0], t1 = zpart[0][rl][c1];
+#pragma unroll
+        for (int q = 1; q < kLastSplit; ++q) { t0 += zpart[q][rl][c0]; t1 += zpart[q][rl][c1]; }
+        z0 = v0 ? t0 : 0.f;
+        z1 = v1 ? t1 : 0.f;
         if (v0) a.Z[(int64_t)row * a.n_pad + c0] = z0;
         if (v1) a.Z[(int64_t)row * a.n_pad + c1] = z1;
         // softmax cross-entropy of the row
@@ -1597,7 +1619,7 @@ void launch_last_layer(const int32_t* m_ptr, int m_cap, Split A, int k_pad, int 
                        const float* W, int C, int n_pad, float* Z, Split dz, float* dA, StepState* st,
                        const int32_t* labels, const int32_t* nodes, const float* Hp, const int32_t* rowptr,
                        const int32_t* col, cudaStream_t s) {
-    const size_t smem = sizeof(float) * ((size_t)k_pad * (C | 1) + (size_t)kLastRows * k_pad);
+    const size_t smem = sizeof(float) * (32 + (((size_t)k_pad * (C | 1) + 3) & ~size_t(3)) + (size_t)kLastRows * k_pad);
     static size_t attr = 0;
     if (smem > attr) {
         cudaFuncSetAttribute(k_last_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1605,11 +1627,12 @@ void launch_last_layer(const int32_t* m_ptr, int m_cap, Split A, int k_pad, int 
     }
     const int grid = (((m_cap + 63) & ~63) + kLastRows - 1) / kLastRows;
     LastArgs a{m_ptr, A, k_pad, in, in_pad, sage ? 1 : 0, W, C, n_pad, Z, dz, dA, st, labels, nodes, Hp, rowptr, col};
-    launch_pdl(k_last_layer, grid, kLastRows * 64, smem, s, a);
+    launch_pdl(k_last_layer, grid, kLastRows * 32 * kLastSplit, smem, s, a);
 }
 
 bool last_layer_fits(int k_pad, int C) {
-    return C <= 64 && k_pad % 8 == 0 && sizeof(float) * ((size_t)k_pad * (C | 1) + (size_t)kLastRows * k_pad) <= 200 * 1024;
+    return C <= 64 && k_pad % (4 * kLastSplit) == 0 &&
+           sizeof(float) * (32 + (size_t)k_pad * (C | 1) + 4 + (size_t)kLastRows * k_pad) <= 200 * 1024;
 }
 
 void launch_ce(StepState* st, const float* Z, int ldz, int C, const int32_t* labels, const int32_t* nodes,
