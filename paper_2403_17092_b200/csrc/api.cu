@@ -104,7 +104,7 @@ struct gnn_graph {
     bool stats_on = false;
     FeatRows rows() const {
         return FeatRows{X, nshards ? shard_ptrs : nullptr, rps, nshards ? cache_desc : nullptr,
-                        rps ? (int)(row_begin / rps) : 0};
+                        rps ? (int)(row_begin / rps) : 0, nshards ? 0 : N};
     }
 };
 

@@ -201,17 +201,38 @@ __global__ void GS_AGG_BOUNDS k_agg_sage(const int32_t* __restrict__ rows_ptr,
 // as split planes, and re-arms the buffer with row t+NB.
 // Memory-level parallelism: NB x (1 + k) rows per warp in flight (products: 2 x 16 rows of 400 B
 // = 12.8 KB per warp, ~200 KB per SM) against ~4 rows per warp for register loads.
+// G4 (the default; GS_L1_G4=0 for one bulk copy per row): the neighbour rows move four at a
+// time by the tensor engine's row gather (cp.async.bulk.tensor.2d...tile::gather4 over a
+// {in_pad x 1}-box map of X, SASS UTMALDG.2D.GATHER4), so a row of 15 neighbours costs 4 copy
+// instructions instead of 15; a buffer is then the self row (padded to 128 B) and groups of 4
+// rows (each 128-B aligned).  Products: 49 -> 43 µs per launch, 4210-4255 -> 4410-4630
+// mini-batches/s: the copy-issue rate, not the bytes, was part of the per-row latency.
 constexpr int kL1Warps = 4;   // warps per block
-template <int NB>
+__device__ __forceinline__ void gather4_g2s(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int r0, int r1,
+                                            int r2, int r3, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(pol)
+        : "memory");
+}
+template <int NB, bool G4>
 __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __restrict__ rows_ptr,
         const float* __restrict__ X, int in_pad, const int32_t* __restrict__ smap,
         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col, Split A, int fixed_k, int slots,
-        int xpol, int apol) {
+        int xpol, int apol, const __grid_constant__ CUtensorMap xmap) {
     extern __shared__ __align__(128) unsigned char l1_smem[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     uint64_t* bar = reinterpret_cast<uint64_t*>(l1_smem) + warp * NB;
     const uint32_t row_bytes = (uint32_t)in_pad * 4u;
-    float* ring = reinterpret_cast<float*>(l1_smem + 128 + (size_t)warp * NB * slots * row_bytes);
+    // buffer geometry: G4: self row (sb bytes) + groups of 4 rows (gs bytes each); else slots rows
+    const uint32_t sb = (row_bytes + 127u) & ~127u, gs = (4u * row_bytes + 127u) & ~127u;
+    const uint32_t buf_bytes = G4 ? sb + (uint32_t)((slots - 1 + 3) / 4) * gs : (uint32_t)slots * row_bytes;
+    float* ring = reinterpret_cast<float*>(l1_smem + 128 + (size_t)warp * NB * buf_bytes);
+    auto nbr_row = [&](const float* buf, int j) -> const float4* {   // neighbour j (0-based) of a buffer
+        if constexpr (G4) return reinterpret_cast<const float4*>(reinterpret_cast<const char*>(buf) + sb + (j >> 2) * gs + (j & 3) * row_bytes);
+        else return reinterpret_cast<const float4*>(buf + (size_t)(j + 1) * in_pad);
+    };
     if (lane == 0) {
 #pragma unroll
         for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
@@ -250,15 +271,30 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
         x.self = smap ? smap[i] : i;
         return x;
     };
-    // arm buffer b with a row: self row -> slot 0, neighbour j -> slot 1 + j
+    // arm buffer b with a row: self row -> slot 0, neighbour j -> slot 1 + j (G4: group j / 4)
     auto issue = [&](int b, const Idx& x) {
-        float* buf = ring + (size_t)b * slots * in_pad;
-        if (lane == 0) mbar_expect_tx(&bar[b], (uint32_t)(x.c + 1) * row_bytes);
-        __syncwarp();
-        const int src = __shfl_up_sync(0xffffffffu, x.nb, 1);   // lane j (>= 1) takes neighbour j-1
-        if (lane <= x.c) {
-            const int r = lane == 0 ? x.self : src;
-            bulk_g2s(buf + (size_t)lane * in_pad, X + (int64_t)r * in_pad, row_bytes, &bar[b], pol);
+        float* buf = reinterpret_cast<float*>(reinterpret_cast<char*>(ring) + (size_t)b * buf_bytes);
+        if constexpr (G4) {
+            const int ng = (x.c + 3) >> 2;
+            const int gl = max(lane - 1, 0);   // lane 1 + g issues group g: neighbours 4g .. 4g+3
+            const int lim = max(x.c - 1, 0);   // a short last group repeats its last row (not summed)
+            const int r0 = __shfl_sync(0xffffffffu, x.nb, min(4 * gl + 0, lim) & 31);
+            const int r1 = __shfl_sync(0xffffffffu, x.nb, min(4 * gl + 1, lim) & 31);
+            const int r2 = __shfl_sync(0xffffffffu, x.nb, min(4 * gl + 2, lim) & 31);
+            const int r3 = __shfl_sync(0xffffffffu, x.nb, min(4 * gl + 3, lim) & 31);
+            if (lane == 0) mbar_expect_tx(&bar[b], row_bytes + (uint32_t)ng * 4u * row_bytes);
+            __syncwarp();
+            if (lane == 0) bulk_g2s(buf, X + (int64_t)x.self * in_pad, row_bytes, &bar[b], pol);
+            else if (lane <= ng)
+                gather4_g2s(reinterpret_cast<char*>(buf) + sb + gl * gs, &xmap, &bar[b], 0, r0, r1, r2, r3, pol);
+        } else {
+            if (lane == 0) mbar_expect_tx(&bar[b], (uint32_t)(x.c + 1) * row_bytes);
+            __syncwarp();
+            const int src = __shfl_up_sync(0xffffffffu, x.nb, 1);   // lane j (>= 1) takes neighbour j-1
+            if (lane <= x.c) {
+                const int r = lane == 0 ? x.self : src;
+                bulk_g2s(buf + (size_t)lane * in_pad, X + (int64_t)r * in_pad, row_bytes, &bar[b], pol);
+            }
         }
     };
     int cnt[NB];
@@ -275,21 +311,21 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_agg_l1_bulk(const int32_t* __
     for (int64_t i = gw; i < n; i += W) {
         const Idx nxt = fetch(i + (int64_t)(NB + 1) * W);   // loads in flight during this row
         mbar_wait(&bar[b], phase);
-        const float* buf = ring + (size_t)b * slots * in_pad;
+        const float* buf = reinterpret_cast<const float*>(reinterpret_cast<const char*>(ring) + (size_t)b * buf_bytes);
         int c = cnt[0];
 #pragma unroll
         for (int q = 1; q < NB; ++q) if (b == q) c = cnt[q];
         float4 sv = kZero4, acc = kZero4;
         if (lane < nch) {
             sv = reinterpret_cast<const float4*>(buf)[lane];
-            for (int j = 1; j <= c; ++j) acc = f4add(acc, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane]);
+            for (int j = 0; j < c; ++j) acc = f4add(acc, nbr_row(buf, j)[lane]);
         }
         // rows of more than 128 floats: lanes take further chunks
         float4 sv2 = kZero4, acc2 = kZero4;
         const bool wide = nch > 32;
         if (wide && lane + 32 < nch) {
             sv2 = reinterpret_cast<const float4*>(buf)[lane + 32];
-            for (int j = 1; j <= c; ++j) acc2 = f4add(acc2, reinterpret_cast<const float4*>(buf + (size_t)j * in_pad)[lane + 32]);
+            for (int j = 0; j < c; ++j) acc2 = f4add(acc2, nbr_row(buf, j)[lane + 32]);
         }
         // the buffer is read: re-arm it with this warp's row i + NB*W (async-proxy writes after
         // generic-proxy reads of the same shared memory need the proxy fence)
@@ -1191,11 +1227,13 @@ static bool force_sh() {
     if ((H).shards || force_sh()) { GS_CPL_DISPATCH_SH(cpl, true, KERNEL, __VA_ARGS__) }   \
     else { GS_CPL_DISPATCH_SH(cpl, false, KERNEL, __VA_ARGS__) }
 
-template <int NB>
+template <int NB, bool G4 = false>
 static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, const int32_t* smap,
                            const int32_t* blk_rowptr, const int32_t* col, Split A, int fixed_k, int slots,
-                           cudaStream_t s) {
-    size_t smem = 128 + (size_t)kL1Warps * NB * slots * in_pad * 4;
+                           cudaStream_t s, const CUtensorMap* xmap = nullptr) {
+    const size_t rb = (size_t)in_pad * 4, sb = (rb + 127) & ~size_t(127), gsz = (4 * rb + 127) & ~size_t(127);
+    const size_t buf = G4 ? sb + (size_t)((slots - 1 + 3) / 4) * gsz : (size_t)slots * rb;
+    size_t smem = 128 + (size_t)kL1Warps * NB * buf;
     if (smem > 200 * 1024) return false;
     // GS_L1_BPS = b: pad the request just past the (b+1)-blocks threshold, so that at most b blocks
     // share an SM and the rest of its shared memory stays free for a co-resident sampling block
@@ -1204,17 +1242,17 @@ static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, 
     static std::map<size_t, int> grids;   // smem bytes -> co-resident blocks x SMs (occupancy-derived)
     int& grid = grids[smem];
     if (!grid) {
-        cudaFuncSetAttribute(k_agg_l1_bulk<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_agg_l1_bulk<NB, G4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // the SMs this kernel runs on are configured with the whole 228 KB as shared memory, so a
         // block of the next batch's sampling kernel (35 KB) still fits beside the 3 gather blocks
         // (the driver otherwise picks the smallest split that holds them, 200 KB, and the sampling
         // kernel, which overlaps training, cannot co-reside: measured -12 % mini-batches/s)
         static const int carve = [] { const char* e = std::getenv("GS_L1_CARVE"); return e ? std::atoi(e) : 100; }();
-        if (carve >= 0) cudaFuncSetAttribute(k_agg_l1_bulk<NB>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+        if (carve >= 0) cudaFuncSetAttribute(k_agg_l1_bulk<NB, G4>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         int per_sm = 0, dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_l1_bulk<NB>, kL1Warps * 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_l1_bulk<NB, G4>, kL1Warps * 32, smem);
         if (per_sm < 1) return false;
         grid = per_sm * sms;
     }
@@ -1222,13 +1260,13 @@ static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, 
     static const int apol = [] { const char* e = std::getenv("GS_L1_APOL"); return e ? std::atoi(e) : 0; }();
     static const int pdl = [] { const char* e = std::getenv("GS_L1_PDL"); return e ? std::atoi(e) : 1; }();
     if (pdl)
-        launch_pdl(k_agg_l1_bulk<NB>, grid, kL1Warps * 32, smem, s, rows_ptr, X, in_pad, smap, blk_rowptr, col, A,
-                   fixed_k, slots, xpol, apol);
+        launch_pdl(k_agg_l1_bulk<NB, G4>, grid, kL1Warps * 32, smem, s, rows_ptr, X, in_pad, smap, blk_rowptr, col, A,
+                   fixed_k, slots, xpol, apol, xmap ? *xmap : CUtensorMap{});
     else
     {
-        apply_carveout((const void*)k_agg_l1_bulk<NB>);
-        k_agg_l1_bulk<NB><<<grid, kL1Warps * 32, smem, s>>>(rows_ptr, X, in_pad, smap, blk_rowptr, col, A, fixed_k,
-                                                           slots, xpol, apol);
+        apply_carveout((const void*)k_agg_l1_bulk<NB, G4>);
+        k_agg_l1_bulk<NB, G4><<<grid, kL1Warps * 32, smem, s>>>(rows_ptr, X, in_pad, smap, blk_rowptr, col, A, fixed_k,
+                                                               slots, xpol, apol, xmap ? *xmap : CUtensorMap{});
     }
     return true;
 }
@@ -1265,6 +1303,21 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
     static const int nb = [] { const char* e = std::getenv("GS_L1_NB"); return e ? std::atoi(e) : 2; }();
     // GS_AGG_BULK_ALL=1 (A/B): the later layers' aggregations (local H rows, self row = i) too
     static const int bulk_all = [] { const char* e = std::getenv("GS_AGG_BULK_ALL"); return e ? std::atoi(e) : 0; }();
+    // the row-gather variant (measured: products gather 49 -> 43 µs, 0.47 -> 0.53 of HBM; papers100M
+    // rows of 512 B unchanged); GS_L1_G4=0: one bulk copy per row
+    static const int g4 = [] { const char* e = std::getenv("GS_L1_G4"); return e ? std::atoi(e) : 1; }();
+    if (g4 && bulk && !H.shards && !gmap && smap && k_max > 0 && k_max <= 31 && in_pad <= 256 && (in_pad * 4) % 16 == 0) {
+        // the tensor map of X (rows of in_pad floats, box {in_pad, 1}), one per table
+        static std::map<const float*, CUtensorMap> maps;
+        auto it = maps.find(H.base);
+        if (it == maps.end()) {
+            CUtensorMap mp;
+            if (H.nrows > 0 && make_tmap_rows_f32(&mp, H.base, H.nrows, in_pad)) it = maps.emplace(H.base, mp).first;
+        }
+        if (it != maps.end() &&
+            launch_l1_bulk<2, true>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, 1 + k_max, s, &it->second))
+            return;
+    }
     if (bulk && !H.shards && !gmap && (smap || bulk_all) && k_max > 0 && k_max <= 31 && in_pad * 4 <= 1024) {
         const bool ok = nb == 3 ? launch_l1_bulk<3>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k,
                                                      1 + k_max, s)

@@ -578,6 +578,18 @@ bool make_tmap_bf16_tiled(CUtensorMap* map, const void* base, int64_t rows, int6
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_tmap_rows_f32(CUtensorMap* map, const float* base, int64_t rows, int cols) {
+    EncodeFn fn = encode_fn();
+    if (!fn || !base || cols > 256 || (cols * 4) % 16 != 0) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    cuuint32_t box[2] = {(cuuint32_t)cols, 1u};
+    cuuint32_t estr[2] = {1u, 1u};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // fp32 [depth x rows x cols] (cols contiguous, row stride ld elements, depth stride dstride
 // elements), box {32, 32, 1}, 128B swizzle: the GEMM epilogue's store target.
 bool make_tmap_f32(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int64_t depth,

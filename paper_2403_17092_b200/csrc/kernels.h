@@ -134,6 +134,7 @@ struct FeatRows {
     int64_t rps;
     const FeatCache* cache;   // sharded tables only (allocated with the graph: never null then)
     int own;                  // this process's shard
+    int64_t nrows = 0;        // rows of base (0: unknown)
     __device__ __forceinline__ void count(int which) const {
         unsigned long long* st = cache->stats;
         if (st && (threadIdx.x & 31) == 0) atomicAdd(st + which, 1ull);
@@ -282,6 +283,9 @@ void launch_init_params(float* p, int64_t cnt, float bound, uint64_t seed, uint3
 struct TcGemmMaps { CUtensorMap a_hi, a_lo, b_hi, b_lo, c; int* sched = nullptr; };
 // 2-D bf16 row-major [rows x cols], box {64 cols, box_rows}, 128B swizzle, OOB reads -> 0.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
+// fp32 rows [rows x cols] (cols contiguous, no padding between rows), box {cols, 1}, no swizzle:
+// the row-gather (tile::gather4) map of a feature table (cols <= 256, cols * 4 a multiple of 16).
+bool make_tmap_rows_f32(CUtensorMap* map, const float* base, int64_t rows, int cols);
 // k-block-tiled bf16 plane (Split layout, `rows` rows, `cols` columns): 3-D map {64, rows,
 // ceil(cols/64)}, box {64, box_rows, 1}, 128B swizzle.
 bool make_tmap_bf16_tiled(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
