@@ -399,7 +399,8 @@ void enqueue_training(gnn_model* m, int set) {
         const int blk = ly.blk;
         const int32_t* rows = rows_ptr(m, set, li);
         // layer 1 reads the feature table (local or row-sharded over peers); later layers H_{l-1}
-        const FeatRows Hrows = li == 0 ? g->rows() : FeatRows{m->layers[li - 1].H, nullptr, 0};
+        const FeatRows Hrows = li == 0 ? g->rows()
+                                       : FeatRows{m->layers[li - 1].H, nullptr, 0, nullptr, 0, m->layers[li - 1].m_cap};
         const int kid = li == 0 ? GNN_K_AGG_L1 : GNN_K_AGG;
         const int32_t* self_ids = li == 0 ? B.nodes : nullptr;
         // the last layer of SAGE + neighbour gathers its A inside k_last_layer (no aggregation launch)

@@ -1306,7 +1306,10 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
     // the row-gather variant (measured: products gather 49 -> 43 µs, 0.47 -> 0.53 of HBM; papers100M
     // rows of 512 B unchanged); GS_L1_G4=0: one bulk copy per row
     static const int g4 = [] { const char* e = std::getenv("GS_L1_G4"); return e ? std::atoi(e) : 1; }();
-    if (g4 && bulk && !H.shards && !gmap && smap && k_max > 0 && k_max <= 31 && in_pad <= 256 && (in_pad * 4) % 16 == 0) {
+    // GS_AGG_G4=1 (A/B): the later layers' aggregations (local H rows, self row = i) by the row gather too
+    static const int g4_all = [] { const char* e = std::getenv("GS_AGG_G4"); return e ? std::atoi(e) : 0; }();
+    if (g4 && bulk && !H.shards && !gmap && (smap || g4_all) && k_max > 0 && k_max <= 31 && in_pad <= 256 &&
+        (in_pad * 4) % 16 == 0) {
         // the tensor map of X (rows of in_pad floats, box {in_pad, 1}), one per table
         static std::map<const float*, CUtensorMap> maps;
         auto it = maps.find(H.base);
