@@ -6,6 +6,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cstdlib>
 #include <map>
+#include <tuple>
 
 #include "kernels.h"
 #include "tma.cuh"
@@ -1310,12 +1311,14 @@ void launch_agg_sage(const int32_t* rows_ptr, FeatRows H, int in_pad, const int3
     static const int g4_all = [] { const char* e = std::getenv("GS_AGG_G4"); return e ? std::atoi(e) : 0; }();
     if (g4 && bulk && !H.shards && !gmap && (smap || g4_all) && k_max > 0 && k_max <= 31 && in_pad <= 256 &&
         (in_pad * 4) % 16 == 0) {
-        // the tensor map of X (rows of in_pad floats, box {in_pad, 1}), one per table
-        static std::map<const float*, CUtensorMap> maps;
-        auto it = maps.find(H.base);
+        // the tensor map of X (rows of in_pad floats, box {in_pad, 1}), one per table: keyed by base,
+        // rows and width (a freed table's address can come back with another shape)
+        static std::map<std::tuple<const float*, int64_t, int>, CUtensorMap> maps;
+        const auto key = std::make_tuple(H.base, H.nrows, in_pad);
+        auto it = maps.find(key);
         if (it == maps.end()) {
             CUtensorMap mp;
-            if (H.nrows > 0 && make_tmap_rows_f32(&mp, H.base, H.nrows, in_pad)) it = maps.emplace(H.base, mp).first;
+            if (H.nrows > 0 && make_tmap_rows_f32(&mp, H.base, H.nrows, in_pad)) it = maps.emplace(key, mp).first;
         }
         if (it != maps.end() &&
             launch_l1_bulk<2, true>(rows_ptr, H.base, in_pad, smap, blk_rowptr, col, A, fixed_k, 1 + k_max, s, &it->second))
