@@ -1241,9 +1241,15 @@ static bool launch_l1_bulk(const int32_t* rows_ptr, const float* X, int in_pad, 
     static const int bps = [] { const char* e = std::getenv("GS_L1_BPS"); return e ? std::atoi(e) : 3; }();
     if (bps > 0) smem = std::max(smem, (size_t)(233472 / (bps + 1) - 1024 + 16));
     static std::map<size_t, int> grids;   // smem bytes -> co-resident blocks x SMs (occupancy-derived)
+    // the function's dynamic shared-memory limit only grows: tables of several widths share the
+    // kernel (a smaller request set later must not lower the limit a cached grid relies on)
+    static size_t attr_max = 0;
+    if (smem > attr_max) {
+        cudaFuncSetAttribute(k_agg_l1_bulk<NB, G4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_max = smem;
+    }
     int& grid = grids[smem];
     if (!grid) {
-        cudaFuncSetAttribute(k_agg_l1_bulk<NB, G4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // the SMs this kernel runs on are configured with the whole 228 KB as shared memory, so a
         // block of the next batch's sampling kernel (35 KB) still fits beside the 3 gather blocks
         // (the driver otherwise picks the smallest split that holds them, 200 KB, and the sampling
@@ -1279,9 +1285,13 @@ static bool launch_l1_stream(const int32_t* rows_ptr, const float* X, int in_pad
     const int G = std::max(2, std::min(16, 155000 / (kL1Warps * NB * in_pad * 4)));
     const size_t smem = 128 + (size_t)kL1Warps * NB * G * in_pad * 4;
     static std::map<size_t, int> grids;
+    static size_t attr_max = 0;   // only grows (see launch_l1_bulk)
+    if (smem > attr_max) {
+        cudaFuncSetAttribute(k_agg_l1_stream<NB, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_max = smem;
+    }
     int& grid = grids[smem];
     if (!grid) {
-        cudaFuncSetAttribute(k_agg_l1_stream<NB, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_agg_l1_stream<NB, CPL>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         int per_sm = 0, dev = 0, sms = 0;
         cudaGetDevice(&dev);
