@@ -152,6 +152,7 @@ struct GemmArgs {
     int mask_ld;
     int diag;               // profiling diagnostics only (env GS_GEMM_DIAG): 1 skip C stores, 2 skip MMAs, 4 skip loads, 8 skip the CE epilogue, 16 skip the loss sum
     int* sched;             // {next tile, CTAs done}: the dynamic tile scheduler (null: static tiles)
+    int clc;                // 1: one CTA per tile, idle CTAs steal pending CTAs' tiles (cluster launch control)
 };
 constexpr int kTileRing = 4;   // tile indices the scheduler may publish ahead of the epilogue
 
@@ -252,6 +253,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
     __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
     __shared__ uint64_t ring_full[kTileRing], ring_empty[kTileRing];
     __shared__ int ring_tile[kTileRing];
+    __shared__ __align__(16) uint4 clc_resp;   // the try_cancel response (16 bytes)
+    __shared__ uint64_t clc_bar;
     __shared__ uint32_t tmem_base_sh;
     __shared__ int ce_last;
     __shared__ float ce_warp[2][4];   // MODE 3: per-tile sums of the 4 epilogue warps (double buffered)
@@ -266,6 +269,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
         for (int r = 0; r < kTileRing; ++r) { mbar_init(&ring_full[r], 1); mbar_init(&ring_empty[r], 5); }
+        mbar_init(&clc_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -285,7 +289,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                                  : ((args.m_static + kBM - 1) / kBM) * args.n_tiles * args.splits;
     const int t_first = (int)blockIdx.x, t_step = (int)gridDim.x;
     // the j-th tile of this CTA: published by the producer (dynamic) or blockIdx + j * gridDim
-    const bool dyn = args.sched != nullptr;
+    const bool dyn = args.sched != nullptr || args.clc;
     auto next_tile = [&](int j) -> int {   // consumers (MMA thread, epilogue warps)
         if (!dyn) return t_first + j * t_step;
         const int r = j % kTileRing;
@@ -301,9 +305,22 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         // ================= TMA producer
         if (lane == 0) {
             int it = 0;
+            int clc_t = (int)blockIdx.x;      // CLC: this CTA's own tile first, then stolen ones
+            uint32_t clc_phase = 0;
             for (int jt = 0;; ++jt) {
                 int t;
-                if (dyn) {   // claim a tile and publish it to the consumers
+                if (args.clc) {   // publish the tile; ask for a pending CTA's tile while this one loads
+                    const int r = jt % kTileRing;
+                    if (jt >= kTileRing) mbar_wait(&ring_empty[r], ((jt / kTileRing) - 1) & 1);
+                    t = clc_t;
+                    const bool valid = t >= 0 && t < ntiles;
+                    ring_tile[r] = valid ? t : -1;
+                    mbar_arrive(&ring_full[r]);
+                    if (!valid) break;
+                    mbar_expect_tx(&clc_bar, 16u);
+                    asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];"
+                                 ::"r"(smem_u32(&clc_resp)), "r"(smem_u32(&clc_bar)) : "memory");
+                } else if (dyn) {   // claim a tile and publish it to the consumers
                     const int r = jt % kTileRing;
                     if (jt >= kTileRing) mbar_wait(&ring_empty[r], ((jt / kTileRing) - 1) & 1);
                     t = atomicAdd(args.sched, 1);
@@ -355,6 +372,19 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
                             if (TERMS == 3) tma_load_2d(b_lo + j * 8192, &mB_lo, &full_bar[s], tile_n + 64 * j, k0);
                         }
                     }
+                }
+                if (args.clc) {   // the stolen CTA's index is the next tile (none left: stop)
+                    mbar_wait(&clc_bar, clc_phase);
+                    clc_phase ^= 1u;
+                    uint32_t cx = 0, ok = 0;
+                    asm volatile(
+                        "{\n\t.reg .pred p1;\n\t.reg .b128 r;\n\t"
+                        "ld.shared.b128 r, [%2];\n\t"
+                        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p1, r;\n\t"
+                        "selp.u32 %1, 1, 0, p1;\n\t"
+                        "@p1 clusterlaunchcontrol.query_cancel.get_first_ctaid.v4.b32.b128 {%0, _, _, _}, r;\n\t}"
+                        : "=r"(cx), "=r"(ok) : "r"(smem_u32(&clc_resp)) : "memory");
+                    clc_t = ok ? (int)cx : -1;
                 }
             }
         }
@@ -508,7 +538,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUt
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
     }
-    if (dyn && threadIdx.x == 0) {
+    if (args.sched && !args.clc && threadIdx.x == 0) {
         // every CTA has claimed its last (past-the-end) tile: the last one to finish re-arms the
         // counter for the next launch from this site
         __threadfence();   // this CTA's claims precede its "done" in every observer's view
@@ -660,6 +690,15 @@ bool dyn_sched() {
     return d;
 }
 
+// GS_GEMM_CLC=1 (A/B): a grid of one CTA per tile of the worst case; a CTA that finished its tile
+// cancels a CTA the hardware has not launched yet (clusterlaunchcontrol.try_cancel) and computes
+// that CTA's tile, so the GEMM finishes on the SMs it got (the others may be held by the
+// overlapped sampling kernel) instead of waiting for a fixed share of tiles on every SM
+bool clc_sched() {
+    static const bool d = [] { const char* e = getenv("GS_GEMM_CLC"); return e && e[0] == '1'; }();
+    return d;
+}
+
 static int gemm_diag() {
     static int d = -1;
     if (d < 0) {
@@ -690,10 +729,11 @@ cudaError_t launch_gemm_tc(int mode, bool bf16x3, const TcGemmMaps& maps, const 
     a.split_stride = split_stride;
     a.diag = gemm_diag();
     a.sched = dyn_sched() ? maps.sched : nullptr;
+    a.clc = clc_sched() ? 1 : 0;
     int tiles_cap;
     if (mode != 1) tiles_cap = a.m_tiles_cap * a.n_tiles;
     else tiles_cap = ((m_static + kBM - 1) / kBM) * a.n_tiles * splits;
-    const int grid = std::max(1, std::min(kSMs, tiles_cap));
+    const int grid = a.clc ? std::max(1, tiles_cap) : std::max(1, std::min(kSMs, tiles_cap));
     if (mode == 0) return bf16x3 ? dispatch_bn<3, 0>(bn, grid, maps, a, s) : dispatch_bn<1, 0>(bn, grid, maps, a, s);
     if (mode == 2) return bf16x3 ? dispatch_bn<3, 2>(bn, grid, maps, a, s) : dispatch_bn<1, 2>(bn, grid, maps, a, s);
     return bf16x3 ? dispatch_bn<3, 1>(bn, grid, maps, a, s) : dispatch_bn<1, 1>(bn, grid, maps, a, s);
